@@ -1,0 +1,208 @@
+/*
+ * skx.h -- C-ABI of the B200-native skew-aware repositioning index and the
+ * operators it accelerates (libskx.so, built from paper_1910_10063_b200/csrc).
+ *
+ * This is the drop-in boundary for the reference library "skewdx"
+ * (/root/reference/proj).  The reference exposes its hot path two ways:
+ *   (1) the C function-pointer plugin table skewdx::kernels::KernelTable
+ *       (proj/include/skewdx/kernels.hpp:16-41), and
+ *   (2) the C++ operator API in permindex.hpp:34-59, operators.hpp:57-122 and
+ *       parallel.hpp:34-61.
+ * Each entry below names the reference interface it replaces.  Plain
+ * pointers and sizes only; no torch or C++ types cross this boundary.
+ *
+ * Conventions
+ *  - Identifiers are 1-based; id 0 and id > D are domain violations
+ *    (operators.cpp:33-38: `fact[k] - 1 >= D` in u32 arithmetic).
+ *  - Device entry points take DEVICE pointers and a cudaStream_t passed as
+ *    `void* stream` (NULL = legacy default stream).  They are asynchronous:
+ *    they enqueue work and return SKX_OK unless an argument is rejected on
+ *    the host.  Device-detected errors (domain violations, a frequency profile
+ *    whose counts do not sum to its total) are recorded in the context and
+ *    reported by the next skx_sync() on that context -- the first offending
+ *    row, exactly as DomainViolation::row() reports it (error.hpp:20-33).
+ *    Enqueue one operator and skx_sync() to attribute an error to it; the
+ *    C++ drop-in (skewdx_b200.hpp) does exactly that and rethrows the
+ *    reference's exception types.
+ *  - A context belongs to one device and one host thread; operators issued on
+ *    one context must be ordered on one stream (the context owns scratch).
+ *    Callers own every input and output buffer.
+ *  - Host-buffer entry points (suffix _host) copy host -> device, run the
+ *    kernel and copy back, pipelined in chunks over two streams; they are
+ *    synchronous and report errors directly.
+ */
+#ifndef SKX_H_
+#define SKX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes (mirror error.hpp:12-49). */
+#define SKX_OK 0
+#define SKX_INVALID_ARGUMENT 1 /* skewdx::InvalidArgument */
+#define SKX_DOMAIN_VIOLATION 2 /* skewdx::DomainViolation{row, value, domain} */
+#define SKX_CUDA_ERROR 3
+#define SKX_ERROR 5 /* any other skewdx::Error */
+
+/* kMaxDomainCardinality, column.hpp:17 */
+#define SKX_MAX_DOMAIN_CARDINALITY 0xFFFFFFFEu
+
+typedef struct skx_ctx skx_ctx;
+
+typedef struct skx_error_info {
+  int32_t status;
+  uint64_t row;    /* DomainViolation::row()   */
+  uint32_t value;  /* DomainViolation::value() */
+  uint64_t domain; /* the D the row was checked against */
+  char message[256];
+} skx_error_info;
+
+/* ---- context ------------------------------------------------------------ */
+int skx_version(void);
+int skx_ctx_create(int device, skx_ctx** out);
+int skx_ctx_destroy(skx_ctx* ctx);
+/* Waits for `stream`, then reports (and clears) any deferred device error. */
+int skx_sync(skx_ctx* ctx, void* stream);
+/* Details of the last non-OK status returned on this context. */
+int skx_last_error(const skx_ctx* ctx, skx_error_info* info);
+/* Number of kernels this context has launched since creation (bench evidence). */
+uint64_t skx_launch_count(const skx_ctx* ctx);
+
+/* ---- Q1 gather: out[k] = dim[fact[k]-1] --------------------------------- *
+ * Replaces KernelTable::gather_u32 (kernels.hpp:21-23; scalar.cpp:13-29,
+ * avx2.cpp:43-57) and the operator materialize() (operators.cpp:60-66) /
+ * parallel_materialize() (parallel.cpp:87-100), with the domain check of
+ * find_domain_violation (operators.cpp:32-41) fused into the same pass.
+ * Unlike the table entry it carries dim_len, so the device can bound-check.
+ * u16/u64 widths restate the same contract for BASELINE's int16/int64/f32
+ * value columns (bit moves; f32 and i32 go through _u32). */
+int skx_gather_u16(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uint16_t* dim,
+                   uint64_t dim_len, uint16_t* out, void* stream);
+int skx_gather_u32(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uint32_t* dim,
+                   uint64_t dim_len, uint32_t* out, void* stream);
+int skx_gather_u64(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uint64_t* dim,
+                   uint64_t dim_len, uint64_t* out, void* stream);
+
+/* ---- index build (permindex.cpp) ---------------------------------------- */
+/* count_frequencies (permindex.cpp:18-30): counts[id-1] = #rows with id.
+ * `counts` (u64[d]) is overwritten. */
+int skx_count_frequencies(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint32_t d,
+                          uint64_t* counts, void* stream);
+/* Same histogram into u32 counters (the per-GPU partial that is NCCL
+ * all-reduced before the sort, BASELINE config 4).  accumulate != 0 adds to
+ * the existing counters instead of overwriting them. */
+int skx_histogram_u32(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint32_t d,
+                      uint32_t* counts, int accumulate, void* stream);
+/* build_index (permindex.cpp:32-58): offsets = ids ordered by (count desc,
+ * id asc), zero-count ids last in ascending order; ranks = inverse
+ * (ranks[offsets[r]-1] = r+1).  Counts must sum to `total` (deferred
+ * SKX_INVALID_ARGUMENT otherwise, permindex.cpp:36-40). */
+int skx_build_index(skx_ctx* ctx, const uint64_t* counts, uint32_t d, uint64_t total,
+                    uint32_t* offsets, uint32_t* ranks, void* stream);
+int skx_build_index_u32(skx_ctx* ctx, const uint32_t* counts, uint32_t d, uint64_t total,
+                        uint32_t* offsets, uint32_t* ranks, void* stream);
+/* rebuild (permindex.cpp:86-88) = count_frequencies + build_index. */
+int skx_rebuild(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint32_t d, uint32_t* offsets,
+                uint32_t* ranks, void* stream);
+/* recode_fact (permindex.cpp:60-64): out[k] = ranks[fact[k]-1]. */
+int skx_recode_fact(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uint32_t* ranks,
+                    uint32_t d, uint32_t* out, void* stream);
+/* permute_dimension (permindex.cpp:66-73): out[r] = dim[offsets[r]-1];
+ * dim_len must equal d (SKX_INVALID_ARGUMENT otherwise). */
+int skx_permute_dimension_u16(skx_ctx* ctx, const uint16_t* dim, uint64_t dim_len,
+                              const uint32_t* offsets, uint32_t d, uint16_t* out, void* stream);
+int skx_permute_dimension_u32(skx_ctx* ctx, const uint32_t* dim, uint64_t dim_len,
+                              const uint32_t* offsets, uint32_t d, uint32_t* out, void* stream);
+int skx_permute_dimension_u64(skx_ctx* ctx, const uint64_t* dim, uint64_t dim_len,
+                              const uint32_t* offsets, uint32_t d, uint64_t* out, void* stream);
+
+/* ---- Q3 group-by --------------------------------------------------------- *
+ * aggregate_count / aggregate_sum (operators.cpp:100-118) and the hybrid
+ * parallel_aggregate (parallel.cpp:178-207): ids <= hot_threshold are
+ * accumulated in per-CTA shared-memory bins, the tail in global atomics.
+ * measure_width is 0 (no measure; sums ignored), 4 (u32, the reference's
+ * Column measure) or 8 (u64, BASELINE config 3's int64 quantity).
+ * counts and/or sums (u64[d]) may be NULL; both are overwritten.
+ * hot_threshold 0 = automatic (as many ids as fit shared memory).  Results
+ * do not depend on it (parallel.hpp:51-53). */
+int skx_aggregate(skx_ctx* ctx, const uint32_t* fact, const void* measure, int measure_width,
+                  uint64_t n, uint32_t d, uint32_t hot_threshold, uint64_t* counts,
+                  uint64_t* sums, void* stream);
+
+/* ---- Q2 selection -------------------------------------------------------- *
+ * KernelTable::select_offsets (kernels.hpp:25-30; scalar.cpp:31-42) and
+ * select()/parallel_select() (operators.cpp:87-98, parallel.cpp:102-129):
+ * ascending base+k for every row whose bit fact[k]-1 is set in the packed
+ * little-endian bitmap of `bits` bits.  n must be <= UINT32_MAX.  The number
+ * written goes to *count_dev (device u64). */
+int skx_select_offsets(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uint64_t* words,
+                       uint64_t bits, uint32_t base, uint32_t* out, uint64_t* count_dev,
+                       void* stream);
+/* permute_bitmap (operators.cpp:21-30): out bit r = in bit offsets[r]-1. */
+int skx_permute_bitmap(skx_ctx* ctx, const uint64_t* words, uint64_t bits,
+                       const uint32_t* offsets, uint32_t d, uint64_t* out_words, void* stream);
+/* build_bitmap(dim, v < threshold) (operators.hpp:38-45) for an int32 column. */
+int skx_build_bitmap_lt_i32(skx_ctx* ctx, const int32_t* dim, uint64_t d, int32_t threshold,
+                            uint64_t* out_words, void* stream);
+/* BASELINE config 5, fused: select rows whose bit is set, gather the four
+ * dimension columns (i32 category, f32 price, u64 supplier, u16 flag) for
+ * the selected rows in ascending row order, and SUM(price) per category in
+ * fp64 (sums[n_categories], overwritten; categories outside
+ * [0, n_categories) are not summed).  Offsets get `base` added. */
+int skx_select_gather_sum(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uint64_t* words,
+                          uint32_t d, const int32_t* cat, const float* price,
+                          const uint64_t* supp, const uint16_t* flag, uint32_t base,
+                          uint32_t n_categories, uint32_t* out_off, int32_t* out_cat,
+                          float* out_price, uint64_t* out_supp, uint16_t* out_flag,
+                          double* sums, uint64_t* count_dev, void* stream);
+
+/* ---- Q3a heavy hitters (operators.cpp:184-203) ---------------------------- *
+ * counts[i] = #rows with id i+1 for i < min(k, d) on a recoded column. */
+int skx_heavy_hitter_count(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint32_t d,
+                           uint32_t k, uint64_t* counts, void* stream);
+
+/* ---- workload generator (column.cpp:44-125) ------------------------------ */
+/* zipf_frequencies + partial_sum with cdf[d-1] = 1.0 (column.cpp:44-60,
+ * 77-79), on the host, bit-identical to the reference's doubles. */
+int skx_zipf_cdf_host(uint32_t d, double z, double* cdf);
+/* random_bijection (column.cpp:62-71), host, bit-identical (mt19937_64). */
+int skx_random_bijection_host(uint32_t n, uint64_t seed, uint32_t* out);
+/* Counter-based parallel Zipf draw on the device:
+ * u_k = (splitmix64(splitmix64(seed^0x5ca1ab1e) + k*0x9e3779b97f4a7c15)>>11)
+ * * 2^-53 for global row k = row_begin + i, rank = upper_bound(cdf, u)
+ * (clamped to d-1), out[i] = rank_to_id[rank] (or rank+1 when NULL). */
+int skx_generate_zipf(skx_ctx* ctx, const double* cdf, uint32_t d, const uint32_t* rank_to_id,
+                      uint64_t seed, uint64_t row_begin, uint64_t n, uint32_t* out,
+                      void* stream);
+
+/* Value-column fixtures for the BASELINE configs (device).  kind 0: raw
+ * splitmix64(seed ^ (0xd1000000 + i)) truncated to width bytes (the reference
+ * bench's dimension column, dataset.cpp:35-38); kind 1: integer
+ * p0 + splitmix64(seed + i*0x9e3779b97f4a7c15) % p1; kind 2: float32
+ * lognormal(mu=p0, sigma=p1) (Box-Muller in fp64), width must be 4. */
+int skx_fill_column(skx_ctx* ctx, int kind, int width, uint64_t seed, uint64_t n, double p0,
+                    double p1, void* out, void* stream);
+
+/* ---- host-buffer entry points (what a reference caller hands over) ------- *
+ * materialize() with host vectors: value_width 2, 4 or 8.  fact/dim/out are
+ * HOST pointers (pinned or pageable).  Synchronous. */
+int skx_materialize_host(skx_ctx* ctx, int value_width, const uint32_t* fact, uint64_t n,
+                         const void* dim, uint64_t dim_len, void* out);
+/* aggregate with host buffers (counts/sums are host u64[d]). */
+int skx_aggregate_host(skx_ctx* ctx, const uint32_t* fact, const void* measure,
+                       int measure_width, uint64_t n, uint32_t d, uint32_t hot_threshold,
+                       uint64_t* counts, uint64_t* sums);
+
+/* ---- tuning / evidence ---------------------------------------------------- *
+ * L2 policy for dimension loads in gathers: 0 = default, 1 = evict_last on
+ * dimension reads with evict_first on the streamed FK/output (default). */
+int skx_set_gather_policy(skx_ctx* ctx, int policy);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKX_H_ */

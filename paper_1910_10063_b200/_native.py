@@ -1,0 +1,102 @@
+"""ctypes binding of libskx.so (include/skx.h).
+
+There is no CPU fallback: if the library or a B200 is missing, loading fails
+loudly (NativeUnavailable).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from .errors import DomainViolation, Error, InvalidArgument, NativeUnavailable
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIBSKX = os.path.join(PKG, "libskx.so")
+
+OK, INVALID_ARGUMENT, DOMAIN_VIOLATION, CUDA_ERROR, ERROR = 0, 1, 2, 3, 5
+
+
+class ErrorInfo(C.Structure):
+    _fields_ = [("status", C.c_int32), ("row", C.c_uint64), ("value", C.c_uint32),
+                ("domain", C.c_uint64), ("message", C.c_char * 256)]
+
+
+_vp, _u64, _u32, _i32, _int, _dbl = (C.c_void_p, C.c_uint64, C.c_uint32, C.c_int32, C.c_int,
+                                     C.c_double)
+
+# name -> (restype, argtypes); mirrors include/skx.h
+SIGNATURES = {
+    "skx_version": (_int, []),
+    "skx_ctx_create": (_int, [_int, C.POINTER(_vp)]),
+    "skx_ctx_destroy": (_int, [_vp]),
+    "skx_sync": (_int, [_vp, _vp]),
+    "skx_last_error": (_int, [_vp, C.POINTER(ErrorInfo)]),
+    "skx_launch_count": (_u64, [_vp]),
+    "skx_gather_u16": (_int, [_vp, _vp, _u64, _vp, _u64, _vp, _vp]),
+    "skx_gather_u32": (_int, [_vp, _vp, _u64, _vp, _u64, _vp, _vp]),
+    "skx_gather_u64": (_int, [_vp, _vp, _u64, _vp, _u64, _vp, _vp]),
+    "skx_count_frequencies": (_int, [_vp, _vp, _u64, _u32, _vp, _vp]),
+    "skx_histogram_u32": (_int, [_vp, _vp, _u64, _u32, _vp, _int, _vp]),
+    "skx_build_index": (_int, [_vp, _vp, _u32, _u64, _vp, _vp, _vp]),
+    "skx_build_index_u32": (_int, [_vp, _vp, _u32, _u64, _vp, _vp, _vp]),
+    "skx_rebuild": (_int, [_vp, _vp, _u64, _u32, _vp, _vp, _vp]),
+    "skx_recode_fact": (_int, [_vp, _vp, _u64, _vp, _u32, _vp, _vp]),
+    "skx_permute_dimension_u16": (_int, [_vp, _vp, _u64, _vp, _u32, _vp, _vp]),
+    "skx_permute_dimension_u32": (_int, [_vp, _vp, _u64, _vp, _u32, _vp, _vp]),
+    "skx_permute_dimension_u64": (_int, [_vp, _vp, _u64, _vp, _u32, _vp, _vp]),
+    "skx_aggregate": (_int, [_vp, _vp, _vp, _int, _u64, _u32, _u32, _vp, _vp, _vp]),
+    "skx_select_offsets": (_int, [_vp, _vp, _u64, _vp, _u64, _u32, _vp, _vp, _vp]),
+    "skx_permute_bitmap": (_int, [_vp, _vp, _u64, _vp, _u32, _vp, _vp]),
+    "skx_build_bitmap_lt_i32": (_int, [_vp, _vp, _u64, _i32, _vp, _vp]),
+    "skx_select_gather_sum": (_int, [_vp, _vp, _u64, _vp, _u32, _vp, _vp, _vp, _vp, _u32, _u32,
+                                     _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "skx_heavy_hitter_count": (_int, [_vp, _vp, _u64, _u32, _u32, _vp, _vp]),
+    "skx_zipf_cdf_host": (_int, [_u32, _dbl, _vp]),
+    "skx_random_bijection_host": (_int, [_u32, _u64, _vp]),
+    "skx_generate_zipf": (_int, [_vp, _vp, _u32, _vp, _u64, _u64, _u64, _vp, _vp]),
+    "skx_materialize_host": (_int, [_vp, _int, _vp, _u64, _vp, _u64, _vp]),
+    "skx_aggregate_host": (_int, [_vp, _vp, _vp, _int, _u64, _u32, _u32, _vp, _vp]),
+    "skx_set_gather_policy": (_int, [_vp, _int]),
+    "skx_fill_column": (_int, [_vp, _int, _int, _u64, _u64, _dbl, _dbl, _vp, _vp]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path: str = LIBSKX) -> C.CDLL:
+    """Load libskx.so once (building it first if only the sources exist)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            try:
+                from .build import build_libskx
+                build_libskx()
+            except Exception as e:  # noqa: BLE001
+                raise NativeUnavailable(f"libskx.so missing and build failed: {e}") from e
+        try:
+            lib = C.CDLL(path)
+        except OSError as e:
+            raise NativeUnavailable(f"cannot load {path}: {e}") from e
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def raise_for(status: int, info: ErrorInfo | None = None) -> None:
+    if status == OK:
+        return
+    msg = info.message.decode(errors="replace") if info is not None else f"status {status}"
+    if status == DOMAIN_VIOLATION:
+        raise DomainViolation(info.row, info.value, info.domain)
+    if status == INVALID_ARGUMENT:
+        raise InvalidArgument(msg)
+    if status == CUDA_ERROR:
+        raise Error("CUDA error: " + msg)
+    raise Error(msg)

@@ -1,0 +1,266 @@
+// capi.cu -- context lifetime, deferred error reporting, scratch arenas and
+// the host-buffer (end-to-end) entry points of include/skx.h.
+#include <cmath>
+#include <cstdarg>
+#include <cstdlib>
+#include <random>
+#include <vector>
+
+#include "skx_internal.cuh"
+
+namespace skx {
+
+int set_error(skx_ctx* ctx, int status, const char* fmt, ...) {
+  if (!ctx) return status;
+  ctx->last.status = status;
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(ctx->last.message, sizeof ctx->last.message, fmt, ap);
+  va_end(ap);
+  return status;
+}
+
+int cuda_fail(skx_ctx* ctx, cudaError_t e, const char* where) {
+  return set_error(ctx, SKX_CUDA_ERROR, "%s: %s", where, cudaGetErrorString(e));
+}
+
+static void* grow(Scratch& sc, size_t bytes) {
+  if (sc.bytes >= bytes && sc.ptr) return sc.ptr;
+  if (sc.ptr) {
+    cudaDeviceSynchronize();
+    cudaFree(sc.ptr);
+    sc.ptr = nullptr;
+    sc.bytes = 0;
+  }
+  size_t want = bytes < 4096 ? 4096 : bytes;
+  if (cudaMalloc(&sc.ptr, want) != cudaSuccess) {
+    cudaGetLastError();
+    sc.ptr = nullptr;
+    return nullptr;
+  }
+  sc.bytes = want;
+  return sc.ptr;
+}
+
+void* scratch(skx_ctx* ctx, int slot, size_t bytes) { return grow(ctx->scratch[slot], bytes); }
+void* host_scratch_dev(skx_ctx* ctx, int slot, size_t bytes) { return grow(ctx->hb[slot], bytes); }
+
+static void reset_err_host(DevErr* e) {
+  for (int i = 0; i < kViolSlots; ++i) e->viol[i] = ~0ull;
+  e->invalid = 0;
+  e->pad = 0;
+  e->sum = 0;
+}
+
+}  // namespace skx
+
+using namespace skx;
+
+extern "C" {
+
+int skx_version(void) { return 1; }
+
+int skx_ctx_create(int device, skx_ctx** out) {
+  if (!out) return SKX_INVALID_ARGUMENT;
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return SKX_CUDA_ERROR;
+  }
+  if ((e = cudaSetDevice(device)) != cudaSuccess) return SKX_CUDA_ERROR;
+  skx_ctx* ctx = new skx_ctx();
+  ctx->device = device;
+  cudaDeviceProp prop{};
+  cudaGetDeviceProperties(&prop, device);
+  if (prop.major != 10) {
+    delete ctx;
+    fprintf(stderr, "skx: device %d is sm_%d%d; libskx.so is built for sm_100a only\n", device,
+            prop.major, prop.minor);
+    return SKX_CUDA_ERROR;
+  }
+  ctx->num_sms = prop.multiProcessorCount;
+  ctx->smem_optin = prop.sharedMemPerBlockOptin;
+  ctx->l2_bytes = prop.l2CacheSize;
+  if (cudaMalloc(&ctx->err, sizeof(DevErr)) != cudaSuccess ||
+      cudaMallocHost(&ctx->err_host, sizeof(DevErr)) != cudaSuccess) {
+    delete ctx;
+    return SKX_CUDA_ERROR;
+  }
+  reset_err_host(ctx->err_host);
+  cudaMemcpy(ctx->err, ctx->err_host, sizeof(DevErr), cudaMemcpyHostToDevice);
+  for (auto& s : ctx->hstream) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  for (auto& ev : ctx->hevent) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  *out = ctx;
+  return SKX_OK;
+}
+
+int skx_ctx_destroy(skx_ctx* ctx) {
+  if (!ctx) return SKX_OK;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  for (auto& sc : ctx->scratch)
+    if (sc.ptr) cudaFree(sc.ptr);
+  for (auto& sc : ctx->hb)
+    if (sc.ptr) cudaFree(sc.ptr);
+  for (auto& s : ctx->hstream)
+    if (s) cudaStreamDestroy(s);
+  for (auto& ev : ctx->hevent)
+    if (ev) cudaEventDestroy(ev);
+  cudaFree(ctx->err);
+  cudaFreeHost(ctx->err_host);
+  delete ctx;
+  return SKX_OK;
+}
+
+uint64_t skx_launch_count(const skx_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
+
+int skx_set_gather_policy(skx_ctx* ctx, int policy) {
+  if (!ctx || policy < 0 || policy > 1) return SKX_INVALID_ARGUMENT;
+  ctx->gather_policy = policy;
+  return SKX_OK;
+}
+
+int skx_last_error(const skx_ctx* ctx, skx_error_info* info) {
+  if (!ctx || !info) return SKX_INVALID_ARGUMENT;
+  *info = ctx->last;
+  return SKX_OK;
+}
+
+int skx_sync(skx_ctx* ctx, void* stream) {
+  if (!ctx) return SKX_INVALID_ARGUMENT;
+  cudaStream_t s = as_stream(stream);
+  cudaError_t e = cudaMemcpyAsync(ctx->err_host, ctx->err, sizeof(DevErr), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "skx_sync");
+  DevErr h = *ctx->err_host;
+  bool dirty = h.invalid != 0;
+  for (int i = 0; i < kViolSlots; ++i) dirty |= h.viol[i] != ~0ull;
+  if (!dirty) return SKX_OK;
+  reset_err_host(ctx->err_host);
+  cudaMemcpy(ctx->err, ctx->err_host, sizeof(DevErr), cudaMemcpyHostToDevice);
+  for (int i = 0; i < kViolSlots; ++i) {
+    if (h.viol[i] != ~0ull) {
+      const uint64_t row = (uint64_t(i) << 32) | (h.viol[i] >> 32);
+      const uint32_t value = static_cast<uint32_t>(h.viol[i]);
+      ctx->last.row = row;
+      ctx->last.value = value;
+      ctx->last.domain = ctx->last_domain;
+      return set_error(ctx, SKX_DOMAIN_VIOLATION, "domain violation at row %llu: value %u outside 1..%llu",
+                       (unsigned long long)row, value, (unsigned long long)ctx->last_domain);
+    }
+  }
+  return set_error(ctx, SKX_INVALID_ARGUMENT, "frequency profile counts do not sum to its total");
+}
+
+// ---- generator host side (column.cpp:44-71) --------------------------------
+
+int skx_zipf_cdf_host(uint32_t d, double z, double* cdf) {
+  if (d == 0 || d > SKX_MAX_DOMAIN_CARDINALITY || !(z >= 0.0) || !cdf) return SKX_INVALID_ARGUMENT;
+  // zipf_frequencies: Kahan-summed normaliser, column.cpp:44-60.
+  double sum = 0.0, carry = 0.0;
+  for (uint32_t r = 1; r <= d; ++r) {
+    const double w = std::pow(static_cast<double>(r), -z);
+    cdf[r - 1] = w;
+    const double y = w - carry;
+    const double t = sum + y;
+    carry = (t - sum) - y;
+    sum = t;
+  }
+  for (uint32_t i = 0; i < d; ++i) cdf[i] /= sum;
+  // std::partial_sum, then cdf.back() = 1.0 (column.cpp:77-79).
+  for (uint32_t i = 1; i < d; ++i) cdf[i] = cdf[i - 1] + cdf[i];
+  cdf[d - 1] = 1.0;
+  return SKX_OK;
+}
+
+int skx_random_bijection_host(uint32_t n, uint64_t seed, uint32_t* map) {
+  if (!map && n) return SKX_INVALID_ARGUMENT;
+  // Fisher-Yates with mt19937_64(seed), j = rng() % i (column.cpp:62-71).
+  for (uint32_t i = 0; i < n; ++i) map[i] = i + 1;
+  std::mt19937_64 rng(seed);
+  for (uint32_t i = n; i > 1; --i) {
+    const uint32_t j = static_cast<uint32_t>(rng() % i);
+    const uint32_t t = map[i - 1];
+    map[i - 1] = map[j];
+    map[j] = t;
+  }
+  return SKX_OK;
+}
+
+// ---- host-buffer entry points ---------------------------------------------
+// Chunked pipeline over two streams: H2D(fact chunk) -> kernel -> D2H(out
+// chunk); chunk i+1's copy-in overlaps chunk i's kernel and copy-out.
+
+int skx_materialize_host(skx_ctx* ctx, int w, const uint32_t* fact, uint64_t n, const void* dim,
+                         uint64_t dim_len, void* out) {
+  if (!ctx) return SKX_INVALID_ARGUMENT;
+  if (w != 2 && w != 4 && w != 8) return set_error(ctx, SKX_INVALID_ARGUMENT, "bad value width");
+  cudaSetDevice(ctx->device);
+  const uint64_t chunk = uint64_t(1) << 25;  // rows per pipeline stage
+  void* d_dim = host_scratch_dev(ctx, 0, dim_len * w + 16);
+  void* d_fact[2] = {host_scratch_dev(ctx, 1, chunk * 4), host_scratch_dev(ctx, 2, chunk * 4)};
+  void* d_out[2] = {host_scratch_dev(ctx, 3, chunk * w), host_scratch_dev(ctx, 4, chunk * w)};
+  if (!d_dim || !d_fact[0] || !d_fact[1] || !d_out[0] || !d_out[1])
+    return set_error(ctx, SKX_CUDA_ERROR, "materialize_host: out of device memory");
+  cudaError_t e = cudaMemcpyAsync(d_dim, dim, dim_len * w, cudaMemcpyHostToDevice, ctx->hstream[0]);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "materialize_host H2D dim");
+  cudaEventRecord(ctx->hevent[2], ctx->hstream[0]);
+  cudaStreamWaitEvent(ctx->hstream[1], ctx->hevent[2], 0);
+  int rc = SKX_OK;
+  for (uint64_t b = 0, i = 0; b < n; b += chunk, ++i) {
+    const int s = static_cast<int>(i & 1);
+    const uint64_t m = (n - b) < chunk ? (n - b) : chunk;
+    cudaStream_t st = ctx->hstream[s];
+    cudaMemcpyAsync(d_fact[s], fact + b, m * 4, cudaMemcpyHostToDevice, st);
+    rc = launch_gather(ctx, w, static_cast<const uint32_t*>(d_fact[s]), m, d_dim, dim_len, d_out[s], st);
+    if (rc) break;
+    cudaMemcpyAsync(static_cast<char*>(out) + b * w, d_out[s], m * w, cudaMemcpyDeviceToHost, st);
+  }
+  cudaStreamSynchronize(ctx->hstream[0]);
+  cudaStreamSynchronize(ctx->hstream[1]);
+  if (rc) return rc;
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "materialize_host");
+  rc = skx_sync(ctx, ctx->hstream[0]);
+  if (rc == SKX_DOMAIN_VIOLATION) {
+    // Chunk launches record chunk-local rows; find the first offending global
+    // row on the host (cold path only).
+    for (uint64_t k = 0; k < n; ++k) {
+      if (fact[k] - 1u >= dim_len) {
+        ctx->last.row = k;
+        ctx->last.value = fact[k];
+        ctx->last.domain = dim_len;
+        return set_error(ctx, SKX_DOMAIN_VIOLATION, "domain violation at row %llu: value %u outside 1..%llu",
+                         (unsigned long long)k, fact[k], (unsigned long long)dim_len);
+      }
+    }
+  }
+  return rc;
+}
+
+int skx_aggregate_host(skx_ctx* ctx, const uint32_t* fact, const void* measure, int mw, uint64_t n,
+                       uint32_t d, uint32_t hot, uint64_t* counts, uint64_t* sums) {
+  if (!ctx) return SKX_INVALID_ARGUMENT;
+  if (mw != 0 && mw != 4 && mw != 8) return set_error(ctx, SKX_INVALID_ARGUMENT, "bad measure width");
+  cudaSetDevice(ctx->device);
+  void* d_fact = host_scratch_dev(ctx, 1, n * 4 + 16);
+  void* d_meas = mw ? host_scratch_dev(ctx, 3, n * mw + 16) : nullptr;
+  void* d_out = host_scratch_dev(ctx, 0, uint64_t(d) * 16 + 16);
+  if (!d_fact || (mw && !d_meas) || !d_out)
+    return set_error(ctx, SKX_CUDA_ERROR, "aggregate_host: out of device memory");
+  cudaStream_t st = ctx->hstream[0];
+  cudaMemcpyAsync(d_fact, fact, n * 4, cudaMemcpyHostToDevice, st);
+  if (mw) cudaMemcpyAsync(d_meas, measure, n * mw, cudaMemcpyHostToDevice, st);
+  uint64_t* dc = static_cast<uint64_t*>(d_out);
+  uint64_t* ds = dc + d;
+  int rc = launch_aggregate(ctx, static_cast<const uint32_t*>(d_fact), d_meas, mw, n, d, hot,
+                            counts ? dc : nullptr, sums ? ds : nullptr, st);
+  if (rc) return rc;
+  if (counts) cudaMemcpyAsync(counts, dc, uint64_t(d) * 8, cudaMemcpyDeviceToHost, st);
+  if (sums) cudaMemcpyAsync(sums, ds, uint64_t(d) * 8, cudaMemcpyDeviceToHost, st);
+  return skx_sync(ctx, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,270 @@
+"""GPU parity: the sm_100a kernels (through the C-ABI in libskx.so) against
+the pinned oracle and the reference's golden fixtures.  Bit-exact for every
+integer / index / byte result; fp64 category sums within 1e-6 relative."""
+import numpy as np
+import pytest
+import torch
+
+from conftest import words_from_bits
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sx():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1910_10063_b200 import skewdx
+    skewdx.context(0)
+    return skewdx
+
+
+def cu(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.view(dtype)
+    return t.cuda()
+
+
+def np_(t):
+    return t.cpu().numpy()
+
+
+# ---------------------------------------------------------------- golden ---
+def test_golden_cases_full_path(sx, ref_cases):
+    for i in range(len(ref_cases)):
+        c = ref_cases.case(i)
+        d = c["d"]
+        fact = cu(c["fact"])
+        prof = sx.count_frequencies(fact, d)
+        assert np.array_equal(np_(prof.counts), c["counts"]), i
+        idx = sx.build_index(prof)
+        assert np.array_equal(np_(idx.offsets), c["offsets"]), i
+        assert np.array_equal(np_(idx.ranks), c["ranks"]), i
+        idx2 = sx.rebuild(fact, d)
+        assert np.array_equal(np_(idx2.offsets), c["offsets"]), i
+        assert np.array_equal(np_(idx2.ranks), c["ranks"]), i
+        rec = sx.recode_fact(fact, idx)
+        assert np.array_equal(np_(rec), c["recoded"]), i
+        dim = cu(c["dim"])
+        dperm = sx.permute_dimension(dim, idx)
+        assert np.array_equal(np_(dperm), c["dim_perm"]), i
+        assert np.array_equal(np_(sx.materialize(fact, dim)), c["mat_rand"]), i
+        assert np.array_equal(np_(sx.materialize(rec, dperm)), c["mat_freq"]), i
+        counts, sums = sx.aggregate_count_sum(rec, cu(c["measure"]), d)
+        assert np.array_equal(np_(counts), c["counts_freq"]), i
+        assert np.array_equal(np_(sums), c["sums"]), i
+        assert np.array_equal(np_(sx.aggregate_count(rec, d)), c["counts_freq"]), i
+        bm = sx.Bitmap.from_numpy(c["words"], d)
+        bmp = sx.permute_bitmap(bm, idx)
+        assert np.array_equal(np_(bmp.words), c["words_perm"]), i
+        assert np.array_equal(np_(sx.select(fact, bm)), c["sel_rand"]), i
+        assert np.array_equal(np_(sx.select(rec, bmp)), c["sel_freq"]), i
+        hh = sx.heavy_hitter_count(rec, d, 13)
+        assert [t[0] for t in hh.top] == c["hh_ids"].tolist(), i
+        assert [t[1] for t in hh.top] == c["hh_counts"].tolist(), i
+
+
+# ------------------------------------------------------------------- KATs ---
+def test_kat(sx, kat):
+    from paper_1910_10063_b200 import DomainViolation, InvalidArgument
+    for c in kat["count_frequencies"]:
+        p = sx.count_frequencies(cu(np.array(c["fact"], np.uint32)), c["d"])
+        assert np_(p.counts).tolist() == c["counts"] and p.total == c["total"]
+    for c in kat["count_frequencies_violation"]:
+        with pytest.raises(DomainViolation) as e:
+            sx.count_frequencies(cu(np.array(c["fact"], np.uint32)), c["d"])
+        assert e.value.row() == c["row"] and e.value.value() == c["value"]
+    pf = kat["popularity_fixture"]
+    fact = np.concatenate([np.full(cnt, i, np.uint32) for i, cnt in pf["by_count"]])
+    np.random.default_rng(99).shuffle(fact)
+    idx = sx.rebuild(cu(fact), pf["d"])
+    assert np_(idx.offsets).tolist() == pf["offsets"] and np_(idx.ranks).tolist() == pf["ranks"]
+    assert np_(sx.recode_fact(cu(np.array(pf["recode_in"], np.uint32)), idx)).tolist() == pf["recode_out"]
+    assert np_(sx.permute_dimension(cu(np.array(pf["dim"], np.uint32)), idx)).tolist() == pf["permuted_dim"]
+    for c in kat["build_index"]:
+        idx = sx.build_index(sx.FrequencyProfile(cu(np.array(c["counts"], np.uint64)), c["total"]))
+        assert np_(idx.offsets).tolist() == c["offsets"] and np_(idx.ranks).tolist() == c["ranks"]
+    for c in kat["build_index_invalid"]:
+        with pytest.raises(InvalidArgument):
+            sx.build_index(sx.FrequencyProfile(cu(np.array(c["counts"], np.uint64)), c["total"]))
+    c = kat["permute_length_mismatch"]
+    idx = sx.rebuild(cu(np.array(c["fact"], np.uint32)), c["d"])
+    with pytest.raises(InvalidArgument):
+        sx.permute_dimension(cu(np.array(c["dim"], np.uint32)), idx)
+    c = kat["aggregate_count"]
+    assert np_(sx.aggregate_count(cu(np.array(c["fact"], np.uint32)), c["d"])).tolist() == c["counts"]
+    c = kat["aggregate_sum"]
+    assert np_(sx.aggregate_sum(cu(np.array(c["fact"], np.uint32)),
+                                cu(np.array(c["measure"], np.uint32)), c["d"])).tolist() == c["sums"]
+    with pytest.raises(InvalidArgument):
+        sx.aggregate_sum(cu(np.array(c["fact"], np.uint32)), cu(np.array([1], np.uint32)), c["d"])
+    for c in kat["select"]:
+        bm = sx.Bitmap.from_numpy(words_from_bits(c["bits"], c["d"]), c["d"])
+        assert np_(sx.select(cu(np.array(c["fact"], np.uint32)), bm)).tolist() == c["offsets"]
+    c = kat["select_violation"]
+    with pytest.raises(DomainViolation) as e:
+        sx.select(cu(np.array(c["fact"], np.uint32)),
+                  sx.Bitmap.from_numpy(words_from_bits(c["bits"], c["d"]), c["d"]))
+    assert e.value.row() == c["row"] and e.value.value() == c["value"]
+    c = kat["build_bitmap"]
+    bm = sx.build_bitmap_lt(cu(np.array(c["values"], np.int32)), c["threshold"])
+    assert np_(bm.words).tolist() == words_from_bits(c["set"], len(c["values"])).tolist()
+    for c in kat["heavy_hitters"]:
+        hh = sx.heavy_hitter_count(cu(np.array(c["fact"], np.uint32)), c["d"], c["k"])
+        assert [list(t) for t in hh.top] == c["top"] and hh.clamped == c["clamped"]
+    g = kat["gather_edges"]
+    dim = cu(np.arange(10, 10 + g["d"], dtype=np.uint32))
+    assert sx.materialize(cu(np.array([], np.uint32)), dim).numel() == 0
+    for bad in (g["bad_high"], g["bad_zero"]):
+        with pytest.raises(DomainViolation):
+            sx.materialize(cu(np.array(bad, np.uint32)), dim)
+
+
+# ------------------------------------------------------- oracle, seeded ---
+@pytest.mark.parametrize("dtype,npdt", [(torch.uint16, np.uint16), (torch.uint32, np.uint32),
+                                        (torch.uint64, np.uint64), (torch.float32, np.float32),
+                                        (torch.int64, np.int64)])
+def test_gather_widths_ragged_and_unaligned(sx, oracle, dtype, npdt):
+    rng = np.random.default_rng(11)
+    d = 5003
+    dim_np = rng.integers(0, 2**63, size=d, dtype=np.uint64).astype(npdt) if npdt != np.float32 \
+        else rng.standard_normal(d).astype(np.float32)
+    dim = cu(dim_np)
+    for n in [0, 1, 3, 4, 5, 7, 8, 9, 63, 64, 1000, 4097, 100003]:
+        fact_np = rng.integers(1, d + 1, size=n + 3, dtype=np.uint32)
+        full = cu(fact_np)
+        for off in range(4):  # misaligned starts exercise the scalar head path
+            f = full[off: off + n]
+            out = sx.materialize(f, dim)
+            exp = dim_np[fact_np[off: off + n].astype(np.int64) - 1]
+            assert np.array_equal(np_(out).view(np.uint8), exp.view(np.uint8)), (n, off)
+            # misaligned output buffer too
+            big = torch.empty(n + 1, dtype=dtype, device="cuda")
+            sx.materialize(f, dim, out=big[1:])
+            assert np.array_equal(np_(big[1:]).view(np.uint8), exp.view(np.uint8)), (n, off)
+
+
+def test_domain_violation_first_row(sx):
+    from paper_1910_10063_b200 import DomainViolation
+    d = 1000
+    fact = np.random.default_rng(1).integers(1, d + 1, size=1 << 20, dtype=np.uint32)
+    fact[777777] = d + 5
+    fact[900001] = 0
+    with pytest.raises(DomainViolation) as e:
+        sx.materialize(cu(fact), cu(np.arange(d, dtype=np.uint32)))
+    assert e.value.row() == 777777 and e.value.value() == d + 5
+    fact[123] = 0
+    for op in (lambda f: sx.count_frequencies(f, d), lambda f: sx.aggregate_count(f, d),
+               lambda f: sx.rebuild(f, d),
+               lambda f: sx.select(f, sx.Bitmap(d)),
+               lambda f: sx.aggregate_count_sum(f, torch.ones(f.numel(), dtype=torch.int64,
+                                                              device="cuda"), d)):
+        with pytest.raises(DomainViolation) as e:
+            op(cu(fact))
+        assert e.value.row() == 123 and e.value.value() == 0
+    # context is clean again afterwards
+    assert sx.count_frequencies(cu(np.array([1, 2], np.uint32)), 2).counts.sum().item() == 2
+
+
+def test_counter_generator_matches_oracle(sx, oracle):
+    for d, z, n, begin in [(1, 0.0, 100, 0), (1000, 1.0, 100000, 0), (1 << 16, 1.25, 1 << 20, 12345)]:
+        cdf_np = sx.zipf_cdf(d, z)
+        assert np.array_equal(cdf_np, oracle.zipf_cdf(d, z))
+        r2i = sx.random_bijection(d, 42)
+        out = sx.generate_zipf(cu(cdf_np), n, 42, rank_to_id=cu(r2i), row_begin=begin)
+        exp = oracle.generate_zipf_counter(cdf_np, r2i, 42, begin, n)
+        assert np.array_equal(np_(out), exp)
+
+
+@pytest.mark.parametrize("d,n,z", [(1, 1000, 0.0), (4096, 1 << 20, 0.0), (1 << 16, 1 << 21, 1.25),
+                                   (1 << 20, 1 << 21, 1.0), (70001, 3 << 19, 2.0),
+                                   (1 << 22, 1 << 22, 0.5)])
+def test_index_build_vs_oracle(sx, oracle, d, n, z):
+    cdf = sx.zipf_cdf(d, z)
+    r2i = sx.random_bijection(d, 7)
+    fact = sx.generate_zipf(cu(cdf), n, 7, rank_to_id=cu(r2i))
+    f_np = np_(fact)
+    counts = oracle.count_frequencies(f_np, d)
+    assert np.array_equal(np_(sx.count_frequencies(fact, d).counts), counts)
+    assert np.array_equal(np_(sx.histogram_u32(fact, d)).astype(np.uint64), counts)
+    off, rk = oracle.build_index(counts, n)
+    idx = sx.rebuild(fact, d)
+    assert np.array_equal(np_(idx.offsets), off)
+    assert np.array_equal(np_(idx.ranks), rk)
+    rec = sx.recode_fact(fact, idx)
+    assert np.array_equal(np_(rec), oracle.recode_fact(f_np, rk))
+
+
+def test_build_index_wide_counts(sx, oracle):
+    """u64 counts above 2^32 take the 64-bit key path."""
+    rng = np.random.default_rng(3)
+    counts = rng.integers(0, 2**40, size=10000, dtype=np.uint64)
+    counts[rng.integers(0, 10000, size=3000)] = 0
+    counts[:50] = 7  # ties
+    total = int(counts.sum())
+    idx = sx.build_index(sx.FrequencyProfile(cu(counts), total))
+    off, rk = oracle.build_index(counts, total)
+    assert np.array_equal(np_(idx.offsets), off) and np.array_equal(np_(idx.ranks), rk)
+
+
+@pytest.mark.parametrize("hot", [0, 1, 7, 1000])
+def test_aggregate_vs_oracle(sx, oracle, hot):
+    d, n = 1 << 18, (1 << 22) + 3
+    cdf = sx.zipf_cdf(d, 1.0)
+    fact = sx.generate_zipf(cu(cdf), n, 99)  # rank space: hot ids are small
+    f_np = np_(fact)
+    meas = np.random.default_rng(2).integers(1, 101, size=n, dtype=np.int64)
+    c_exp, s_exp = oracle.aggregate_count_sum(f_np, meas.view(np.uint64), d)
+    c, s = sx.aggregate_count_sum(fact, cu(meas), d, hot_threshold=hot)
+    assert np.array_equal(np_(c), c_exp) and np.array_equal(np_(s), s_exp)
+    c, s = sx.aggregate_count_sum(fact[1:], cu(meas)[1:], d, hot_threshold=hot)  # unaligned
+    c_exp, s_exp = oracle.aggregate_count_sum(f_np[1:], meas[1:].view(np.uint64), d)
+    assert np.array_equal(np_(c), c_exp) and np.array_equal(np_(s), s_exp)
+    c = sx.parallel_aggregate(fact, d, sx.ParallelPlan(threads=8, strategy=sx.AggStrategy.hybrid,
+                                                       hot_threshold=max(hot, 1)))
+    assert np.array_equal(np_(c), oracle.aggregate_count_sum(f_np, None, d)[0])
+
+
+def test_select_gather_sum_vs_oracle(sx, oracle):
+    d, n = 1 << 15, (1 << 21) + 17
+    rng = np.random.default_rng(4)
+    cat = rng.integers(0, 1000, size=d, dtype=np.int32)
+    price = np.exp(3 + rng.standard_normal(d)).astype(np.float32)
+    supp = rng.integers(0, 2**63, size=d, dtype=np.uint64)
+    flag = rng.integers(0, 2**16, size=d, dtype=np.uint16)
+    cdf = sx.zipf_cdf(d, 1.0)
+    r2i = sx.random_bijection(d, 5)
+    fact = sx.generate_zipf(cu(cdf), n, 5, rank_to_id=cu(r2i))
+    bm = sx.build_bitmap_lt(cu(cat), 100)
+    got = sx.select_gather_sum(fact, bm, cu(cat), cu(price), cu(supp), cu(flag), 1000, base=3)
+    exp = oracle.select_gather_sum(np_(fact), np_(bm.words), cat, price, supp, flag, 1000, base=3)
+    for g, e in zip(got[:5], exp[:5]):
+        assert np.array_equal(np_(g), e)
+    s, se = np_(got[5]), exp[5]
+    assert np.allclose(s, se, rtol=1e-6, atol=0)  # fp64 sums, order differs
+    # selection alone equals the oracle's select, also in the reordered space
+    assert np.array_equal(np_(sx.select(fact, bm)), oracle.select_offsets(np_(fact), np_(bm.words), d))
+
+
+def test_reorder_invariants_at_scale(sx):
+    """Size-independent properties at 2^26 rows: gather equality across
+    layouts, rank-space counts map back through offsets, multiset of counts
+    preserved, bijection."""
+    d, n = 1 << 22, 1 << 26
+    cdf = cu(sx.zipf_cdf(d, 1.0))
+    r2i = cu(sx.random_bijection(d, 42))
+    fact = sx.generate_zipf(cdf, n, 42, rank_to_id=r2i)
+    idx = sx.rebuild(fact, d)
+    off = idx.offsets.to(torch.int64)
+    rk = idx.ranks.to(torch.int64)
+    assert torch.equal(rk[off - 1], torch.arange(1, d + 1, device="cuda"))
+    rec = sx.recode_fact(fact, idx)
+    dim = torch.randint(0, 2**62, (d,), dtype=torch.int64, device="cuda")
+    dperm = sx.permute_dimension(dim, idx)
+    assert torch.equal(sx.materialize(fact, dim), sx.materialize(rec, dperm))
+    c_rand = sx.aggregate_count(fact, d).to(torch.int64)
+    c_freq = sx.aggregate_count(rec, d).to(torch.int64)
+    assert torch.equal(c_freq, c_rand[off - 1])
+    assert bool((c_freq[:-1] >= c_freq[1:]).all())  # frequency-sorted
+    assert int(c_freq.sum()) == n
