@@ -1,0 +1,429 @@
+#!/usr/bin/env python
+"""Benchmark of the skew-reordered FK-join gather (+ group-by) on B200.
+
+Headline workload (BASELINE.json configs[1], "Large FK-join gather"): a
+dimension of 2^27 keys with an int64 value column (1 GiB), 2^30 int32 FK rows
+drawn Zipf(s) over ranks with ranks scattered to ids by a seeded random
+bijection, the skew-aware index built on the GPU (histogram -> sort-by-count
+-> recode -> permute), and the timed step is one gather
+``out[k] = dim_freq[fact_freq[k]-1]`` over every fact row of the (reordered)
+layout -- one ``skx_gather_u64`` launch.  Scaling is weak: every GPU owns a
+2^30-row shard of the fact table (rows partitioned, no data-path collective
+for the gather) and the dimension columns are replicated; the index build
+all-reduces the per-GPU histograms.
+
+Prints ONE JSON line (rank 0).  ``--impl reference`` times the reference's
+CPU path on the host instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+D_C2, N_C2, SEED = 1 << 27, 1 << 30, 42
+D_C3 = 1 << 24
+CPU_SAMPLE_ROWS = 1 << 27
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--z", type=float, default=1.0, help="Zipf exponent (C2 sweeps 0.5/1.0/1.5)")
+    p.add_argument("--rows", type=int, default=N_C2, help="fact rows per GPU")
+    p.add_argument("--domain", type=int, default=D_C2)
+    p.add_argument("--no-extras", action="store_true", help="skip rand-layout / group-by lines")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--policy", type=int, default=1, help="gather L2 policy (0 default, 1 evict_last)")
+    return p.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(name):
+    """Per-launch DRAM bytes from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(name)
+    except Exception:  # noqa: BLE001
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        rows = []
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                try:
+                    rows.append((float(parts[0]), float(parts[1]), parts[2:]))
+                except ValueError:
+                    pass
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v == "Active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "samples": len(rows), "reasons": reasons}
+
+
+# ---------------------------------------------------------------------------
+# CPU side (rank 0, N=1): the reference's path on the host's cores
+# ---------------------------------------------------------------------------
+def cpu_gather_baseline(fact_np, dim_np, steps=3):
+    """Port of parallel_materialize for the i64 value width (the reference's
+    parallel.cpp:87-100 is u32-only) over chunk_spans with all host threads,
+    plus the unmodified reference's u32 KernelTable gather for context."""
+    from oracle.oracle import Oracle, Reference
+    import numpy as np
+    orc = Oracle()
+    threads = os.cpu_count() or 1
+    out = np.empty(len(fact_np), np.uint64)
+    orc.parallel_gather_u64(fact_np, dim_np, out, threads)  # warm-up
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        orc.parallel_gather_u64(fact_np, dim_np, out, threads)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    res = {"value": len(fact_np) / t, "unit": "rows/s", "cores": threads, "kind": "port",
+           "sample": (f"{len(fact_np)} rows of the same reordered (freq) FK shard, full "
+                      f"{len(dim_np)}-key int64 dimension; parallel_materialize port "
+                      f"(parallel.cpp:87-100, i64 width) over chunk_spans, {threads} threads, "
+                      f"median of {steps}")}
+    try:
+        ref = Reference()
+        dim32 = np.ascontiguousarray(dim_np.astype(np.uint32))
+        out32 = np.empty(len(fact_np), np.uint32)
+        import ctypes as C
+        ns = ref.L.ref_time_gather_kernel(fact_np.ctypes.data_as(C.c_void_p), len(fact_np),
+                                          dim32.ctypes.data_as(C.c_void_p),
+                                          out32.ctypes.data_as(C.c_void_p), threads, steps)
+        res["reference_u32_kernel_rows_per_s"] = len(fact_np) / (ns * 1e-9)
+        res["reference_u32_kernel_table"] = ref.active_kernels_name()
+    except Exception as e:  # noqa: BLE001
+        res["reference_u32_kernel_rows_per_s"] = None
+        res["reference_note"] = f"oracle/_ref unavailable: {e}"
+    return res
+
+
+def run_reference_arm(args):
+    """--impl reference: the reference's CPU gather on a bounded sample of the
+    same workload, all host threads, K timed steps after W warm-ups."""
+    import numpy as np
+    from oracle.oracle import Oracle, Reference
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    orc = Oracle()
+    threads = os.cpu_count() or 1
+    d = args.domain
+    rows = min(CPU_SAMPLE_ROWS, args.rows)
+    # Inputs: the counter-based Zipf draw of the same (D, s, seed), ids = ranks
+    # (the skew-reordered layout, Layout::freq up to empirical tie order).
+    cdf = orc.zipf_cdf(d, args.z)
+    fact = orc.generate_zipf_counter_mt(cdf, None, SEED, rows, threads)
+    dim = np.random.default_rng(SEED).integers(0, 2**63, size=d, dtype=np.uint64)
+    out = np.empty(rows, np.uint64)
+    for _ in range(args.warmup):
+        orc.parallel_gather_u64(fact, dim, out, threads)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        orc.parallel_gather_u64(fact, dim, out, threads)
+        ts.append(time.perf_counter() - t0)
+    total = sum(ts)
+    value = rows * args.steps / total
+    kind = "port"
+    sample = (f"{rows} rows per step of the C2 workload (D={d}, s={args.z}, int64 dim, reordered "
+              f"layout); parallel_materialize port (i64) over chunk_spans, {threads} threads")
+    line = {
+        "impl": "reference", "metric": "fact rows/s (skew-reordered FK-join gather)",
+        "value": value, "unit": "rows/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": "C2 large FK-join gather", "domain": d, "rows": rows, "z": args.z,
+                   "value": "int64", "layout": "freq", "seed": SEED},
+        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": threads, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    try:
+        ref = Reference()
+        import ctypes as C
+        dim32 = np.ascontiguousarray(dim.astype(np.uint32))
+        out32 = np.empty(rows, np.uint32)
+        ns = ref.L.ref_time_gather_kernel(fact.ctypes.data_as(C.c_void_p), rows,
+                                          dim32.ctypes.data_as(C.c_void_p),
+                                          out32.ctypes.data_as(C.c_void_p), threads, 3)
+        line["reference_u32_kernel_rows_per_s"] = rows / (ns * 1e-9)
+        line["reference_u32_kernel_table"] = ref.active_kernels_name()
+    except Exception as e:  # noqa: BLE001
+        line["reference_note"] = f"oracle/_ref unavailable: {e}"
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU side
+# ---------------------------------------------------------------------------
+def timed_launches(fn, steps, warmup, stream, dist_on, ctx=None):
+    """W warm-ups; then K steps bracketed by barrier + synchronize, one CUDA
+    event per step on the launching stream.  Returns (total_ms, [per-step ms],
+    libskx kernel launches inside the timed region)."""
+    import torch
+    import torch.distributed as dist
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    if dist_on:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    l0 = ctx.launches() if ctx is not None else 0
+    ev[0].record(stream)
+    for i in range(steps):
+        fn()
+        ev[i + 1].record(stream)
+    launches = (ctx.launches() - l0) if ctx is not None else 0
+    torch.cuda.synchronize()
+    if dist_on:
+        dist.barrier()
+    per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+    return ev[0].elapsed_time(ev[steps]), per, launches
+
+
+def max_over_ranks(x, dist_on):
+    import torch
+    import torch.distributed as dist
+    if not dist_on:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1910_10063_b200 import dataset as ds_mod
+    from paper_1910_10063_b200 import skewdx as sx
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist_on = world > 1
+    if dist_on:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = sx.context(local)
+    ctx.set_gather_policy(args.policy)
+    peak, peak_kind = load_peaks()
+
+    d = args.domain
+    rows_local = args.rows  # weak scaling: fixed rows per GPU
+    n_total = rows_local * world
+    shard = ds_mod.Shard(rank, world, rank * rows_local, (rank + 1) * rows_local)
+    t0 = time.perf_counter()
+    data = ds_mod.make_gather_dataset(d, n_total, args.z, SEED, torch.int64, shard)
+    setup_s = time.perf_counter() - t0
+    stream = torch.cuda.current_stream()
+    out = torch.empty(rows_local, dtype=torch.int64, device="cuda")
+
+    def step_freq():
+        sx.materialize(data.fact_freq, data.dim_freq, out=out, ctx=ctx, sync=False)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    total_ms, per, launches = timed_launches(step_freq, args.steps, args.warmup, stream, dist_on,
+                                             ctx)
+    clocks = sampler.stop()
+    ctx.sync()  # raises on a deferred domain violation
+    total_ms = max_over_ranks(total_ms, dist_on)
+    value = n_total * args.steps / (total_ms * 1e-3)
+    alg_bytes = rows_local * (4 + 8)  # FK read + int64 output write per row
+    avg_launch_s = statistics.mean(per) * 1e-3
+    achieved = alg_bytes / avg_launch_s / 1e9
+    out_freq = out.clone()
+
+    extras = {}
+    if not args.no_extras:
+        # original (rand) layout through the same kernel, same timing rules
+        outr = torch.empty_like(out)
+
+        def step_rand():
+            sx.materialize(data.fact_rand, data.dim_rand, out=outr, ctx=ctx, sync=False)
+        tr, per_r, _ = timed_launches(step_rand, args.steps, args.warmup, stream, dist_on)
+        tr = max_over_ranks(tr, dist_on)
+        # CorrectnessError gate of bench.cpp:300-304: both layouts, same result
+        same = bool(torch.equal(outr, out_freq))
+        extras["rand_layout"] = {
+            "value": n_total * args.steps / (tr * 1e-3), "unit": "rows/s",
+            "roofline_frac": alg_bytes / (statistics.mean(per_r) * 1e-3) / 1e9 / peak,
+            "freq_over_rand": (n_total * args.steps / (total_ms * 1e-3)) / (n_total * args.steps / (tr * 1e-3)),
+            "outputs_equal": same}
+        if not same:
+            raise SystemExit("CorrectnessError: rand and freq layouts disagree")
+        del outr
+        extras["index_build"] = {k: round(v, 3) for k, v in data.timings_ms.items()}
+        extras["index_build"]["note"] = ("histogram+all-reduce+sort of D=%d over %d rows, then "
+                                         "recode and permute (ms, CUDA events)" % (d, n_total))
+
+    # e2e through the C-ABI host-buffer entry (pinned host fact+dim in, out back)
+    e2e = None
+    if not args.no_e2e:
+        import ctypes as C
+        f_h = data.fact_freq.cpu().pin_memory()
+        d_h = data.dim_freq.cpu().pin_memory()
+        o_h = torch.empty(rows_local, dtype=torch.int64).pin_memory()
+        lib = ctx.lib
+
+        def e2e_step():
+            ctx.check(lib.skx_materialize_host(ctx.handle, 8, C.c_void_p(f_h.data_ptr()), rows_local,
+                                               C.c_void_p(d_h.data_ptr()), d,
+                                               C.c_void_p(o_h.data_ptr())))
+        e2e_step()
+        e_steps = max(1, min(args.steps, 3))
+        if dist_on:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            e2e_step()
+        te = max_over_ranks(time.perf_counter() - t0, dist_on)
+        if not torch.equal(o_h[:1 << 20].cuda(), out_freq[:1 << 20]):
+            raise SystemExit("CorrectnessError: host-buffer path disagrees with device path")
+        e2e = {"value": n_total * e_steps / te, "unit": "rows/s",
+               "h2d_bytes_per_step": rows_local * 4 + d * 8, "d2h_bytes_per_step": rows_local * 8,
+               "path": "skx_materialize_host (pinned host fact+dim -> device -> pinned host out, "
+                       "chunked 2-stream pipeline)"}
+        del f_h, d_h, o_h
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        m = min(CPU_SAMPLE_ROWS, rows_local)
+        cpu = cpu_gather_baseline(data.fact_freq[:m].cpu().numpy(),
+                                  data.dim_freq.cpu().numpy().view(np.uint64))
+
+    groupby = None
+    if not args.no_extras:
+        del data, out, out_freq
+        torch.cuda.empty_cache()
+        gdat = ds_mod.make_groupby_dataset(D_C3, rows_local * world, 1.0, SEED + 1,
+                                           ds_mod.Shard(rank, world, rank * rows_local,
+                                                        (rank + 1) * rows_local))
+        counts = torch.empty(D_C3, dtype=torch.uint64, device="cuda")
+        sums = torch.empty(D_C3, dtype=torch.uint64, device="cuda")
+
+        def step_gb():
+            ctx.call("skx_aggregate", C_ptr(gdat.fact_freq), C_ptr(gdat.qty), 8, rows_local, D_C3, 0,
+                     C_ptr(counts), C_ptr(sums), ctx.stream(), sync=False)
+            if dist_on:  # per-GPU partials combined with NCCL reduce (BASELINE config 3)
+                dist.reduce(counts.view(torch.int64), dst=0)
+                dist.reduce(sums.view(torch.int64), dst=0)
+        tg, per_g, _ = timed_launches(step_gb, args.steps, args.warmup, stream, dist_on)
+        ctx.sync()
+        tg = max_over_ranks(tg, dist_on)
+        gb_bytes = rows_local * 12 + D_C3 * 16
+        groupby = {"workload": "C3 group-by COUNT+SUM(int64 qty), D=2^24, s=1.0, reordered",
+                   "value": rows_local * world * args.steps / (tg * 1e-3), "unit": "rows/s",
+                   "ms_per_step": tg / args.steps,
+                   "roofline": {"bound": "hbm", "achieved": gb_bytes / (statistics.mean(per_g) * 1e-3) / 1e9,
+                                "peak": peak, "unit": "GB/s",
+                                "frac": gb_bytes / (statistics.mean(per_g) * 1e-3) / 1e9 / peak,
+                                "alg_bytes_per_step": gb_bytes}}
+        del gdat
+
+    if rank == 0:
+        line = {
+            "metric": "fact rows/s (skew-reordered FK-join gather)",
+            "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": "C2 large FK-join gather (BASELINE configs[1])", "domain": d,
+                       "rows_per_gpu": rows_local, "rows_total": n_total, "z": args.z,
+                       "value": "int64", "layout": "freq (skew-reordered)", "seed": SEED,
+                       "parallelism": f"dp{world} (fact rows sharded, dimension replicated)",
+                       "l2": "inputs larger than L2 (4 GiB FK + 8 GiB output + 1 GiB dim per step)",
+                       "gather_policy": args.policy},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_kind": peak_kind,
+                         "traffic": ncu_traffic("gather_c2"),
+                         "alg_bytes_per_launch": alg_bytes,
+                         "avg_launch_ms": statistics.mean(per)},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "setup_s": round(setup_s, 2),
+        }
+        line.update(extras)
+        if groupby:
+            line["groupby_c3"] = groupby
+        print(json.dumps(line), flush=True)
+    if dist_on:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def C_ptr(t):
+    import ctypes as C
+    return C.c_void_p(t.data_ptr())
+
+
+def main():
+    args = parse()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -198,9 +198,30 @@ int skx_aggregate_host(skx_ctx* ctx, const uint32_t* fact, const void* measure,
                        uint64_t* counts, uint64_t* sums);
 
 /* ---- tuning / evidence ---------------------------------------------------- *
- * L2 policy for dimension loads in gathers: 0 = default, 1 = evict_last on
- * dimension reads with evict_first on the streamed FK/output (default). */
+ * Cache policy of the gathers (materialize/recode/permute), a bit set:
+ *   1 = evict_first on the streamed FK/output, evict_last on dimension reads;
+ *   2 = hot prefix in shared memory: the leading dimension values (the most
+ *       popular ids after reordering) are staged per CTA and served on chip;
+ *   4 = L2 access-policy window (persisting) over the dimension bytes after
+ *       the shared-memory tier;
+ *   8 = dimension loads bypass L1 allocation;
+ *  16 = FK stream software-pipelined one iteration ahead;
+ *  32 = tiered: the reordered id selects the cache class of each dimension
+ *       load -- ids below t1 allocate in L1, ids below t2 are L2 evict_last,
+ *       colder ids are L2 evict_first and skip L1 (skx_set_gather_tiers). */
 int skx_set_gather_policy(skx_ctx* ctx, int policy);
+/* cudaLimitMaxL2FetchGranularity (32, 64 or 128 bytes): device-wide. */
+int skx_set_l2_fetch_granularity(skx_ctx* ctx, int bytes);
+/* Tier sizes: shared-memory tier (policy bit 2) capped at smem_bytes (0 = all
+ * opt-in shared memory); for policy bit 32, t1 = hot + l1_bytes / width and
+ * t2 = l2_fraction * L2 size / width. */
+int skx_set_gather_tiers(skx_ctx* ctx, uint64_t smem_bytes, uint64_t l1_bytes,
+                         double l2_fraction);
+/* cudaCtxResetPersistingL2Cache: demote lines left persisting by windows. */
+int skx_reset_persisting_l2(skx_ctx* ctx);
+/* info[0..n): num_sms, smem_optin, l2_bytes, persisting-L2 max, access-policy
+ * window max, current L2 fetch granularity. */
+int skx_device_info(skx_ctx* ctx, uint64_t* info, int n);
 
 #ifdef __cplusplus
 }

@@ -83,6 +83,7 @@ class Oracle:
         L.orc_random_bijection.argtypes = [u32, u64, vp]
         L.orc_generate_fact_column_rand.argtypes = [u32, u64, dbl, u64, vp, vp]
         L.orc_generate_zipf_counter.argtypes = [vp, u32, vp, u64, u64, u64, vp]
+        L.orc_generate_zipf_counter_mt.argtypes = [vp, u32, vp, u64, u64, vp, u32]
         L.orc_find_domain_violation.restype = u64
         L.orc_find_domain_violation.argtypes = [vp, u64, u64]
         L.orc_count_frequencies.argtypes = [vp, u64, u32, vp, vp, vp]
@@ -137,6 +138,13 @@ class Oracle:
         r2i = None if rank_to_id is None else _u32(rank_to_id)
         out = np.empty(n, np.uint32)
         self.L.orc_generate_zipf_counter(_p(cdf), len(cdf), _p(r2i), seed, row_begin, n, _p(out))
+        return out
+
+    def generate_zipf_counter_mt(self, cdf, rank_to_id, seed, n, threads):
+        cdf = np.ascontiguousarray(cdf, np.float64)
+        r2i = None if rank_to_id is None else _u32(rank_to_id)
+        out = np.empty(n, np.uint32)
+        self.L.orc_generate_zipf_counter_mt(_p(cdf), len(cdf), _p(r2i), seed, n, _p(out), threads)
         return out
 
     # -- index ----------------------------------------------------------------

@@ -425,3 +425,40 @@ uint64_t orc_unordered_checksum_u64(const uint64_t* v, uint64_t n) {
   for (uint64_t i = 0; i < n; ++i) h += orc_splitmix64(v[i]);
   return h;
 }
+
+/* Multithreaded orc_generate_zipf_counter (same values; rows split by
+ * chunk_spans) -- only so bench.py's CPU arm can build its bounded sample in
+ * seconds. */
+typedef struct {
+  const double* cdf;
+  uint32_t d;
+  const uint32_t* r2i;
+  uint64_t seed, b, e;
+  uint32_t* out;
+} gen_job;
+
+static void* gen_worker(void* p) {
+  gen_job* j = (gen_job*)p;
+  orc_generate_zipf_counter(j->cdf, j->d, j->r2i, j->seed, j->b, j->e - j->b, j->out + j->b);
+  return NULL;
+}
+
+void orc_generate_zipf_counter_mt(const double* cdf, uint32_t d, const uint32_t* rank_to_id,
+                                  uint64_t seed, uint64_t n, uint32_t* out, uint32_t threads) {
+  if (threads == 0) threads = 1;
+  uint64_t* bs = (uint64_t*)malloc(sizeof(uint64_t) * threads);
+  uint64_t* es = (uint64_t*)malloc(sizeof(uint64_t) * threads);
+  gen_job* jobs = (gen_job*)malloc(sizeof(gen_job) * threads);
+  pthread_t* tids = (pthread_t*)malloc(sizeof(pthread_t) * threads);
+  orc_chunk_spans(n, threads, bs, es);
+  for (uint32_t t = 0; t < threads; ++t) {
+    jobs[t] = (gen_job){cdf, d, rank_to_id, seed, bs[t], es[t], out};
+    if (t + 1 < threads) pthread_create(&tids[t], NULL, gen_worker, &jobs[t]);
+  }
+  gen_worker(&jobs[threads - 1]);
+  for (uint32_t t = 0; t + 1 < threads; ++t) pthread_join(tids[t], NULL);
+  free(bs);
+  free(es);
+  free(jobs);
+  free(tids);
+}

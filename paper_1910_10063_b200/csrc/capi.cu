@@ -83,6 +83,17 @@ int skx_ctx_create(int device, skx_ctx** out) {
   ctx->num_sms = prop.multiProcessorCount;
   ctx->smem_optin = prop.sharedMemPerBlockOptin;
   ctx->l2_bytes = prop.l2CacheSize;
+  // Limits for the optional persisting L2 window (gather policy bit 4).  The
+  // set-aside itself is only reserved while that bit is on: a reserved
+  // set-aside shrinks the L2 available to normal accesses (measured).
+  int pmax = 0, wmax = 0;
+  cudaDeviceGetAttribute(&pmax, cudaDevAttrMaxPersistingL2CacheSize, device);
+  cudaDeviceGetAttribute(&wmax, cudaDevAttrMaxAccessPolicyWindowSize, device);
+  if (pmax > 0 && wmax > 0) {
+    ctx->persist_max = (size_t)pmax;
+    ctx->window_max = (size_t)wmax;
+  }
+  cudaGetLastError();
   if (cudaMalloc(&ctx->err, sizeof(DevErr)) != cudaSuccess ||
       cudaMallocHost(&ctx->err_host, sizeof(DevErr)) != cudaSuccess) {
     delete ctx;
@@ -117,8 +128,49 @@ int skx_ctx_destroy(skx_ctx* ctx) {
 uint64_t skx_launch_count(const skx_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
 
 int skx_set_gather_policy(skx_ctx* ctx, int policy) {
-  if (!ctx || policy < 0 || policy > 1) return SKX_INVALID_ARGUMENT;
+  if (!ctx || policy < 0 || policy > 127) return SKX_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  const bool want = (policy & 4) != 0 && ctx->persist_max > 0;
+  if (want != ctx->setaside_on) {
+    cudaError_t e = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want ? ctx->persist_max : 0);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "set persisting L2 limit");
+    if (!want) cudaCtxResetPersistingL2Cache();
+    ctx->setaside_on = want;
+  }
   ctx->gather_policy = policy;
+  return SKX_OK;
+}
+
+int skx_set_gather_tiers(skx_ctx* ctx, uint64_t smem_bytes, uint64_t l1_bytes, double l2_fraction) {
+  if (!ctx || !(l2_fraction >= 0.0 && l2_fraction <= 1.0)) return SKX_INVALID_ARGUMENT;
+  ctx->tier_smem_bytes = smem_bytes;
+  ctx->tier_l1_bytes = l1_bytes;
+  ctx->tier_l2_frac = l2_fraction;
+  return SKX_OK;
+}
+
+int skx_reset_persisting_l2(skx_ctx* ctx) {
+  if (!ctx) return SKX_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  cudaError_t e = cudaCtxResetPersistingL2Cache();
+  return e == cudaSuccess ? SKX_OK : cuda_fail(ctx, e, "reset_persisting_l2");
+}
+
+int skx_set_l2_fetch_granularity(skx_ctx* ctx, int bytes) {
+  if (!ctx || (bytes != 32 && bytes != 64 && bytes != 128)) return SKX_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  cudaError_t e = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)bytes);
+  return e == cudaSuccess ? SKX_OK : cuda_fail(ctx, e, "set_l2_fetch_granularity");
+}
+
+int skx_device_info(skx_ctx* ctx, uint64_t* info, int n) {
+  // [num_sms, smem_optin, l2_bytes, persist_max, window_max, l2_fetch_granularity]
+  if (!ctx || !info) return SKX_INVALID_ARGUMENT;
+  size_t gran = 0;
+  cudaDeviceGetLimit(&gran, cudaLimitMaxL2FetchGranularity);
+  const uint64_t v[6] = {(uint64_t)ctx->num_sms, ctx->smem_optin, ctx->l2_bytes, ctx->persist_max,
+                         ctx->window_max, gran};
+  for (int i = 0; i < n && i < 6; ++i) info[i] = v[i];
   return SKX_OK;
 }
 

@@ -11,20 +11,48 @@
 // B200 design:
 //  * HBM roofline: algorithmic bytes per row = 4 (FK) + w (output).  The
 //    dimension reads are data-dependent and are what the skew-aware index
-//    turns into L2 hits: the reordered hot ids form a contiguous prefix.
+//    turns into on-chip hits: the reordered hot ids form a contiguous prefix.
 //  * FK stream: 128-bit ld.global.nc.L1::no_allocate with an L2 evict_first
-//    policy; output: 128-bit st.global with evict_first.  Dimension loads take
-//    the read-only path with L2 evict_last so the hot prefix survives the
-//    streams.
-//  * Each thread keeps UNROLL x 4 independent dimension loads in flight;
-//    persistent grid-stride loop, grid = 148 x resident blocks.
+//    policy; output: 128-bit st.global with evict_first.
+//  * Hot prefix (policy bit 2): the first `hot` dimension values are staged
+//    in shared memory once per CTA (one 1024-thread CTA per SM) and served
+//    from there -- a random shared load costs a few bank wavefronts where a
+//    random global load costs one L1TEX wavefront per lane.
+//  * Remaining dimension loads take the read-only path with L2 evict_last,
+//    optionally without L1 allocation and under an L2 persisting window.
+//  * Each thread keeps UNROLL x 4 independent loads in flight; persistent
+//    grid-stride loop.
 #include "skx_internal.cuh"
 
 namespace skx {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kUnroll = 4;  // uint4 FK vectors per thread per iteration (16 rows)
+constexpr int kThreads = 256;      // plain variant: several CTAs per SM
+constexpr int kThreadsHot = 1024;  // hot-prefix variant: one CTA per SM owns the smem copy
+constexpr int kUnroll = 4;         // uint4 FK vectors per thread per iteration (16 rows)
+
+// Policy bits (skx_set_gather_policy).
+constexpr int kPolHints = 1;   // evict_first streams, evict_last dimension
+constexpr int kPolHot = 2;     // shared-memory hot prefix
+constexpr int kPolWindow = 4;  // L2 persisting access-policy window over the dimension
+constexpr int kPolNoL1 = 8;    // dimension loads bypass L1 allocation
+constexpr int kPolPrefetch = 16;  // software-pipeline the FK stream one iteration ahead
+constexpr int kPolTiered = 32;    // per-access cache class from the reordered id (see below)
+
+// Cache tiers of a skew-reordered dimension (policy bit 32).  After the
+// index, popularity decreases with the id, so the id alone says how hot an
+// access is -- the GPU form of the paper's hot/cold threshold t
+// (§4.2.1, operators.cpp:68-85):
+//   idx <  hot: shared memory                          (policy bit 2)
+//   idx <  t1 : L1 evict_last,  L2 evict_last          (per-SM hot tier)
+//   idx <  t2 : L1 evict_first, L2 evict_last          (chip-wide warm tier)
+//   otherwise : L1 evict_first, L2 evict_first         (cold: must not evict
+//               the warmer tiers -- untiered, every cold miss displaces them)
+struct GatherTiers {
+  uint32_t hot;  // shared-memory tier (policy bit 2)
+  uint64_t t1;
+  uint64_t t2;
+};
 
 template <typename V>
 struct Pack4;  // 4 values of width V as 16B/8B stores
@@ -55,24 +83,104 @@ struct Pack4<uint16_t> {
   }
 };
 
+// Dimension load without L1 allocation (L2 evict_last).
+template <typename V>
+__device__ __forceinline__ V ld_dim_nol1(const V* p, uint64_t pol);
+template <>
+__device__ __forceinline__ uint32_t ld_dim_nol1<uint32_t>(const uint32_t* p, uint64_t pol) {
+  return ld_stream_u32(p, pol);
+}
+template <>
+__device__ __forceinline__ uint64_t ld_dim_nol1<uint64_t>(const uint64_t* p, uint64_t pol) {
+  return ld_stream_u64(p, pol);
+}
+template <>
+__device__ __forceinline__ uint16_t ld_dim_nol1<uint16_t>(const uint16_t* p, uint64_t pol) {
+  unsigned short r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;"
+               : "=h"(r)
+               : "l"(p), "l"(pol));
+  return r;
+}
+
+// Dimension load with an L1 eviction priority (allocating) and an L2 policy.
+template <typename V, bool LAST>
+__device__ __forceinline__ V ld_dim_l1p(const V* p, uint64_t pol) {
+  if constexpr (sizeof(V) == 8) {
+    uint64_t r;
+    if (LAST)
+      asm volatile("ld.global.nc.L1::evict_last.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(pol));
+    else
+      asm volatile("ld.global.nc.L1::evict_first.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(pol));
+    return (V)r;
+  } else if constexpr (sizeof(V) == 4) {
+    uint32_t r;
+    if (LAST)
+      asm volatile("ld.global.nc.L1::evict_last.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    else
+      asm volatile("ld.global.nc.L1::evict_first.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    return (V)r;
+  } else {
+    unsigned short r;
+    if (LAST)
+      asm volatile("ld.global.nc.L1::evict_last.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(r) : "l"(p), "l"(pol));
+    else
+      asm volatile("ld.global.nc.L1::evict_first.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(r) : "l"(p), "l"(pol));
+    return (V)r;
+  }
+}
+
 // Vector body: rows [head, head + 4*nvec) where fact + head is 16B aligned.
 // OUT_VEC: out + head is aligned for Pack4 stores.
-template <typename V, bool OUT_VEC, bool POL>
-__global__ void __launch_bounds__(kThreads)
+template <typename V, bool OUT_VEC, int F>
+__global__ void __launch_bounds__((F & kPolHot) ? kThreadsHot : kThreads, (F & kPolHot) ? 1 : 4)
     k_gather_vec(const uint32_t* __restrict__ fact, uint64_t head, uint64_t nvec,
-                 const V* __restrict__ dim, uint64_t dim_len, V* __restrict__ out, DevErr* err) {
+                 const V* __restrict__ dim, uint64_t dim_len, V* __restrict__ out, DevErr* err,
+                 GatherTiers tiers) {
+  constexpr bool HOT = (F & kPolHot) != 0;
+  constexpr bool HINTS = (F & kPolHints) != 0;
+  constexpr bool NOL1 = (F & kPolNoL1) != 0;
+  constexpr bool PREF = (F & kPolPrefetch) != 0;
+  constexpr bool TIER = (F & kPolTiered) != 0;
+  const uint32_t hot = tiers.hot;
+  constexpr int NT = HOT ? kThreadsHot : kThreads;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* s_hot = reinterpret_cast<V*>(smem_raw);
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_d = policy_evict_last();
+  if (HOT) {
+    // 16-byte cooperative copy of dim[0, hot) (hot * sizeof(V) is a multiple of 16).
+    const uint4* src = reinterpret_cast<const uint4*>(dim);
+    uint4* dst = reinterpret_cast<uint4*>(s_hot);
+    const uint32_t nv = (uint32_t)((uint64_t)hot * sizeof(V) / 16);
+    for (uint32_t i = threadIdx.x; i < nv; i += NT) dst[i] = __ldg(src + i);
+    __syncthreads();
+  }
   const uint4* fv = reinterpret_cast<const uint4*>(fact + head);
   V* o = out + head;
-  const uint64_t stride = (uint64_t)gridDim.x * kThreads * kUnroll;
-  for (uint64_t base = (uint64_t)blockIdx.x * kThreads * kUnroll + threadIdx.x; base < nvec;
-       base += stride) {
-    uint4 f[kUnroll];
+  const uint64_t stride = (uint64_t)gridDim.x * NT * kUnroll;
+  uint64_t base = (uint64_t)blockIdx.x * NT * kUnroll + threadIdx.x;
+  uint4 f[kUnroll];
+  uint64_t dbg = 0;
+  if (PREF) {
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const uint64_t vi = base + (uint64_t)u * kThreads;
+      const uint64_t vi = base + (uint64_t)u * NT;
       f[u] = vi < nvec ? ld_stream_v4(fv + vi, pol_s) : make_uint4(1, 1, 1, 1);
+    }
+  }
+  for (; base < nvec; base += stride) {
+    uint4 fn[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      // PREF: next iteration's FK vectors are in flight while this one's
+      // dimension loads resolve.
+      const uint64_t vi = PREF ? base + stride + (uint64_t)u * NT : base + (uint64_t)u * NT;
+      fn[u] = vi < nvec ? ld_stream_v4(fv + vi, pol_s) : make_uint4(1, 1, 1, 1);
+    }
+    if (!PREF) {
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) f[u] = fn[u];
     }
     V v[kUnroll][4];
 #pragma unroll
@@ -81,20 +189,33 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const uint32_t idx = ids[j] - 1u;
-        if (idx < dim_len) {
-          v[u][j] = ld_dim<V>(dim + idx, pol_d, POL);
+        if (HOT && idx < hot) {
+          v[u][j] = s_hot[idx];
+        } else if (idx < dim_len) {
+          if (TIER) {
+            if (idx < tiers.t1)
+              v[u][j] = ld_dim_l1p<V, true>(dim + idx, pol_d);
+            else
+              v[u][j] = ld_dim_l1p<V, false>(dim + idx, idx < tiers.t2 ? pol_d : pol_s);
+          } else if (NOL1) {
+            v[u][j] = ld_dim_nol1<V>(dim + idx, pol_d);
+          } else {
+            v[u][j] = ld_dim<V>(dim + idx, pol_d, HINTS);
+          }
         } else {
           v[u][j] = 0;
-          const uint64_t vi = base + (uint64_t)u * kThreads;
+          const uint64_t vi = base + (uint64_t)u * NT;
           if (vi < nvec) record_violation(err, head + vi * 4 + j, ids[j]);
         }
       }
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const uint64_t vi = base + (uint64_t)u * kThreads;
+      const uint64_t vi = base + (uint64_t)u * NT;
       if (vi < nvec) {
-        if (OUT_VEC) {
+        if (F & 64) {  // diagnostic: keep the loads, drop the output stream
+          dbg ^= (uint64_t)v[u][0] ^ (uint64_t)v[u][1] ^ (uint64_t)v[u][2] ^ (uint64_t)v[u][3];
+        } else if (OUT_VEC) {
           Pack4<V>::store(o + vi * 4, v[u], pol_s);
         } else {
 #pragma unroll
@@ -102,7 +223,12 @@ __global__ void __launch_bounds__(kThreads)
         }
       }
     }
+    if (PREF) {
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) f[u] = fn[u];
+    }
   }
+  if ((F & 64) && dbg == 0x5eed5eed5eedull) o[threadIdx.x] = (V)dbg;
 }
 
 // Scalar rows [b, e) -- the unaligned head and the ragged tail (< 4 rows each).
@@ -120,6 +246,61 @@ __global__ void k_gather_scalar(const uint32_t* __restrict__ fact, uint64_t b, u
     out[k] = 0;
     record_violation(err, k, id);
   }
+}
+
+template <typename V, bool OUT_VEC, int F>
+cudaError_t launch_vec(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64_t nvec,
+                       const V* dim, uint64_t dim_len, V* out, GatherTiers tiers, cudaStream_t s) {
+  const uint32_t hot = tiers.hot;
+  constexpr bool HOT = (F & kPolHot) != 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(HOT ? kThreadsHot : kThreads);
+  cfg.gridDim = dim3(HOT ? grid_for(ctx, nvec, kThreadsHot * kUnroll, 1)
+                         : grid_for(ctx, nvec, kThreads * kUnroll, 8));
+  cfg.dynamicSmemBytes = HOT ? (size_t)hot * sizeof(V) : 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  cfg.attrs = attr;
+  cfg.numAttrs = 0;
+  const uint64_t dim_bytes = dim_len * sizeof(V);
+  if ((F & kPolWindow) && ctx->persist_max > 0 && dim_bytes > cfg.dynamicSmemBytes) {
+    // Persist the bytes right after the shared-memory tier, as far as the
+    // L2 set-aside allows (hitRatio 1: a window no larger than the set-aside).
+    const uint64_t skip = cfg.dynamicSmemBytes & ~uint64_t(127);
+    uint64_t win = dim_bytes - skip;
+    const uint64_t cap = (uint64_t)((double)ctx->persist_max * ctx->tier_l2_frac);
+    if (win > cap) win = cap;
+    if (win > ctx->window_max) win = ctx->window_max;
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow.base_ptr =
+        const_cast<char*>(reinterpret_cast<const char*>(dim) + skip);
+    attr[0].val.accessPolicyWindow.num_bytes = (size_t)win;
+    attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
+    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.numAttrs = 1;
+  }
+  if (HOT)
+    cudaFuncSetAttribute(k_gather_vec<V, OUT_VEC, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)cfg.dynamicSmemBytes);
+  return cudaLaunchKernelEx(&cfg, k_gather_vec<V, OUT_VEC, F>, fact, head, nvec, dim, dim_len, out,
+                            ctx->err, tiers);
+}
+
+template <typename V, bool OUT_VEC>
+cudaError_t dispatch_vec(skx_ctx* ctx, int F, const uint32_t* fact, uint64_t head, uint64_t nvec,
+                         const V* dim, uint64_t dim_len, V* out, GatherTiers t, cudaStream_t s) {
+  // Bit 4 (window) is a launch attribute; instantiate the useful variants only.
+  const bool win = (F & kPolWindow) != 0;
+#define SKX_F(x)                                                                            \
+  if ((F & ~kPolWindow) == (x))                                                             \
+    return win ? launch_vec<V, OUT_VEC, (x) | kPolWindow>(ctx, fact, head, nvec, dim, dim_len, \
+                                                          out, t, s)                        \
+               : launch_vec<V, OUT_VEC, (x)>(ctx, fact, head, nvec, dim, dim_len, out, t, s);
+  SKX_F(0) SKX_F(1) SKX_F(3) SKX_F(9) SKX_F(17) SKX_F(19)
+  SKX_F(33) SKX_F(35) SKX_F(49) SKX_F(51) SKX_F(65) SKX_F(97) SKX_F(69)
+#undef SKX_F
+  return cudaErrorInvalidValue;
 }
 
 template <typename V>
@@ -140,19 +321,29 @@ int gather_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const V* dim, ui
   if (nvec > 0) {
     const uintptr_t oa = reinterpret_cast<uintptr_t>(out + head);
     const bool out_vec = (sizeof(V) == 2) ? (oa % 8 == 0) : (oa % 16 == 0);
-    const unsigned grid = grid_for(ctx, nvec, kThreads * kUnroll, 8);
-    const bool pol = ctx->gather_policy == 1;
-    if (out_vec) {
-      if (pol)
-        k_gather_vec<V, true, true><<<grid, kThreads, 0, s>>>(fact, head, nvec, dim, dim_len, out, ctx->err);
-      else
-        k_gather_vec<V, true, false><<<grid, kThreads, 0, s>>>(fact, head, nvec, dim, dim_len, out, ctx->err);
-    } else {
-      if (pol)
-        k_gather_vec<V, false, true><<<grid, kThreads, 0, s>>>(fact, head, nvec, dim, dim_len, out, ctx->err);
-      else
-        k_gather_vec<V, false, false><<<grid, kThreads, 0, s>>>(fact, head, nvec, dim, dim_len, out, ctx->err);
+    int F = ctx->gather_policy;
+    // Shared-memory tier: as many leading dimension values as fit.
+    uint32_t hot = 0;
+    if ((F & kPolHot) && (reinterpret_cast<uintptr_t>(dim) % 16) == 0) {
+      size_t budget = ctx->smem_optin > 4096 ? ctx->smem_optin - 4096 : 0;
+      if (ctx->tier_smem_bytes && ctx->tier_smem_bytes < budget) budget = ctx->tier_smem_bytes;
+      uint64_t h = budget / sizeof(V);
+      if (h > dim_len) h = dim_len;
+      h &= ~uint64_t(32 / sizeof(V) - 1);  // hot * sizeof(V) a multiple of 32
+      if (h >= 1024) hot = (uint32_t)h;
     }
+    if (!hot) F &= ~kPolHot;
+    GatherTiers t{hot, 0, 0};
+    if (F & kPolTiered) {
+      // t1: what one SM's L1 can hold (minus the smem tier); t2: the share of
+      // L2 the warm tier may occupy (the rest carries the streams).
+      t.t1 = hot + (uint64_t)ctx->tier_l1_bytes / sizeof(V);
+      t.t2 = (uint64_t)((double)ctx->l2_bytes * ctx->tier_l2_frac) / sizeof(V);
+    }
+    const cudaError_t e =
+        out_vec ? dispatch_vec<V, true>(ctx, F, fact, head, nvec, dim, dim_len, out, t, s)
+                : dispatch_vec<V, false>(ctx, F, fact, head, nvec, dim, dim_len, out, t, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "gather launch");
     ctx->launches++;
   }
   if (tail_b < n) {

@@ -139,6 +139,12 @@ struct skx_ctx {
   skx::DevErr* err_host = nullptr;  // pinned mirror
   uint64_t last_domain = 0;
   int gather_policy = 1;
+  size_t persist_max = 0;  // cudaDevAttrMaxPersistingL2CacheSize (0: no windows)
+  size_t window_max = 0;   // cudaDevAttrMaxAccessPolicyWindowSize
+  bool setaside_on = false;  // cudaLimitPersistingL2CacheSize currently reserved
+  size_t tier_smem_bytes = 0;         // gather shared-memory tier cap (0: all opt-in smem)
+  size_t tier_l1_bytes = 160 * 1024;  // gather tier t1 (bytes of the dimension prefix)
+  double tier_l2_frac = 0.6;          // gather tier t2 (share of L2)
   std::atomic<uint64_t> launches{0};
   skx_error_info last{};
   // scratch arenas (grow-only)
