@@ -18,6 +18,8 @@
 //   4. at exit the table is flushed with one global red.add per live slot.
 // The FK column is streamed once with 128-bit evict_first loads; the domain
 // check is fused (first bad row via atomicMin, reported at skx_sync).
+#include <cstdlib>
+
 #include "skx_internal.cuh"
 
 namespace skx {
@@ -74,7 +76,8 @@ __device__ __forceinline__ void count_one(uint32_t id, bool valid, uint32_t* key
 template <typename CT>
 __global__ void __launch_bounds__(kThreads)
     k_histogram(const uint32_t* __restrict__ fact, uint64_t head, uint64_t nvec, uint64_t n,
-                uint32_t d, CT* __restrict__ counts, DevErr* err) {
+                uint32_t d, uint32_t lo, uint32_t hi, bool check, CT* __restrict__ counts,
+                DevErr* err) {
   extern __shared__ uint32_t smem_tab[];
   uint32_t* keys = smem_tab;
   uint32_t* cnts = smem_tab + kTable;
@@ -104,9 +107,9 @@ __global__ void __launch_bounds__(kThreads)
       const uint32_t ids[4] = {f[u].x, f[u].y, f[u].z, f[u].w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const bool ok = (ids[j] - 1u) < d;
-        if (live && !ok) record_violation(err, head + vi * 4 + j, ids[j]);
-        count_one<CT>(ids[j], live && ok, keys, cnts, counts);
+        const uint32_t idx = ids[j] - 1u;
+        if (check && live && idx >= d) record_violation(err, head + vi * 4 + j, ids[j]);
+        count_one<CT>(ids[j], live && idx >= lo && idx < hi, keys, cnts, counts);
       }
     }
   }
@@ -120,9 +123,9 @@ __global__ void __launch_bounds__(kThreads)
       bool live = t < extra;
       if (live) k = t < head ? t : tail_b + (t - head);
       const uint32_t id = live ? fact[k] : 0u;
-      const bool ok = (id - 1u) < d;
-      if (live && !ok) record_violation(err, k, id);
-      count_one<CT>(id, live && ok, keys, cnts, counts);
+      const uint32_t idx = id - 1u;
+      if (check && live && idx >= d) record_violation(err, k, id);
+      count_one<CT>(id, live && idx >= lo && idx < hi, keys, cnts, counts);
     }
   }
   __syncthreads();
@@ -153,13 +156,27 @@ int launch_histogram(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint32_t d,
     cudaFuncSetAttribute(k_histogram<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   else
     cudaFuncSetAttribute(k_histogram<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (counter_bytes == 4)
-    k_histogram<uint32_t><<<grid, kThreads, smem, s>>>(fact, head, nvec, n, d,
-                                                    static_cast<uint32_t*>(counts), ctx->err);
-  else
-    k_histogram<unsigned long long><<<grid, kThreads, smem, s>>>(
-        fact, head, nvec, n, d, static_cast<unsigned long long*>(counts), ctx->err);
-  ctx->launches++;
+  // Optional key-range passes (SKX_HIST_RANGE ids per pass): each pass only
+  // updates counters of ids in [lo, hi) so cold-key atomics stay in L2, at
+  // the price of re-streaming the FK column per pass.  Measured on B200
+  // (profiles/): one pass wins at BASELINE sizes (D=2^26: 6.96 ms single vs
+  // 11.1 ms with 16M-key passes), so the default is a single pass.
+  uint64_t range = (uint64_t)d + 1;
+  if (const char* ev = getenv("SKX_HIST_RANGE")) range = strtoull(ev, nullptr, 10);
+  if (range < (1u << 20)) range = 1u << 20;
+  for (uint64_t lo = 0; lo < d || lo == 0; lo += range) {
+    const uint32_t hi = (uint32_t)((lo + range < d) ? lo + range : d);
+    const bool check = lo == 0;
+    if (counter_bytes == 4)
+      k_histogram<uint32_t><<<grid, kThreads, smem, s>>>(fact, head, nvec, n, d, (uint32_t)lo, hi,
+                                                         check, static_cast<uint32_t*>(counts), ctx->err);
+    else
+      k_histogram<unsigned long long><<<grid, kThreads, smem, s>>>(
+          fact, head, nvec, n, d, (uint32_t)lo, hi, check,
+          static_cast<unsigned long long*>(counts), ctx->err);
+    ctx->launches++;
+    if (hi >= d) break;
+  }
   SKX_CHECK_LAUNCH(ctx, "histogram");
   return SKX_OK;
 }

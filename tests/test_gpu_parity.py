@@ -268,3 +268,23 @@ def test_reorder_invariants_at_scale(sx):
     assert torch.equal(c_freq, c_rand[off - 1])
     assert bool((c_freq[:-1] >= c_freq[1:]).all())  # frequency-sorted
     assert int(c_freq.sum()) == n
+
+
+def test_aggregate_packed_tail_exactness(sx):
+    """The packed tail accumulator (count << 40 | sum) must stay exact through
+    sum-field carries, count-field wraps and wide (>= 2^32) measures."""
+    n = (1 << 24) + 1000
+    fact = torch.full((n,), 2, dtype=torch.int32, device="cuda").view(torch.uint32)
+    meas = torch.full((n,), 2**32 - 1, dtype=torch.int64, device="cuda")
+    c, s = sx.aggregate_count_sum(fact, meas, 3, hot_threshold=1)  # id 2 is a tail key
+    assert int(c[1].item()) == n
+    assert int(s[1].view(torch.int64).item()) & (2**64 - 1) == (n * (2**32 - 1)) % 2**64
+    rng = np.random.default_rng(8)
+    m = rng.integers(0, 2**63, size=200000, dtype=np.int64)
+    m[::3] = rng.integers(0, 100, size=len(m[::3]))
+    f = rng.integers(1, 50, size=200000, dtype=np.uint32)
+    c, s = sx.aggregate_count_sum(cu(f), cu(m), 49, hot_threshold=5)
+    ce = np.bincount(f.astype(np.int64) - 1, minlength=49).astype(np.uint64)
+    se = np.zeros(49, np.uint64)
+    np.add.at(se, f.astype(np.int64) - 1, m.view(np.uint64))
+    assert np.array_equal(np_(c), ce) and np.array_equal(np_(s), se)
