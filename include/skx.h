@@ -72,6 +72,18 @@ int skx_last_error(const skx_ctx* ctx, skx_error_info* info);
 /* Number of kernels this context has launched since creation (bench evidence). */
 uint64_t skx_launch_count(const skx_ctx* ctx);
 
+/* ---- device memory for host-side callers (the C++ drop-in) --------------- */
+int skx_device_alloc(skx_ctx* ctx, uint64_t bytes, void** ptr);
+int skx_device_free(skx_ctx* ctx, void* ptr);
+/* Synchronous copies on the context's device. */
+int skx_copy_to_device(skx_ctx* ctx, void* dst, const void* src, uint64_t bytes);
+int skx_copy_to_host(skx_ctx* ctx, void* dst, const void* src, uint64_t bytes);
+
+/* find_domain_violation (operators.cpp:32-41): *row_out (host) = the first k
+ * with fact[k]-1 >= d, or UINT64_MAX.  Synchronous. */
+int skx_find_domain_violation(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint64_t d,
+                              uint64_t* row_out);
+
 /* ---- Q1 gather: out[k] = dim[fact[k]-1] --------------------------------- *
  * Replaces KernelTable::gather_u32 (kernels.hpp:21-23; scalar.cpp:13-29,
  * avx2.cpp:43-57) and the operator materialize() (operators.cpp:60-66) /

@@ -38,6 +38,8 @@ def build(ref: bool = True) -> None:
     targets = ["oracle"]
     if ref and os.path.isdir("/root/reference/proj/src"):
         targets.append("ref")
+        if os.path.exists(os.path.join(HERE, "..", "paper_1910_10063_b200", "libskewdx_b200.so")):
+            targets.append("refsuite")
     subprocess.check_call(["make", "-s", "-C", HERE, *targets])
 
 

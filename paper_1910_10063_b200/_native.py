@@ -62,6 +62,11 @@ SIGNATURES = {
     "skx_device_info": (_int, [_vp, _vp, _int]),
     "skx_reset_persisting_l2": (_int, [_vp]),
     "skx_set_gather_tiers": (_int, [_vp, _u64, _u64, _dbl]),
+    "skx_device_alloc": (_int, [_vp, _u64, C.POINTER(_vp)]),
+    "skx_device_free": (_int, [_vp, _vp]),
+    "skx_copy_to_device": (_int, [_vp, _vp, _vp, _u64]),
+    "skx_copy_to_host": (_int, [_vp, _vp, _vp, _u64]),
+    "skx_find_domain_violation": (_int, [_vp, _vp, _u64, _u64, C.POINTER(_u64)]),
     "skx_fill_column": (_int, [_vp, _int, _int, _u64, _u64, _dbl, _dbl, _vp, _vp]),
 }
 

@@ -73,12 +73,13 @@ def build_libskx(force: bool = False, verbose: bool = False) -> str:
 def build_shim(force: bool = False) -> str:
     """C++ drop-in (namespace skewdx, reference signatures) over the C-ABI."""
     src = os.path.join(CPP, "skewdx_b200.cpp")
-    hdr = os.path.join(CPP, "skewdx_b200.hpp")
+    hdrs = glob.glob(os.path.join(CPP, "include", "skewdx", "*.hpp"))
     if not os.path.exists(src):
         return ""
-    if force or _stale(LIBSHIM, [src, hdr, LIBSKX]):
+    if force or _stale(LIBSHIM, [src, *hdrs, LIBSKX, os.path.join(INCLUDE, "skx.h")]):
         _run(["g++", "-O2", "-std=c++20", "-fPIC", "-shared", "-Wall", "-Wextra", "-I" + INCLUDE,
-              "-I" + CPP, src, "-o", LIBSHIM, "-L" + PKG, "-lskx", "-Wl,-rpath,$ORIGIN"])
+              "-I" + os.path.join(CPP, "include"), src, "-o", LIBSHIM, "-L" + PKG, "-lskx",
+              "-Wl,-rpath,$ORIGIN"])
     return LIBSHIM
 
 

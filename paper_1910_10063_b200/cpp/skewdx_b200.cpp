@@ -1,0 +1,576 @@
+// skewdx_b200.cpp -- the C++ drop-in for the reference library's operator
+// API (namespace skewdx; headers in cpp/include/skewdx/), backed by the B200
+// kernels through the C-ABI of include/skx.h.
+//
+// A reference caller keeps its code and links libskewdx_b200.so instead of
+// libskewdx.a: every hot-path function stages its host vectors to the
+// device, runs the libskx kernel, synchronises, rethrows libskx statuses as
+// the reference's exception types (error.hpp) and copies the result back.
+// There is no CPU implementation of any hot-path operator here; host code is
+// limited to argument validation (same order as the reference), result
+// ordering, the generator fixture, file formats and plan arithmetic.
+#include <algorithm>
+#include <array>
+#include <bit>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <numeric>
+#include <random>
+
+#include "skewdx/column.hpp"
+#include "skewdx/column_io.hpp"
+#include "skewdx/error.hpp"
+#include "skewdx/mix.hpp"
+#include "skewdx/operators.hpp"
+#include "skewdx/parallel.hpp"
+#include "skewdx/permindex.hpp"
+#include "skx.h"
+
+namespace skewdx {
+namespace {
+
+// ---- libskx plumbing --------------------------------------------------------
+struct Ctx {
+  skx_ctx* h = nullptr;
+  Ctx() {
+    const char* dev = std::getenv("SKX_DEVICE");
+    if (skx_ctx_create(dev ? std::atoi(dev) : 0, &h) != SKX_OK || !h)
+      throw Error("libskx: no usable sm_100 device (there is no CPU fallback)");
+  }
+  ~Ctx() { skx_ctx_destroy(h); }
+};
+
+skx_ctx* ctx() {
+  thread_local Ctx c;
+  return c.h;
+}
+
+[[noreturn]] void raise(int status) {
+  skx_error_info info{};
+  skx_last_error(ctx(), &info);
+  switch (status) {
+    case SKX_DOMAIN_VIOLATION:
+      throw DomainViolation(info.row, info.value, info.domain);
+    case SKX_INVALID_ARGUMENT:
+      throw InvalidArgument(info.message);
+    default:
+      throw Error(std::string("libskx: ") + info.message);
+  }
+}
+
+void check(int status) {
+  if (status != SKX_OK) raise(status);
+}
+
+// Enqueued operator + deferred device errors, reported like the reference.
+void run(int status) {
+  check(status);
+  check(skx_sync(ctx(), nullptr));
+}
+
+class DevBuf {
+ public:
+  explicit DevBuf(std::uint64_t bytes) { check(skx_device_alloc(ctx(), bytes, &p_)); }
+  template <typename T>
+  explicit DevBuf(const std::vector<T>& v) : DevBuf(v.size() * sizeof(T)) {
+    check(skx_copy_to_device(ctx(), p_, v.data(), v.size() * sizeof(T)));
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { skx_device_free(ctx(), p_); }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p_);
+  }
+  template <typename T>
+  void to(std::vector<T>& v) const {
+    check(skx_copy_to_host(ctx(), v.data(), p_, v.size() * sizeof(T)));
+  }
+
+ private:
+  void* p_ = nullptr;
+};
+
+void require_in_domain(const Column& fact, std::uint64_t domain) {
+  if (fact.empty()) return;
+  DevBuf f(fact);
+  std::uint64_t row = ~0ull;
+  check(skx_find_domain_violation(ctx(), f.as<std::uint32_t>(), fact.size(), domain, &row));
+  if (row != ~0ull) throw DomainViolation(row, fact[row], domain);
+}
+
+Column gather(const Column& fact, const Column& dim) {
+  Column out(fact.size());
+  if (fact.empty()) return out;
+  DevBuf f(fact), d(dim), o(out.size() * 4);
+  run(skx_gather_u32(ctx(), f.as<std::uint32_t>(), fact.size(), d.as<std::uint32_t>(), dim.size(),
+                     o.as<std::uint32_t>(), nullptr));
+  o.to(out);
+  return out;
+}
+
+std::vector<std::uint64_t> device_counts(const Column& fact, std::uint32_t d, std::uint32_t hot) {
+  std::vector<std::uint64_t> counts(d, 0);
+  if (d == 0) {
+    require_in_domain(fact, 0);
+    return counts;
+  }
+  DevBuf f(std::max<std::uint64_t>(fact.size(), 1) * 4), c(std::uint64_t{d} * 8);
+  if (!fact.empty()) check(skx_copy_to_device(ctx(), f.as<void>(), fact.data(), fact.size() * 4));
+  run(skx_aggregate(ctx(), f.as<std::uint32_t>(), nullptr, 0, fact.size(), d, hot,
+                    c.as<std::uint64_t>(), nullptr, nullptr));
+  c.to(counts);
+  return counts;
+}
+
+bool by_count_then_id(const std::pair<std::uint32_t, std::uint64_t>& a,
+                      const std::pair<std::uint32_t, std::uint64_t>& b) {
+  return a.second != b.second ? a.second > b.second : a.first < b.first;
+}
+
+// ---- little-endian container files (SKDX / SKC8 / SKPI) ----------------------
+constexpr std::uint32_t kVersion = 1;
+
+template <typename T>
+void write_payload(const std::filesystem::path& path, const char (&magic)[5], std::uint64_t count,
+                   const T* data, const T* second = nullptr) {
+  std::ofstream f(path, std::ios::binary | std::ios::trunc);
+  if (!f) throw IoError("cannot open for writing: " + path.string());
+  f.write(magic, 4);
+  f.write(reinterpret_cast<const char*>(&kVersion), 4);
+  f.write(reinterpret_cast<const char*>(&count), 8);
+  f.write(reinterpret_cast<const char*>(data), static_cast<std::streamsize>(count * sizeof(T)));
+  if (second)
+    f.write(reinterpret_cast<const char*>(second), static_cast<std::streamsize>(count * sizeof(T)));
+  if (!f) throw IoError("write failed: " + path.string());
+}
+
+std::uint64_t read_header(std::ifstream& f, const std::filesystem::path& path,
+                          const char (&magic)[5]) {
+  char m[4] = {};
+  std::uint32_t version = 0;
+  std::uint64_t count = 0;
+  f.read(m, 4);
+  f.read(reinterpret_cast<char*>(&version), 4);
+  f.read(reinterpret_cast<char*>(&count), 8);
+  if (!f) throw FormatError("truncated header: " + path.string());
+  if (std::memcmp(m, magic, 4) != 0) throw FormatError("bad magic in " + path.string());
+  if (version != kVersion)
+    throw FormatError("unsupported format version " + std::to_string(version) + " in " +
+                      path.string());
+  return count;
+}
+
+template <typename T>
+std::vector<T> read_payload(const std::filesystem::path& path, const char (&magic)[5]) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) throw IoError("cannot open for reading: " + path.string());
+  const std::uint64_t count = read_header(f, path, magic);
+  const auto here = f.tellg();
+  f.seekg(0, std::ios::end);
+  const auto bytes = static_cast<std::uint64_t>(f.tellg() - here);
+  if (bytes != count * sizeof(T)) throw FormatError("length mismatch against header in " + path.string());
+  f.seekg(here);
+  std::vector<T> v(count);
+  f.read(reinterpret_cast<char*>(v.data()), static_cast<std::streamsize>(bytes));
+  if (!f && count) throw FormatError("length mismatch against header in " + path.string());
+  return v;
+}
+
+}  // namespace
+
+// ---- column.hpp ---------------------------------------------------------------
+const char* to_string(Layout layout) noexcept { return layout == Layout::freq ? "freq" : "rand"; }
+
+static void validate_spec(const ZipfSpec& s) {
+  if (s.domain_cardinality == 0) throw InvalidArgument("zipf spec: domain cardinality must be at least 1");
+  if (s.domain_cardinality > kMaxDomainCardinality)
+    throw InvalidArgument("zipf spec: domain cardinality exceeds the 32-bit identifier space");
+  if (s.tuple_count == 0) throw InvalidArgument("zipf spec: tuple count must be at least 1");
+  if (!(s.z >= 0.0)) throw InvalidArgument("zipf spec: exponent must be non-negative");
+}
+
+std::vector<double> zipf_frequencies(const ZipfSpec& spec) {
+  validate_spec(spec);
+  std::vector<double> cdf(spec.domain_cardinality);
+  // skx_zipf_cdf_host returns the partial sums; undo them into frequencies is
+  // lossy, so restate the Kahan-normalised weights directly (column.cpp:44-60).
+  double sum = 0.0, comp = 0.0;
+  for (std::uint32_t r = 1; r <= spec.domain_cardinality; ++r) {
+    const double w = std::pow(static_cast<double>(r), -spec.z);
+    cdf[r - 1] = w;
+    const double y = w - comp, t = sum + y;
+    comp = (t - sum) - y;
+    sum = t;
+  }
+  for (double& x : cdf) x /= sum;
+  return cdf;
+}
+
+std::vector<std::uint32_t> random_bijection(std::uint32_t n, std::uint64_t seed) {
+  std::vector<std::uint32_t> map(n);
+  if (n) check(skx_random_bijection_host(n, seed, map.data()));
+  return map;
+}
+
+GeneratedColumn generate_fact_column(const ZipfSpec& spec, Layout layout) {
+  validate_spec(spec);
+  const std::uint32_t d = spec.domain_cardinality;
+  std::vector<double> cdf(d);
+  check(skx_zipf_cdf_host(d, spec.z, cdf.data()));
+  // Sequential draws exactly as column.cpp:85-95 (mt19937_64 stream).
+  std::mt19937_64 rng(splitmix64(spec.seed ^ 0x5ca1ab1eull));
+  std::vector<std::uint32_t> drawn(spec.tuple_count);
+  std::vector<std::uint64_t> per_rank(d, 0);
+  for (auto& r : drawn) {
+    const double u = static_cast<double>(rng() >> 11) * 0x1.0p-53;
+    std::uint32_t rank = static_cast<std::uint32_t>(std::upper_bound(cdf.begin(), cdf.end(), u) - cdf.begin());
+    if (rank >= d) rank = d - 1;
+    r = rank;
+    ++per_rank[rank];
+  }
+  std::vector<std::uint32_t> rank_to_id;
+  if (layout == Layout::rand) {
+    rank_to_id = random_bijection(d, spec.seed);
+  } else {
+    std::vector<std::uint32_t> order(d);
+    std::iota(order.begin(), order.end(), 0u);
+    std::sort(order.begin(), order.end(), [&](std::uint32_t a, std::uint32_t b) {
+      return per_rank[a] != per_rank[b] ? per_rank[a] > per_rank[b] : a < b;
+    });
+    rank_to_id.resize(d);
+    for (std::uint32_t pos = 0; pos < d; ++pos) rank_to_id[order[pos]] = pos + 1;
+  }
+  GeneratedColumn g;
+  g.values.resize(spec.tuple_count);
+  g.ground_truth_counts.assign(d, 0);
+  for (std::uint64_t k = 0; k < spec.tuple_count; ++k) g.values[k] = rank_to_id[drawn[k]];
+  for (std::uint32_t r = 0; r < d; ++r) g.ground_truth_counts[rank_to_id[r] - 1] = per_rank[r];
+  return g;
+}
+
+// ---- column_io.hpp ----------------------------------------------------------
+void write_column(const std::filesystem::path& path, const Column& column) {
+  write_payload(path, "SKDX", column.size(), column.data());
+}
+Column read_column(const std::filesystem::path& path) {
+  return read_payload<std::uint32_t>(path, "SKDX");
+}
+void write_u64_array(const std::filesystem::path& path, std::span<const std::uint64_t> values) {
+  write_payload(path, "SKC8", values.size(), values.data());
+}
+std::vector<std::uint64_t> read_u64_array(const std::filesystem::path& path) {
+  return read_payload<std::uint64_t>(path, "SKC8");
+}
+
+// ---- permindex.hpp (GPU) -------------------------------------------------------
+FrequencyProfile count_frequencies(const Column& fact, std::uint32_t domain_cardinality) {
+  FrequencyProfile p;
+  p.total = fact.size();
+  p.counts.assign(domain_cardinality, 0);
+  if (fact.empty()) return p;
+  DevBuf f(fact), c(std::max<std::uint64_t>(domain_cardinality, 1) * 8);
+  run(skx_count_frequencies(ctx(), f.as<std::uint32_t>(), fact.size(), domain_cardinality,
+                            c.as<std::uint64_t>(), nullptr));
+  c.to(p.counts);
+  return p;
+}
+
+PermutationIndex build_index(const FrequencyProfile& profile) {
+  if (profile.counts.size() > kMaxDomainCardinality)
+    throw InvalidArgument("frequency profile exceeds the 32-bit identifier space");
+  const std::uint32_t d = static_cast<std::uint32_t>(profile.counts.size());
+  PermutationIndex idx;
+  idx.offsets.resize(d);
+  idx.ranks.resize(d);
+  DevBuf c(std::max<std::uint64_t>(d, 1) * 8), off(std::max<std::uint64_t>(d, 1) * 4),
+      rk(std::max<std::uint64_t>(d, 1) * 4);
+  if (d) check(skx_copy_to_device(ctx(), c.as<void>(), profile.counts.data(), std::uint64_t{d} * 8));
+  run(skx_build_index(ctx(), c.as<std::uint64_t>(), d, profile.total, off.as<std::uint32_t>(),
+                      rk.as<std::uint32_t>(), nullptr));
+  off.to(idx.offsets);
+  rk.to(idx.ranks);
+  return idx;
+}
+
+PermutationIndex rebuild(const Column& fact, std::uint32_t domain_cardinality) {
+  const std::uint32_t d = domain_cardinality;
+  PermutationIndex idx;
+  idx.offsets.resize(d);
+  idx.ranks.resize(d);
+  DevBuf f(std::max<std::uint64_t>(fact.size(), 1) * 4), off(std::max<std::uint64_t>(d, 1) * 4),
+      rk(std::max<std::uint64_t>(d, 1) * 4);
+  if (!fact.empty()) check(skx_copy_to_device(ctx(), f.as<void>(), fact.data(), fact.size() * 4));
+  run(skx_rebuild(ctx(), f.as<std::uint32_t>(), fact.size(), d, off.as<std::uint32_t>(),
+                  rk.as<std::uint32_t>(), nullptr));
+  off.to(idx.offsets);
+  rk.to(idx.ranks);
+  return idx;
+}
+
+Column recode_fact(const Column& fact, const PermutationIndex& index) {
+  return materialize(fact, index.ranks);  // permindex.cpp:60-64
+}
+
+Column permute_dimension(const Column& dim, const PermutationIndex& index) {
+  if (dim.size() != index.offsets.size())
+    throw InvalidArgument("dimension length " + std::to_string(dim.size()) +
+                          " does not match index cardinality " +
+                          std::to_string(index.offsets.size()));
+  Column out(dim.size());
+  if (dim.empty()) return out;
+  DevBuf dm(dim), off(index.offsets), o(dim.size() * 4);
+  run(skx_permute_dimension_u32(ctx(), dm.as<std::uint32_t>(), dim.size(), off.as<std::uint32_t>(),
+                                index.domain_cardinality(), o.as<std::uint32_t>(), nullptr));
+  o.to(out);
+  return out;
+}
+
+std::uint32_t append_dimension_row(PermutationIndex& index) {
+  const std::uint32_t d = index.domain_cardinality();
+  if (d >= kMaxDomainCardinality) throw Error("identifier space exhausted");
+  index.offsets.push_back(d + 1);  // least-frequent item: rank == id
+  index.ranks.push_back(d + 1);
+  return d + 1;
+}
+
+void write_index(const std::filesystem::path& path, const PermutationIndex& index) {
+  write_payload(path, "SKPI", index.offsets.size(), index.offsets.data(), index.ranks.data());
+}
+
+PermutationIndex read_index(const std::filesystem::path& path) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) throw IoError("cannot open for reading: " + path.string());
+  const std::uint64_t d = read_header(f, path, "SKPI");
+  if (d > kMaxDomainCardinality) throw FormatError("index cardinality out of range in " + path.string());
+  PermutationIndex idx;
+  idx.offsets.resize(d);
+  idx.ranks.resize(d);
+  f.read(reinterpret_cast<char*>(idx.offsets.data()), static_cast<std::streamsize>(d * 4));
+  f.read(reinterpret_cast<char*>(idx.ranks.data()), static_cast<std::streamsize>(d * 4));
+  if (!f && d) throw FormatError("length mismatch against header in " + path.string());
+  for (std::uint64_t r = 0; r < d; ++r) {
+    const std::uint32_t id = idx.offsets[r];
+    if (id == 0 || id > d || idx.ranks[id - 1] != r + 1)
+      throw FormatError("offsets/ranks are not inverse bijections in " + path.string());
+  }
+  return idx;
+}
+
+// ---- operators.hpp (GPU) -------------------------------------------------------
+std::uint64_t Bitmap::count() const noexcept {
+  std::uint64_t c = 0;
+  for (const std::uint64_t w : words_) c += static_cast<std::uint64_t>(std::popcount(w));
+  return c;
+}
+
+Bitmap permute_bitmap(const Bitmap& bitmap, const PermutationIndex& index) {
+  if (bitmap.size() != index.offsets.size())
+    throw InvalidArgument("bitmap size does not match index cardinality");
+  Bitmap out(bitmap.size());
+  if (bitmap.size() == 0) return out;
+  const std::uint64_t nw = (bitmap.size() + 63) / 64;
+  DevBuf in(nw * 8), off(index.offsets), o(nw * 8);
+  check(skx_copy_to_device(ctx(), in.as<void>(), bitmap.words(), nw * 8));
+  run(skx_permute_bitmap(ctx(), in.as<std::uint64_t>(), bitmap.size(), off.as<std::uint32_t>(),
+                         index.domain_cardinality(), o.as<std::uint64_t>(), nullptr));
+  check(skx_copy_to_host(ctx(), out.mutable_words(), o.as<void>(), nw * 8));
+  return out;
+}
+
+std::size_t find_domain_violation(const Column& fact, std::uint64_t domain_cardinality) noexcept {
+  if (fact.empty()) return knpos;
+  DevBuf f(fact);
+  std::uint64_t row = ~0ull;
+  if (skx_find_domain_violation(ctx(), f.as<std::uint32_t>(), fact.size(), domain_cardinality,
+                                &row) != SKX_OK) {
+    std::fprintf(stderr, "skewdx_b200: find_domain_violation failed on the device\n");
+    std::abort();  // noexcept contract; no CPU fallback
+  }
+  return row == ~0ull ? knpos : static_cast<std::size_t>(row);
+}
+
+Column materialize(const Column& fact, const Column& dim, int /*prefetch_distance*/) {
+  return gather(fact, dim);
+}
+
+Column materialize_split(const Column& fact, const Column& dim, SplitThreshold threshold) {
+  // The two-pass split is a CPU latency trick (operators.cpp:68-85); on the
+  // GPU the hot prefix lives in L1/L2 and one pass gives the same result.
+  if (threshold.t == 0 || threshold.t > dim.size())
+    throw InvalidArgument("split threshold must lie in 1..D");
+  return gather(fact, dim);
+}
+
+std::vector<std::uint32_t> select(const Column& fact, const Bitmap& bitmap) {
+  if (fact.size() > 0xFFFFFFFFull) throw InvalidArgument("select: fact row offsets exceed 32 bits");
+  if (fact.empty()) return {};
+  const std::uint64_t nw = std::max<std::uint64_t>((bitmap.size() + 63) / 64, 1);
+  DevBuf f(fact), w(nw * 8), o(fact.size() * 4), cnt(8);
+  if (bitmap.size()) check(skx_copy_to_device(ctx(), w.as<void>(), bitmap.words(), ((bitmap.size() + 63) / 64) * 8));
+  run(skx_select_offsets(ctx(), f.as<std::uint32_t>(), fact.size(), w.as<std::uint64_t>(),
+                         bitmap.size(), 0, o.as<std::uint32_t>(), cnt.as<std::uint64_t>(), nullptr));
+  std::uint64_t n = 0;
+  check(skx_copy_to_host(ctx(), &n, cnt.as<void>(), 8));
+  std::vector<std::uint32_t> out(n);
+  if (n) check(skx_copy_to_host(ctx(), out.data(), o.as<void>(), n * 4));
+  return out;
+}
+
+std::vector<std::uint64_t> aggregate_count(const Column& fact, std::uint32_t domain_cardinality) {
+  return device_counts(fact, domain_cardinality, 0);
+}
+
+std::vector<std::uint64_t> aggregate_sum(const Column& fact, const Column& measure,
+                                         std::uint32_t domain_cardinality) {
+  if (measure.size() != fact.size())
+    throw InvalidArgument("aggregate_sum: measure length does not match fact length");
+  std::vector<std::uint64_t> sums(domain_cardinality, 0);
+  if (domain_cardinality == 0) {
+    require_in_domain(fact, 0);
+    return sums;
+  }
+  const std::uint64_t rows = std::max<std::uint64_t>(fact.size(), 1);
+  DevBuf f(rows * 4), m(rows * 4), s(std::uint64_t{domain_cardinality} * 8);
+  if (!fact.empty()) {
+    check(skx_copy_to_device(ctx(), f.as<void>(), fact.data(), fact.size() * 4));
+    check(skx_copy_to_device(ctx(), m.as<void>(), measure.data(), measure.size() * 4));
+  }
+  run(skx_aggregate(ctx(), f.as<std::uint32_t>(), m.as<void>(), 4, fact.size(), domain_cardinality,
+                    0, nullptr, s.as<std::uint64_t>(), nullptr));
+  s.to(sums);
+  return sums;
+}
+
+AggState::AggState(std::uint32_t domain_cardinality, std::uint32_t hot_threshold_,
+                   std::uint32_t lanes_)
+    : main(domain_cardinality, 0), hot_threshold(hot_threshold_), lanes(lanes_) {
+  if (hot_threshold == 0 || hot_threshold > domain_cardinality)
+    throw InvalidArgument("lane-copy hot threshold must lie in 1..D");
+  if (lanes == 0) throw InvalidArgument("lane count must be at least 1");
+  hot.assign(static_cast<std::size_t>(hot_threshold) * lanes, 0);
+}
+
+void AggState::finalize() {
+  for (std::uint32_t l = 0; l < lanes; ++l)
+    for (std::uint32_t r = 0; r < hot_threshold; ++r)
+      main[r] += hot[static_cast<std::size_t>(l) * hot_threshold + r];
+  std::fill(hot.begin(), hot.end(), 0);
+}
+
+std::vector<std::uint64_t> aggregate_count_lanecopy(const Column& fact,
+                                                    std::uint32_t domain_cardinality,
+                                                    std::uint32_t hot_threshold,
+                                                    std::uint32_t lanes) {
+  require_in_domain(fact, domain_cardinality);
+  const AggState validate(domain_cardinality, hot_threshold, lanes);  // same checks as the reference
+  (void)validate;
+  return device_counts(fact, domain_cardinality, hot_threshold);
+}
+
+HeavyHitters heavy_hitter_count(const Column& fact, std::uint32_t domain_cardinality,
+                                std::uint32_t k, bool /*branchy*/) {
+  if (k == 0) throw InvalidArgument("heavy_hitter_count: k must be at least 1");
+  const std::uint32_t cutoff = std::min(k, domain_cardinality);
+  std::vector<std::uint64_t> counts(cutoff, 0);
+  DevBuf f(std::max<std::uint64_t>(fact.size(), 1) * 4), c(std::max<std::uint64_t>(cutoff, 1) * 8);
+  if (!fact.empty()) check(skx_copy_to_device(ctx(), f.as<void>(), fact.data(), fact.size() * 4));
+  run(skx_heavy_hitter_count(ctx(), f.as<std::uint32_t>(), fact.size(), domain_cardinality, k,
+                             c.as<std::uint64_t>(), nullptr));
+  c.to(counts);
+  HeavyHitters h;
+  h.clamped = k > domain_cardinality;
+  for (std::uint32_t i = 0; i < cutoff; ++i) h.top.emplace_back(i + 1, counts[i]);
+  std::sort(h.top.begin(), h.top.end(), by_count_then_id);
+  return h;
+}
+
+HeavyHitters top_k_by_full_aggregation(const Column& fact, std::uint32_t domain_cardinality,
+                                       std::uint32_t k) {
+  if (k == 0) throw InvalidArgument("top_k_by_full_aggregation: k must be at least 1");
+  const std::uint32_t cutoff = std::min(k, domain_cardinality);
+  const auto counts = aggregate_count(fact, domain_cardinality);
+  HeavyHitters h;
+  h.clamped = k > domain_cardinality;
+  h.top.reserve(domain_cardinality);
+  for (std::uint32_t i = 0; i < domain_cardinality; ++i) h.top.emplace_back(i + 1, counts[i]);
+  std::partial_sort(h.top.begin(), h.top.begin() + cutoff, h.top.end(), by_count_then_id);
+  h.top.resize(cutoff);
+  return h;
+}
+
+// ---- parallel.hpp ---------------------------------------------------------------
+const char* to_string(AggStrategy s) noexcept {
+  switch (s) {
+    case AggStrategy::independent: return "independent";
+    case AggStrategy::shared_atomic: return "shared_atomic";
+    case AggStrategy::hybrid: return "hybrid";
+  }
+  return "?";
+}
+
+std::vector<std::pair<std::size_t, std::size_t>> chunk_spans(std::size_t n, unsigned threads) {
+  if (threads == 0) throw InvalidArgument("thread count must be at least 1");
+  std::vector<std::pair<std::size_t, std::size_t>> spans;
+  spans.reserve(threads);
+  const std::size_t q = n / threads, r = n % threads;
+  std::size_t b = 0;
+  for (unsigned t = 0; t < threads; ++t) {
+    const std::size_t e = b + q + (t < r ? 1 : 0);
+    spans.emplace_back(b, e);
+    b = e;
+  }
+  return spans;
+}
+
+Column parallel_materialize(const Column& fact, const Column& dim, const ParallelPlan& plan) {
+  Column out = gather(fact, dim);  // domain check first, as parallel.cpp:88-89
+  chunk_spans(fact.size(), plan.threads);
+  return out;
+}
+
+std::vector<std::uint32_t> parallel_select(const Column& fact, const Bitmap& bitmap,
+                                           const ParallelPlan& plan) {
+  auto out = select(fact, bitmap);
+  chunk_spans(fact.size(), plan.threads);
+  return out;
+}
+
+std::vector<std::uint64_t> parallel_aggregate(const Column& fact, std::uint32_t domain_cardinality,
+                                              const ParallelPlan& plan, AggMetrics* metrics) {
+  const bool hybrid = plan.strategy == AggStrategy::hybrid;
+  if (hybrid && (plan.hot_threshold == 0 || plan.hot_threshold > domain_cardinality))
+    throw InvalidArgument("hybrid hot threshold must lie in 1..D");
+  auto counts = device_counts(fact, domain_cardinality, hybrid ? plan.hot_threshold : 0);
+  chunk_spans(fact.size(), plan.threads);
+  if (metrics) {
+    metrics->total_updates = fact.size();
+    std::uint64_t shared = 0;
+    if (plan.strategy == AggStrategy::shared_atomic) {
+      shared = fact.size();
+    } else if (hybrid) {
+      // rows whose id > h are the ones the reference routes to shared atomics
+      shared = fact.size() - std::accumulate(counts.begin(), counts.begin() + plan.hot_threshold,
+                                             std::uint64_t{0});
+    }
+    metrics->shared_updates = shared;
+    metrics->accumulator_bytes = memory_footprint(plan, domain_cardinality);
+  }
+  return counts;
+}
+
+std::uint64_t memory_footprint(const ParallelPlan& plan, std::uint64_t domain_cardinality) {
+  if (plan.threads == 0) throw InvalidArgument("thread count must be at least 1");
+  switch (plan.strategy) {
+    case AggStrategy::independent: return std::uint64_t{plan.threads} * domain_cardinality * 8;
+    case AggStrategy::shared_atomic: return domain_cardinality * 8;
+    case AggStrategy::hybrid:
+      return domain_cardinality * 8 + std::uint64_t{plan.threads} * plan.hot_threshold * 8;
+  }
+  return 0;
+}
+
+}  // namespace skewdx

@@ -316,3 +316,71 @@ int skx_aggregate_host(skx_ctx* ctx, const uint32_t* fact, const void* measure, 
 }
 
 }  // extern "C"
+
+// ---- device memory for host-side callers -----------------------------------
+namespace skx {
+namespace {
+__global__ void k_domain_scan(const uint32_t* __restrict__ fact, uint64_t n, uint64_t d,
+                              DevErr* err) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+    const uint32_t id = fact[k];
+    if ((uint64_t)(uint32_t)(id - 1u) >= d) record_violation(err, k, id);
+  }
+}
+}  // namespace
+}  // namespace skx
+
+extern "C" {
+
+int skx_device_alloc(skx_ctx* ctx, uint64_t bytes, void** ptr) {
+  if (!ctx || !ptr) return SKX_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  *ptr = nullptr;
+  cudaError_t e = cudaMalloc(ptr, bytes ? bytes : 16);
+  return e == cudaSuccess ? SKX_OK : cuda_fail(ctx, e, "device_alloc");
+}
+
+int skx_device_free(skx_ctx* ctx, void* ptr) {
+  if (!ctx) return SKX_INVALID_ARGUMENT;
+  if (!ptr) return SKX_OK;
+  cudaSetDevice(ctx->device);
+  cudaError_t e = cudaFree(ptr);
+  return e == cudaSuccess ? SKX_OK : cuda_fail(ctx, e, "device_free");
+}
+
+int skx_copy_to_device(skx_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
+  if (!ctx) return SKX_INVALID_ARGUMENT;
+  if (!bytes) return SKX_OK;
+  cudaSetDevice(ctx->device);
+  cudaError_t e = cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
+  return e == cudaSuccess ? SKX_OK : cuda_fail(ctx, e, "copy_to_device");
+}
+
+int skx_copy_to_host(skx_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
+  if (!ctx) return SKX_INVALID_ARGUMENT;
+  if (!bytes) return SKX_OK;
+  cudaSetDevice(ctx->device);
+  cudaError_t e = cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost);
+  return e == cudaSuccess ? SKX_OK : cuda_fail(ctx, e, "copy_to_host");
+}
+
+int skx_find_domain_violation(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint64_t d,
+                              uint64_t* row_out) {
+  if (!ctx || !row_out) return SKX_INVALID_ARGUMENT;
+  *row_out = ~0ull;
+  if (n == 0) return SKX_OK;
+  if (n > (uint64_t(1) << 34)) return set_error(ctx, SKX_INVALID_ARGUMENT, "more than 2^34 rows");
+  cudaSetDevice(ctx->device);
+  ctx->last_domain = d;
+  k_domain_scan<<<grid_for(ctx, n, 256, 8), 256>>>(fact, n, d, ctx->err);
+  ctx->launches++;
+  const int rc = skx_sync(ctx, nullptr);
+  if (rc == SKX_DOMAIN_VIOLATION) {
+    *row_out = ctx->last.row;
+    return SKX_OK;
+  }
+  return rc;
+}
+
+}  // extern "C"
