@@ -45,7 +45,8 @@ def parse():
     p.add_argument("--no-extras", action="store_true", help="skip rand-layout / group-by lines")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--policy", type=int, default=1, help="gather L2 policy (0 default, 1 evict_last)")
+    p.add_argument("--policy", type=int, default=129,
+                   help="skx_set_gather_policy bits (include/skx.h); 129 = library default")
     return p.parse_args()
 
 

@@ -220,7 +220,11 @@ int skx_aggregate_host(skx_ctx* ctx, const uint32_t* fact, const void* measure,
  *  16 = FK stream software-pipelined one iteration ahead;
  *  32 = tiered: the reordered id selects the cache class of each dimension
  *       load -- ids below t1 allocate in L1, ids below t2 are L2 evict_last,
- *       colder ids are L2 evict_first and skip L1 (skx_set_gather_tiers). */
+ *       colder ids are L2 evict_first and skip L1 (skx_set_gather_tiers);
+ *  64 = diagnostic: loads only, output stores dropped (NOT a valid gather);
+ * 128 = FK stream / output use the .cs (streaming) cache operator;
+ * 256, 512 = int64 dimension loads via the coherent / .cg (L2-only) path.
+ * Default 129 (= 1 | 128); measurements in profiles/r1_experiments.md. */
 int skx_set_gather_policy(skx_ctx* ctx, int policy);
 /* cudaLimitMaxL2FetchGranularity (32, 64 or 128 bytes): device-wide. */
 int skx_set_l2_fetch_granularity(skx_ctx* ctx, int bytes);

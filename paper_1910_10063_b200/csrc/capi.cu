@@ -128,7 +128,7 @@ int skx_ctx_destroy(skx_ctx* ctx) {
 uint64_t skx_launch_count(const skx_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
 
 int skx_set_gather_policy(skx_ctx* ctx, int policy) {
-  if (!ctx || policy < 0 || policy > 127) return SKX_INVALID_ARGUMENT;
+  if (!ctx || policy < 0 || policy > 1023) return SKX_INVALID_ARGUMENT;
   cudaSetDevice(ctx->device);
   const bool want = (policy & 4) != 0 && ctx->persist_max > 0;
   if (want != ctx->setaside_on) {

@@ -176,7 +176,10 @@ __global__ void __launch_bounds__((F & kPolHot) ? kThreadsHot : kThreads, (F & k
       // PREF: next iteration's FK vectors are in flight while this one's
       // dimension loads resolve.
       const uint64_t vi = PREF ? base + stride + (uint64_t)u * NT : base + (uint64_t)u * NT;
-      fn[u] = vi < nvec ? ld_stream_v4(fv + vi, pol_s) : make_uint4(1, 1, 1, 1);
+      if (F & 128)
+        fn[u] = vi < nvec ? __ldcs(fv + vi) : make_uint4(1, 1, 1, 1);
+      else
+        fn[u] = vi < nvec ? ld_stream_v4(fv + vi, pol_s) : make_uint4(1, 1, 1, 1);
     }
     if (!PREF) {
 #pragma unroll
@@ -200,7 +203,15 @@ __global__ void __launch_bounds__((F & kPolHot) ? kThreadsHot : kThreads, (F & k
           } else if (NOL1) {
             v[u][j] = ld_dim_nol1<V>(dim + idx, pol_d);
           } else {
-            v[u][j] = ld_dim<V>(dim + idx, pol_d, HINTS);
+            if constexpr ((F & 512) != 0 && sizeof(V) == 8) {  // .cg: cache in L2 only
+              v[u][j] = (V)__ldcg(reinterpret_cast<const unsigned long long*>(dim + idx));
+            } else if constexpr ((F & 256) != 0 && sizeof(V) == 8) {  // coherent (non-.nc) load path
+              uint64_t r;
+              asm volatile("ld.global.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(dim + idx), "l"(pol_d));
+              v[u][j] = (V)r;
+            } else {
+              v[u][j] = ld_dim<V>(dim + idx, pol_d, HINTS);
+            }
           }
         } else {
           v[u][j] = 0;
@@ -216,7 +227,16 @@ __global__ void __launch_bounds__((F & kPolHot) ? kThreadsHot : kThreads, (F & k
         if (F & 64) {  // diagnostic: keep the loads, drop the output stream
           dbg ^= (uint64_t)v[u][0] ^ (uint64_t)v[u][1] ^ (uint64_t)v[u][2] ^ (uint64_t)v[u][3];
         } else if (OUT_VEC) {
-          Pack4<V>::store(o + vi * 4, v[u], pol_s);
+          if (F & 128) {  // .cs (streaming) cache operator instead of an L2 policy
+            if constexpr (sizeof(V) == 8) {
+              __stcs(reinterpret_cast<ulonglong2*>(o + vi * 4), make_ulonglong2(v[u][0], v[u][1]));
+              __stcs(reinterpret_cast<ulonglong2*>(o + vi * 4) + 1, make_ulonglong2(v[u][2], v[u][3]));
+            } else {
+              Pack4<V>::store(o + vi * 4, v[u], pol_s);
+            }
+          } else {
+            Pack4<V>::store(o + vi * 4, v[u], pol_s);
+          }
         } else {
 #pragma unroll
           for (int j = 0; j < 4; ++j) o[vi * 4 + j] = v[u][j];
@@ -298,7 +318,8 @@ cudaError_t dispatch_vec(skx_ctx* ctx, int F, const uint32_t* fact, uint64_t hea
                                                           out, t, s)                        \
                : launch_vec<V, OUT_VEC, (x)>(ctx, fact, head, nvec, dim, dim_len, out, t, s);
   SKX_F(0) SKX_F(1) SKX_F(3) SKX_F(9) SKX_F(17) SKX_F(19)
-  SKX_F(33) SKX_F(35) SKX_F(49) SKX_F(51) SKX_F(65) SKX_F(97) SKX_F(69)
+  SKX_F(33) SKX_F(35) SKX_F(49) SKX_F(51) SKX_F(65) SKX_F(97) SKX_F(69) SKX_F(129) SKX_F(128)
+  SKX_F(131) SKX_F(385) SKX_F(641)
 #undef SKX_F
   return cudaErrorInvalidValue;
 }
