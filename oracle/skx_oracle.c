@@ -23,6 +23,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <immintrin.h>
 
 #define ORC_OK 0
 #define ORC_INVALID 1
@@ -382,8 +383,31 @@ typedef struct {
   uint64_t b, e;
 } gather_job;
 
+/* AVX2 inner loop in the shape of the reference's gather_u32_avx2
+ * (proj/src/kernels/avx2.cpp:43-57), widened to int64 values: 4 ids per
+ * _mm256_i32gather_epi64 (dimension length < 2^31, as kernels_for requires,
+ * operators.cpp:51-56). */
+__attribute__((target("avx2"))) static void gather_u64_avx2(const uint32_t* fact, uint64_t b,
+                                                             uint64_t e, const uint64_t* dim,
+                                                             uint64_t* out) {
+  const __m128i one = _mm_set1_epi32(1);
+  uint64_t k = b;
+  for (; k + 4 <= e; k += 4) {
+    const __m128i ids = _mm_loadu_si128((const __m128i*)(fact + k));
+    const __m256i v = _mm256_i32gather_epi64((const long long*)dim, _mm_sub_epi32(ids, one), 8);
+    _mm256_storeu_si256((__m256i*)(out + k), v);
+  }
+  for (; k < e; ++k) out[k] = dim[fact[k] - 1];
+}
+
+static int g_dim_small = 0; /* dimension fits signed 32-bit gather indices */
+
 static void* gather_u64_worker(void* p) {
   gather_job* j = (gather_job*)p;
+  if (g_dim_small && __builtin_cpu_supports("avx2")) {
+    gather_u64_avx2(j->fact, j->b, j->e, j->dim, j->out);
+    return NULL;
+  }
   for (uint64_t k = j->b; k < j->e; ++k) j->out[k] = j->dim[j->fact[k] - 1];
   return NULL;
 }
@@ -398,6 +422,7 @@ int orc_parallel_gather_u64(const uint32_t* fact, uint64_t n, const uint64_t* di
   gather_job* jobs = (gather_job*)malloc(sizeof(gather_job) * threads);
   pthread_t* tids = (pthread_t*)malloc(sizeof(pthread_t) * threads);
   orc_chunk_spans(n, threads, bs, es);
+  g_dim_small = dim_len <= 0x7FFFFFFFull;
   for (uint32_t t = 0; t < threads; ++t) {
     jobs[t] = (gather_job){fact, dim, out, bs[t], es[t]};
     if (t + 1 < threads) pthread_create(&tids[t], NULL, gather_u64_worker, &jobs[t]);
