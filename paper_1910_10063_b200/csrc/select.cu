@@ -7,15 +7,18 @@
 // (parallel.cpp:102-129: per-thread results concatenated in chunk order),
 // permute_bitmap (operators.cpp:21-30), build_bitmap (operators.hpp:38-45).
 //
-// B200 design: single pass over the FK column
-// with decoupled look-back.  A persistent grid takes 4096-row tiles from an
-// atomic ticket (so every predecessor tile is already running), computes the
-// tile's selected count with warp ballots, publishes its aggregate, looks
-// back over predecessors' published prefixes (acquire/release at gpu scope)
-// and writes the selected rows' offsets (and, fused, their gathered
-// category/price/supplier/flag) at prefix + local rank -- ascending row
-// order, exactly the reference's concatenation order.  Per-category sums
-// live in shared memory (fp64) for the CTA's lifetime and are flushed once.
+// B200 design: two streaming passes over the
+// FK column with a device scan between them -- pass 1 counts each 4096-row
+// tile's selected rows (ballots), the scan turns the counts into tile
+// offsets, pass 2 re-probes and writes each selected row at
+// tile offset + rank in tile: ascending row order, exactly the reference's
+// chunk-ordered concatenation.  (A single-pass decoupled look-back version
+// was measured 8-10x slower on B200: CTAs stall on the look-back chain,
+// profiles/r1_experiments.md.)  Pass 2 of the C5 variant gathers category /
+// price / supplier / flag for the selected rows and sums price per category
+// in warp-private fp64 shared bins: lanes of one category are pre-summed
+// with __match_any_sync + shuffles, because shared fp64 atomics compile to
+// CAS spin loops on sm_100a.  Bins are flushed once per CTA.
 #include "scan.cuh"
 
 namespace skx {
@@ -25,18 +28,7 @@ constexpr int kThreads = 256;
 constexpr int kItems = 16;
 constexpr int kTile = kThreads * kItems;  // 4096 rows
 constexpr int kWarps = kThreads / 32;
-constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62;
-constexpr unsigned long long kValMask = (1ull << 62) - 1;
-constexpr uint32_t kSmemCategories = 8192;
-
-__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
+constexpr uint32_t kSmemCategories = 2048;  // per-warp fp64 bins: 8 x 2048 x 8 B = 128 KB
 
 struct Cols {
   const int32_t* cat;
@@ -51,108 +43,161 @@ struct Cols {
   uint32_t n_categories;
 };
 
+// Probe one warp-striped item: row = tile*4096 + w*512 + i*32 + lane.  The
+// first `sw` bitmap words live in shared memory: on a skew-reordered column
+// the hot ids -- most probes -- fall in that prefix.
+__device__ __forceinline__ bool probe(const uint32_t* __restrict__ fact, uint64_t k, uint64_t n,
+                                      const unsigned long long* __restrict__ words, uint64_t bits,
+                                      const unsigned long long* s_words, uint32_t sw, uint64_t pol,
+                                      bool check, DevErr* err, uint32_t& idx) {
+  idx = 0;
+  if (k >= n) return false;
+  const uint32_t id = ld_stream_u32(fact + k, pol);
+  idx = id - 1u;
+  if (idx < bits) {
+    const uint32_t wi = idx >> 6;
+    const unsigned long long wv = wi < sw ? s_words[wi] : __ldg(words + wi);
+    return (wv >> (idx & 63)) & 1ull;
+  }
+  if (check) record_violation(err, k, id);
+  return false;
+}
+
+// Pass 1: probe every row once, store the selection as one 32-bit mask word
+// per warp-item (1 bit per row, coalesced), count selected rows per tile
+// (grid-stride over tiles) and check the domain.
+__global__ void __launch_bounds__(kThreads)
+    k_select_count(const uint32_t* __restrict__ fact, uint64_t n,
+                   const unsigned long long* __restrict__ words, uint64_t bits,
+                   uint32_t* __restrict__ mask, uint32_t* __restrict__ tile_counts, uint32_t sw,
+                   DevErr* err) {
+  extern __shared__ __align__(16) unsigned long long s_words[];  // bitmap prefix [sw]
+  __shared__ uint32_t s_w[kWarps];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  const uint64_t pol = policy_evict_first();
+  for (uint32_t i = threadIdx.x; i < sw; i += kThreads) s_words[i] = __ldg(words + i);
+  __syncthreads();
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint64_t row0 = tile * kTile + (uint64_t)w * (kItems * 32);
+    uint32_t c = 0, mine = 0;
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      uint32_t idx;
+      const uint32_t b = __ballot_sync(
+          0xffffffffu,
+          probe(fact, row0 + i * 32 + lane, n, words, bits, s_words, sw, pol, true, err, idx));
+      c += __popc(b);
+      if (lane == i) mine = b;
+    }
+    if (lane < kItems) mask[(row0 >> 5) + lane] = mine;  // 16 consecutive words per warp
+    if (lane == 0) s_w[w] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+      for (int i = 0; i < kWarps; ++i) t += s_w[i];
+      tile_counts[tile] = t;
+    }
+    __syncthreads();
+  }
+}
+
+// Pass 2, per tile: (A) read the mask words, load the FK of selected rows
+// and compact (dimension index, row in tile) into shared memory in row order;
+// (B) process the compacted rows densely -- consecutive threads take
+// consecutive selected rows, so the gathers are independent and the output
+// stores coalesce.  FUSED adds the 4-column gather and per-category sums.
 template <bool FUSED>
 __global__ void __launch_bounds__(kThreads)
-    k_select(const uint32_t* __restrict__ fact, uint64_t n, const unsigned long long* __restrict__ words,
-             uint64_t bits, uint32_t base_off, uint32_t* __restrict__ out_off, Cols cols,
-             unsigned long long* __restrict__ status, unsigned int* __restrict__ ticket,
-             unsigned long long* __restrict__ count_dev, DevErr* err) {
-  extern __shared__ double s_sums[];  // [n_categories] when FUSED and small
-  __shared__ uint32_t s_tile;
-  __shared__ uint32_t s_wtot[kWarps];
-  __shared__ unsigned long long s_excl;
+    k_select_write(const uint32_t* __restrict__ fact, uint64_t n, const uint32_t* __restrict__ mask,
+                   uint32_t base_off, const uint32_t* __restrict__ tile_off,
+                   const uint32_t* __restrict__ total, uint32_t* __restrict__ out_off, Cols cols,
+                   unsigned long long* __restrict__ count_dev) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* s_idx = reinterpret_cast<uint32_t*>(smem_raw);             // [kTile]
+  uint16_t* s_row = reinterpret_cast<uint16_t*>(s_idx + kTile);        // [kTile]
+  double* s_sums = reinterpret_cast<double*>(s_row + kTile);           // [kWarps][ncat] (FUSED)
+  __shared__ uint32_t s_w[kWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const bool smem_sums = FUSED && cols.n_categories <= kSmemCategories;
-  if (smem_sums) {
-    for (uint32_t i = threadIdx.x; i < cols.n_categories; i += kThreads) s_sums[i] = 0.0;
-  }
+  if (smem_sums)
+    for (uint32_t i = threadIdx.x; i < kWarps * cols.n_categories; i += kThreads) s_sums[i] = 0.0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *count_dev = *total;
   const uint64_t ntiles = (n + kTile - 1) / kTile;
   const uint64_t pol = policy_evict_first();
   const uint32_t lt = lanemask_lt();
-  for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
-    __syncthreads();
-    const uint64_t tile = s_tile;
-    if (tile >= ntiles) break;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint64_t row0 = tile * kTile + (uint64_t)w * (kItems * 32);
-    uint32_t sel[kItems];
-    uint32_t idxs[kItems];
-    uint32_t wcount = 0;
+    // (A) this warp's 16 mask words: lane i holds word i
+    const uint32_t mw = lane < kItems ? __ldg(mask + (row0 >> 5) + lane) : 0u;
+    uint32_t c = 0;
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) c += __popc(__shfl_sync(0xffffffffu, mw, i));
+    if (lane == 0) s_w[w] = c;
+    __syncthreads();
+    uint32_t lpos = 0;
+    for (int i = 0; i < w; ++i) lpos += s_w[i];
+    uint32_t cnt_tile = 0;
+    for (int i = 0; i < kWarps; ++i) cnt_tile += s_w[i];
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
-      const uint64_t k = row0 + i * 32 + lane;
-      bool s = false;
-      uint32_t idx = 0;
-      if (k < n) {
-        const uint32_t id = ld_stream_u32(fact + k, pol);
-        idx = id - 1u;
-        if (idx < bits) {
-          s = (__ldg(words + (idx >> 6)) >> (idx & 63)) & 1ull;
-        } else {
-          record_violation(err, k, id);
-        }
+      const uint32_t m = __shfl_sync(0xffffffffu, mw, i);
+      if ((m >> lane) & 1u) {
+        const uint32_t r = (uint32_t)(w * (kItems * 32) + i * 32 + lane);
+        const uint32_t j = lpos + __popc(m & lt);
+        s_idx[j] = ld_stream_u32(fact + tile * kTile + r, pol) - 1u;
+        s_row[j] = (uint16_t)r;
       }
-      idxs[i] = idx;
-      sel[i] = __ballot_sync(0xffffffffu, s);
-      wcount += __popc(sel[i]);
-    }
-    if (lane == 0) s_wtot[w] = wcount;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long agg = 0;
-      for (int i = 0; i < kWarps; ++i) agg += s_wtot[i];
-      unsigned long long excl = 0;
-      if (tile == 0) {
-        st_release(&status[0], kFlagInc | agg);
-      } else {
-        st_release(&status[tile], kFlagAgg | agg);
-        int64_t j = (int64_t)tile - 1;
-        for (;;) {
-          const unsigned long long st = ld_acquire(&status[j]);
-          const unsigned long long flag = st & ~kValMask;
-          if (flag == 0) continue;  // predecessor still counting
-          excl += st & kValMask;
-          if (flag == kFlagInc) break;
-          --j;
-        }
-        st_release(&status[tile], kFlagInc | (excl + agg));
-      }
-      if (tile == ntiles - 1) *count_dev = excl + agg;
-      s_excl = excl;
+      lpos += __popc(m);
     }
     __syncthreads();
-    uint64_t pos = s_excl;
-    for (int i = 0; i < w; ++i) pos += s_wtot[i];
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-      if ((sel[i] >> lane) & 1u) {
-        const uint64_t p = pos + __popc(sel[i] & lt);
-        const uint64_t k = row0 + i * 32 + lane;
-        out_off[p] = base_off + (uint32_t)k;
+    // (B) dense pass over the tile's selected rows
+    const uint64_t obase = tile_off[tile];
+    for (uint32_t j0 = 0; j0 < cnt_tile; j0 += kThreads) {
+      const uint32_t j = j0 + threadIdx.x;
+      const bool live = j < cnt_tile;
+      int32_t ct = -1;
+      float pr = 0.f;
+      if (live) {
+        const uint64_t p = obase + j;
+        out_off[p] = base_off + (uint32_t)(tile * kTile + s_row[j]);
         if (FUSED) {
-          const uint32_t idx = idxs[i];
-          const int32_t c = __ldg(cols.cat + idx);
-          const float pr = __ldg(cols.price + idx);
-          cols.out_cat[p] = c;
+          const uint32_t idx = s_idx[j];
+          ct = __ldg(cols.cat + idx);
+          pr = __ldg(cols.price + idx);
+          const unsigned long long sp = __ldg(cols.supp + idx);
+          const unsigned short fl = __ldg(reinterpret_cast<const unsigned short*>(cols.flag) + idx);
+          cols.out_cat[p] = ct;
           cols.out_price[p] = pr;
-          cols.out_supp[p] = __ldg(cols.supp + idx);
-          cols.out_flag[p] = __ldg(reinterpret_cast<const unsigned short*>(cols.flag) + idx);
-          if ((uint32_t)c < cols.n_categories) {
+          cols.out_supp[p] = sp;
+          cols.out_flag[p] = fl;
+        }
+      }
+      if (FUSED) {
+        // SUM(price) per category: lanes of one category elect a leader that
+        // adds the group's fp64 sum to its warp-private bin (no fp64 atomics).
+        const bool ok = live && (uint32_t)ct < cols.n_categories;
+        const uint32_t key = ok ? (uint32_t)ct : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, key);
+        if (ok) {
+          double grp = 0.0;
+          for (uint32_t m = peers; m; m &= m - 1)
+            grp += __shfl_sync(peers, (double)pr, __ffs(m) - 1);
+          if (lane == __ffs(peers) - 1) {
             if (smem_sums)
-              atomicAdd(&s_sums[c], (double)pr);
+              s_sums[(size_t)w * cols.n_categories + ct] += grp;
             else
-              atomicAdd(&cols.sums[c], (double)pr);
+              atomicAdd(&cols.sums[ct], grp);
           }
         }
       }
-      pos += __popc(sel[i]);
     }
+    __syncthreads();  // s_idx / s_row / s_w reused by the next tile
   }
   if (smem_sums) {
-    __syncthreads();
     for (uint32_t i = threadIdx.x; i < cols.n_categories; i += kThreads) {
-      const double v = s_sums[i];
+      double v = 0.0;
+      for (int ww = 0; ww < kWarps; ++ww) v += s_sums[(size_t)ww * cols.n_categories + i];
       if (v != 0.0) atomicAdd(&cols.sums[i], v);
     }
   }
@@ -205,33 +250,45 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
     return e == cudaSuccess ? SKX_OK : cuda_fail(ctx, e, "select memset");
   }
   const uint64_t ntiles = (n + kTile - 1) / kTile;
-  char* sp = static_cast<char*>(scratch(ctx, 2, ntiles * 8 + 256));
+  // scratch: mask words [ntiles * 128] | tile counts | tile offsets | total
+  uint32_t* sp = static_cast<uint32_t*>(scratch(ctx, 2, ntiles * (kTile / 32 + 2) * 4 + 256));
   if (!sp) return set_error(ctx, SKX_CUDA_ERROR, "select: out of device memory");
-  unsigned int* ticket = reinterpret_cast<unsigned int*>(sp);
-  unsigned long long* status = reinterpret_cast<unsigned long long*>(sp + 256);
-  e = cudaMemsetAsync(sp, 0, ntiles * 8 + 256, s);
-  if (e != cudaSuccess) return cuda_fail(ctx, e, "select memset");
-  const size_t smem =
-      (fused && cols.n_categories <= kSmemCategories) ? (size_t)cols.n_categories * 8 : 0;
-  // Persistent grid: all CTAs resident, so look-back always makes progress.
+  uint32_t* mask = sp;
+  uint32_t* counts = sp + ntiles * (kTile / 32);
+  uint32_t* offs = counts + ntiles;
+  uint32_t* total = offs + ntiles;
+  const auto* wd = reinterpret_cast<const unsigned long long*>(words);
+  // Optional bitmap prefix staged per CTA in shared memory.  Off: measured on
+  // B200 at C5 (96 KB prefix, 2 CTAs/SM) 20.5 -> 38.2 ms -- the lost
+  // occupancy and L1 capacity cost more than the on-chip probes save.
+  const uint32_t sw = 0;
+  const size_t smem1 = (size_t)sw * 8;
+  cudaFuncSetAttribute(k_select_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+  int per_sm1 = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm1, k_select_count, kThreads, smem1);
+  const unsigned grid1 = grid_for(ctx, ntiles, 1, per_sm1 < 1 ? 1 : per_sm1);
+  k_select_count<<<grid1, kThreads, smem1, s>>>(fact, n, wd, bits, mask, counts, sw, ctx->err);
+  ctx->launches++;
+  int rc = launch_exclusive_scan_u32(ctx, counts, offs, ntiles, total, 3, s);
+  if (rc) return rc;
+  const size_t tile_smem = (size_t)kTile * (4 + 2);
+  const size_t smem = tile_smem + ((fused && cols.n_categories <= kSmemCategories)
+                                       ? (size_t)kWarps * cols.n_categories * 8
+                                       : 0);
   int per_sm = 0;
   if (fused) {
-    cudaFuncSetAttribute(k_select<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select<true>, kThreads, smem);
+    cudaFuncSetAttribute(k_select_write<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_write<true>, kThreads, smem);
+    const unsigned grid2 = grid_for(ctx, ntiles, 1, per_sm < 1 ? 1 : per_sm);
+    k_select_write<true><<<grid2, kThreads, smem, s>>>(fact, n, mask, base, offs, total, out, cols,
+                                                      reinterpret_cast<unsigned long long*>(count_dev));
   } else {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select<false>, kThreads, 0);
+    cudaFuncSetAttribute(k_select_write<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_write<false>, kThreads, smem);
+    const unsigned grid2 = grid_for(ctx, ntiles, 1, per_sm < 1 ? 1 : per_sm);
+    k_select_write<false><<<grid2, kThreads, smem, s>>>(fact, n, mask, base, offs, total, out, cols,
+                                                       reinterpret_cast<unsigned long long*>(count_dev));
   }
-  if (per_sm < 1) per_sm = 1;
-  uint64_t grid = (uint64_t)ctx->num_sms * per_sm;
-  if (grid > ntiles) grid = ntiles;
-  if (fused)
-    k_select<true><<<(unsigned)grid, kThreads, smem, s>>>(
-        fact, n, reinterpret_cast<const unsigned long long*>(words), bits, base, out, cols, status,
-        ticket, reinterpret_cast<unsigned long long*>(count_dev), ctx->err);
-  else
-    k_select<false><<<(unsigned)grid, kThreads, 0, s>>>(
-        fact, n, reinterpret_cast<const unsigned long long*>(words), bits, base, out, cols, status,
-        ticket, reinterpret_cast<unsigned long long*>(count_dev), ctx->err);
   ctx->launches++;
   SKX_CHECK_LAUNCH(ctx, "select");
   return SKX_OK;
