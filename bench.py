@@ -407,7 +407,9 @@ def run_ours(args):
                                 "peak": peak, "unit": "GB/s",
                                 "frac": gb_bytes / (statistics.mean(per_g) * 1e-3) / 1e9 / peak,
                                 "alg_bytes_per_step": gb_bytes}}
-        del gdat
+        del gdat, counts, sums
+        torch.cuda.empty_cache()
+        extras.update(other_configs(args, ctx, stream, dist_on, rank, world, peak))
 
     if rank == 0:
         line = {
@@ -439,6 +441,108 @@ def run_ours(args):
     if dist_on:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def other_configs(args, ctx, stream, dist_on, rank, world, peak):
+    """The remaining BASELINE configs, each timed like the headline (W
+    warm-ups, K launches between barriers, CUDA events, max over ranks):
+    C1 small gather (both layouts), C4 index build at scale, C5 select +
+    4-column gather + per-category fp64 SUM."""
+    import torch
+
+    from paper_1910_10063_b200 import dataset as ds_mod
+    from paper_1910_10063_b200 import skewdx as sx
+    out = {}
+    k = max(3, min(args.steps, 10))
+
+    # C1: D=2^22 int32 price (uniform 1..1e6), 2^24 int32 FKs per GPU, s=1.0.
+    d1, n1 = 1 << 22, 1 << 24
+    g = ds_mod.make_gather_dataset(d1, n1 * world, 1.0, SEED + 7, torch.int32,
+                                   ds_mod.Shard(rank, world, rank * n1, (rank + 1) * n1))
+    price = ds_mod.fill_column(ds_mod.KIND_UNIFORM, torch.int32, d1, SEED + 8, 1, 1000000)
+    price_f = sx.permute_dimension(price, g.index, sync=False)
+    o1 = torch.empty(n1, dtype=torch.int32, device="cuda")
+    c1 = {}
+    for layout, f, dm in (("freq", g.fact_freq, price_f), ("rand", g.fact_rand, price)):
+        t, per, _ = timed_launches(lambda f=f, dm=dm: sx.materialize(f, dm, out=o1, ctx=ctx, sync=False),
+                                   k * 10, args.warmup, stream, dist_on)
+        t = max_over_ranks(t, dist_on)
+        c1[layout] = {"value": n1 * world * k * 10 / (t * 1e-3), "unit": "rows/s",
+                      "us_per_launch": 1e3 * t / (k * 10),
+                      "roofline_frac": n1 * 8 / (statistics.mean(per) * 1e-3) / 1e9 / peak}
+    c1["note"] = ("L2-resident 16 MiB dimension; back-to-back launches (inputs 192 MiB > L2), "
+                  "per-launch time includes launch overhead")
+    out["gather_c1"] = c1
+    del g, price, price_f, o1
+
+    # C4: index build at scale, D=2^26, s=1.25, 2^30 rows per GPU.
+    d4, n4 = 1 << 26, 1 << 30
+    sh = ds_mod.Shard(rank, world, rank * n4, (rank + 1) * n4)
+    fact = ds_mod.make_rand_fact(d4, n4 * world, 1.25, SEED + 9, sh)
+    dim_i = ds_mod.fill_column(ds_mod.KIND_RAW, torch.int32, d4, SEED + 10)
+    dim_f = ds_mod.fill_column(ds_mod.KIND_RAW, torch.int32, d4, SEED + 11).view(torch.float32)
+    counts = torch.empty(d4, dtype=torch.uint32, device="cuda")
+    ff = torch.empty_like(fact)
+
+    def c4_step():
+        sx.histogram_u32(fact, d4, counts, ctx=ctx, sync=False)
+        ds_mod._allreduce_u32(counts)
+        idx = sx.build_index(sx.FrequencyProfile(counts, n4 * world), ctx=ctx, sync=False)
+        sx.recode_fact(fact, idx, out=ff, ctx=ctx, sync=False)
+        sx.permute_dimension(dim_i, idx, ctx=ctx, sync=False)
+        sx.permute_dimension(dim_f, idx, ctx=ctx, sync=False)
+    t4, _, _ = timed_launches(c4_step, 3, 1, stream, dist_on)
+    ctx.sync()
+    t4 = max_over_ranks(t4, dist_on) / 3
+    alg4 = n4 * 12 + d4 * 28
+    out["index_build_c4"] = {"ms_per_build": t4, "rows_per_s": n4 * world / (t4 * 1e-3),
+                             "roofline_frac": alg4 / (t4 * 1e-3) / 1e9 / peak,
+                             "alg_bytes": alg4,
+                             "note": "histogram + all-reduce + sort + recode + permute int32 and "
+                                     "float32 dims; warm"}
+    del fact, dim_i, dim_f, counts, ff
+    torch.cuda.empty_cache()
+
+    # C5: 2^31 rows (per GPU), D=2^25, category < 100, 4-column gather + fp64 SUM(price).
+    d5, n5 = 1 << 25, 1 << 31
+    sh = ds_mod.Shard(rank, world, rank * n5, (rank + 1) * n5)
+    fact = ds_mod.make_rand_fact(d5, n5 * world, 1.0, SEED + 12, sh)
+    counts = sx.histogram_u32(fact, d5, ctx=ctx, sync=False)
+    ds_mod._allreduce_u32(counts)
+    idx = sx.build_index(sx.FrequencyProfile(counts, n5 * world), ctx=ctx, sync=False)
+    fact_f = sx.recode_fact(fact, idx, ctx=ctx, sync=False)
+    del fact, counts
+    cat = sx.permute_dimension(ds_mod.fill_column(ds_mod.KIND_UNIFORM, torch.int32, d5, SEED + 13, 0, 1000), idx)
+    prc = sx.permute_dimension(ds_mod.fill_column(ds_mod.KIND_LOGNORMAL, torch.float32, d5, SEED + 14, 3.0, 1.0), idx)
+    sup = sx.permute_dimension(ds_mod.fill_column(ds_mod.KIND_RAW, torch.int64, d5, SEED + 15), idx)
+    flg = sx.permute_dimension(ds_mod.fill_column(ds_mod.KIND_RAW, torch.int16, d5, SEED + 16), idx)
+    bm = sx.build_bitmap_lt(cat, 100)  # category < 100, already in rank space
+    cap = n5 // 5
+    bufs = [torch.empty(cap, dtype=t, device="cuda")
+            for t in (torch.uint32, torch.int32, torch.float32, torch.int64, torch.int16)]
+    sums = torch.empty(1000, dtype=torch.float64, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.uint64, device="cuda")
+
+    def c5_step():
+        ctx.call("skx_select_gather_sum", C_ptr(fact_f), n5, C_ptr(bm.words), d5, C_ptr(cat),
+                 C_ptr(prc), C_ptr(sup), C_ptr(flg), sh.begin, 1000, *[C_ptr(b) for b in bufs],
+                 C_ptr(sums), C_ptr(cnt), ctx.stream(), sync=False)
+        if dist_on:  # per-category fp64 partials reduced to rank 0
+            torch.distributed.reduce(sums, dst=0)
+    t5, per5, _ = timed_launches(c5_step, k, args.warmup, stream, dist_on)
+    ctx.sync()
+    t5 = max_over_ranks(t5, dist_on)
+    sel = int(cnt.item())
+    if sel > cap:
+        raise SystemExit("C5 output capacity exceeded")
+    alg5 = n5 * 4 + sel * 22 + 1000 * 8
+    out["select_c5"] = {"value": n5 * world * k / (t5 * 1e-3), "unit": "rows/s",
+                        "ms_per_step": t5 / k, "selected": sel, "selectivity": sel / n5,
+                        "roofline_frac": alg5 / (statistics.mean(per5) * 1e-3) / 1e9 / peak,
+                        "alg_bytes_per_step": alg5}
+    del fact_f, cat, prc, sup, flg, bm, bufs, sums, cnt, idx
+    torch.cuda.empty_cache()
+    return out
 
 
 def C_ptr(t):
