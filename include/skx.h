@@ -233,6 +233,10 @@ int skx_set_l2_fetch_granularity(skx_ctx* ctx, int bytes);
  * t2 = l2_fraction * L2 size / width. */
 int skx_set_gather_tiers(skx_ctx* ctx, uint64_t smem_bytes, uint64_t l1_bytes,
                          double l2_fraction);
+/* Histogram cold-key handling for domains whose counters exceed half of L2:
+ * 0 = direct global reductions (default, faster as measured), 1 = key-range
+ * buckets folded in shared memory (csrc/bucket.cuh). */
+int skx_set_histogram_mode(skx_ctx* ctx, int bucketed);
 /* cudaCtxResetPersistingL2Cache: demote lines left persisting by windows. */
 int skx_reset_persisting_l2(skx_ctx* ctx);
 /* info[0..n): num_sms, smem_optin, l2_bytes, persisting-L2 max, access-policy

@@ -149,6 +149,12 @@ int skx_set_gather_tiers(skx_ctx* ctx, uint64_t smem_bytes, uint64_t l1_bytes, d
   return SKX_OK;
 }
 
+int skx_set_histogram_mode(skx_ctx* ctx, int bucketed) {
+  if (!ctx || bucketed < 0 || bucketed > 1) return SKX_INVALID_ARGUMENT;
+  ctx->hist_bucketed = bucketed != 0;
+  return SKX_OK;
+}
+
 int skx_reset_persisting_l2(skx_ctx* ctx) {
   if (!ctx) return SKX_INVALID_ARGUMENT;
   cudaSetDevice(ctx->device);

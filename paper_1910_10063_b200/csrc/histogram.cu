@@ -4,23 +4,21 @@
 // scattered increment that throws DomainViolation at the first bad row.
 //
 // B200 design.  Before the reorder the hot
-// keys are scattered ids, so the "ids <= h are hot" trick is unavailable and a
-// Zipf(1.25) key alone takes ~22% of all rows: plain global atomics would
-// serialise on a handful of L2 addresses.  Each CTA therefore keeps a
-// shared-memory open-addressing table (key -> count) that captures the keys
-// it sees first -- for skewed data these are the hot ones -- and:
-//   1. warp-aggregates equal keys with __match_any_sync (one update per
-//      distinct key per warp instruction),
-//   2. the leader lane adds the group size to its table slot with a shared
-//      atomic (claiming an empty slot with atomicCAS),
-//   3. keys that do not find a slot within kProbe probes go straight to a
-//      global red.add (cold tail, spread over many L2 lines),
-//   4. at exit the table is flushed with one global red.add per live slot.
+// keys are scattered ids (a Zipf(1.25) key alone is ~22% of all rows), so:
+//  1. lanes of a warp holding equal keys merge with __match_any_sync (one
+//     update per distinct key per warp instruction);
+//  2. the leader adds the group size to a per-CTA shared-memory
+//     open-addressing table (key -> count) that captures the keys the CTA
+//     sees first -- for skewed data the hot ones -- claiming slots with CAS;
+//  3. a key that finds no slot within kProbe probes is cold: for small
+//     domains (counters L2-resident) it is a global red.add; for large ones
+//     (counters >> L2) it is appended to the bucket of its key range
+//     (bucket.cuh) and folded in shared memory by a second kernel, so no
+//     cold update read-modify-writes an HBM line;
+//  4. each CTA flushes its table once.
 // The FK column is streamed once with 128-bit evict_first loads; the domain
 // check is fused (first bad row via atomicMin, reported at skx_sync).
-#include <cstdlib>
-
-#include "skx_internal.cuh"
+#include "bucket.cuh"
 
 namespace skx {
 namespace {
@@ -29,7 +27,10 @@ constexpr int kThreads = 512;
 constexpr int kTableBits = 13;  // 8192 slots x 8 B = 64 KB per CTA
 constexpr int kTable = 1 << kTableBits;
 constexpr int kProbe = 4;
-constexpr int kUnroll = 2;  // uint4 per thread per iteration
+constexpr int kUnroll = 2;        // uint4 per thread per iteration
+constexpr int kBucketShift = 15;  // 32768 keys per bucket: 128 KB of u32 fold counters
+constexpr uint32_t kBucketRange = 1u << kBucketShift;
+constexpr int kFoldThreads = 1024;
 
 __device__ __forceinline__ uint32_t slot_hash(uint32_t id) {
   return (id * 0x9E3779B1u) >> (32 - kTableBits);
@@ -47,37 +48,53 @@ __device__ __forceinline__ void global_add<unsigned long long>(unsigned long lon
   atomicAdd(counts + idx, (unsigned long long)c);
 }
 
-template <typename CT>
+struct Buckets {
+  unsigned int* cursors;  // [nb]
+  uint32_t* buf;          // [nb][cap]: (count << 16) | (id-1 within bucket)
+  uint64_t cap;
+};
+
+// Warp-collective: every lane calls it (invalid lanes with valid = false).
+template <typename CT, bool BK>
 __device__ __forceinline__ void count_one(uint32_t id, bool valid, uint32_t* keys, uint32_t* cnts,
-                                          CT* counts) {
-  // id is 1-based and in-domain when valid; invalid lanes carry id 0.
+                                          CT* counts, const Buckets& bk) {
   const uint32_t key = valid ? id : 0u;
   const uint32_t peers = __match_any_sync(0xffffffffu, key);
   const uint32_t lane = threadIdx.x & 31;
-  if (key == 0u || lane != (uint32_t)(__ffs(peers) - 1)) return;
+  const bool leader = key != 0u && lane == (uint32_t)(__ffs(peers) - 1);
   const uint32_t c = __popc(peers);
-  uint32_t h = slot_hash(key);
+  bool cold = false;
+  if (leader) {
+    uint32_t h = slot_hash(key);
+    cold = true;
 #pragma unroll
-  for (int p = 0; p < kProbe; ++p) {
-    uint32_t k = keys[h];
-    if (k == 0u) {
-      k = atomicCAS(&keys[h], 0u, key);
-      if (k == 0u) k = key;
+    for (int p = 0; p < kProbe; ++p) {
+      uint32_t k = keys[h];
+      if (k == 0u) {
+        k = atomicCAS(&keys[h], 0u, key);
+        if (k == 0u) k = key;
+      }
+      if (k == key) {
+        atomicAdd(&cnts[h], c);
+        cold = false;
+        break;
+      }
+      h = (h + 1) & (kTable - 1);
     }
-    if (k == key) {
-      atomicAdd(&cnts[h], c);
-      return;
-    }
-    h = (h + 1) & (kTable - 1);
+    if (cold && !BK) global_add<CT>(counts, key - 1, c);
   }
-  global_add<CT>(counts, key - 1, c);
+  if (BK && __any_sync(0xffffffffu, cold)) {
+    const uint32_t idx = key - 1u;
+    if (!bucket_append<uint32_t>(idx >> kBucketShift, cold, (c << 16) | (idx & (kBucketRange - 1)),
+                                 bk.cursors, bk.buf, bk.cap))
+      global_add<CT>(counts, idx, c);  // bucket full: fall back to a direct update
+  }
 }
 
-template <typename CT>
+template <typename CT, bool BK>
 __global__ void __launch_bounds__(kThreads)
     k_histogram(const uint32_t* __restrict__ fact, uint64_t head, uint64_t nvec, uint64_t n,
-                uint32_t d, uint32_t lo, uint32_t hi, bool check, CT* __restrict__ counts,
-                DevErr* err) {
+                uint32_t d, CT* __restrict__ counts, Buckets bk, DevErr* err) {
   extern __shared__ uint32_t smem_tab[];
   uint32_t* keys = smem_tab;
   uint32_t* cnts = smem_tab + kTable;
@@ -90,7 +107,7 @@ __global__ void __launch_bounds__(kThreads)
   const uint4* fv = reinterpret_cast<const uint4*>(fact + head);
   const uint64_t per_iter = (uint64_t)kThreads * kUnroll;
   const uint64_t stride = (uint64_t)gridDim.x * per_iter;
-  // Vector body; every lane of a warp runs the same trip count (match_any).
+  // Vector body; every lane of a warp runs the same trip count (warp collectives).
   const uint64_t nvec_round = (nvec + per_iter - 1) / per_iter * per_iter;
   for (uint64_t base = (uint64_t)blockIdx.x * per_iter + threadIdx.x; base < nvec_round;
        base += stride) {
@@ -107,9 +124,9 @@ __global__ void __launch_bounds__(kThreads)
       const uint32_t ids[4] = {f[u].x, f[u].y, f[u].z, f[u].w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const uint32_t idx = ids[j] - 1u;
-        if (check && live && idx >= d) record_violation(err, head + vi * 4 + j, ids[j]);
-        count_one<CT>(ids[j], live && idx >= lo && idx < hi, keys, cnts, counts);
+        const bool ok = (ids[j] - 1u) < d;
+        if (live && !ok) record_violation(err, head + vi * 4 + j, ids[j]);
+        count_one<CT, BK>(ids[j], live && ok, keys, cnts, counts, bk);
       }
     }
   }
@@ -120,12 +137,12 @@ __global__ void __launch_bounds__(kThreads)
     for (uint64_t t0 = 0; t0 < extra; t0 += kThreads) {
       const uint64_t t = t0 + threadIdx.x;
       uint64_t k = 0;
-      bool live = t < extra;
+      const bool live = t < extra;
       if (live) k = t < head ? t : tail_b + (t - head);
       const uint32_t id = live ? fact[k] : 0u;
-      const uint32_t idx = id - 1u;
-      if (check && live && idx >= d) record_violation(err, k, id);
-      count_one<CT>(id, live && idx >= lo && idx < hi, keys, cnts, counts);
+      const bool ok = (id - 1u) < d;
+      if (live && !ok) record_violation(err, k, id);
+      count_one<CT, BK>(id, live && ok, keys, cnts, counts, bk);
     }
   }
   __syncthreads();
@@ -133,6 +150,70 @@ __global__ void __launch_bounds__(kThreads)
     const uint32_t k = keys[i];
     if (k != 0u && cnts[i] != 0u) global_add<CT>(counts, k - 1, cnts[i]);
   }
+}
+
+// Second kernel: fold each key-range bucket in shared memory, then update its
+// (exclusively owned) counters with plain coalesced read-modify-writes.
+template <typename CT>
+__global__ void __launch_bounds__(kFoldThreads, 1)
+    k_hist_fold(Buckets bk, uint32_t nb, uint32_t d, CT* __restrict__ counts) {
+  extern __shared__ uint32_t sc[];  // [kBucketRange]
+  for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    for (uint32_t j = threadIdx.x; j < kBucketRange; j += kFoldThreads) sc[j] = 0u;
+    __syncthreads();
+    const uint64_t m = bk.cursors[b] < bk.cap ? bk.cursors[b] : bk.cap;
+    const uint32_t* src = bk.buf + (uint64_t)b * bk.cap;
+    for (uint64_t i = threadIdx.x; i < m; i += kFoldThreads) {
+      const uint32_t v = __ldcs(src + i);
+      atomicAdd(&sc[v & 0xFFFFu], v >> 16);
+    }
+    __syncthreads();
+    const uint64_t g0 = (uint64_t)b << kBucketShift;
+    for (uint32_t j = threadIdx.x; j < kBucketRange; j += kFoldThreads) {
+      const uint32_t c = sc[j];
+      if (c && g0 + j < d) counts[g0 + j] += (CT)c;
+    }
+    __syncthreads();
+  }
+}
+
+template <typename CT>
+int histogram_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64_t nvec, uint64_t n,
+                   uint32_t d, CT* counts, cudaStream_t s) {
+  const unsigned grid = grid_for(ctx, nvec ? nvec : 1, kThreads * kUnroll, 3);
+  const size_t smem = size_t(2) * kTable * sizeof(uint32_t);
+  // Bucket the cold updates only when the counters overflow half of L2 --
+  // and only when enabled: measured on B200 (profiles/r1_experiments.md) the
+  // per-element warp-aggregated bucket append is still slower than direct
+  // reductions (C4 histogram 6.96 -> 9.11 ms, C2 index 17.4 -> 25.5 ms)
+  // because the bucket cursors become the contended addresses.  Kept,
+  // parity-tested, for the CTA-staged variant planned next.
+  const bool bucketed = ctx->hist_bucketed && (uint64_t)d * sizeof(CT) > ctx->l2_bytes / 2 &&
+                        n >= (uint64_t(1) << 20);
+  Buckets bk{nullptr, nullptr, 0};
+  uint32_t nb = 0;
+  if (bucketed) {
+    nb = (uint32_t)(((uint64_t)d + kBucketRange - 1) >> kBucketShift);
+    bk.cap = n / nb + 4096;
+    char* sp = static_cast<char*>(scratch(ctx, 0, (uint64_t)nb * bk.cap * 4 + (uint64_t)nb * 4 + 256));
+    if (!sp) return set_error(ctx, SKX_CUDA_ERROR, "histogram: out of device memory for buckets");
+    bk.cursors = reinterpret_cast<unsigned int*>(sp);
+    bk.buf = reinterpret_cast<uint32_t*>(sp + (((uint64_t)nb * 4 + 255) & ~uint64_t(255)));
+    cudaError_t e = cudaMemsetAsync(bk.cursors, 0, (size_t)nb * 4, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "histogram memset");
+    cudaFuncSetAttribute(k_histogram<CT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_histogram<CT, true><<<grid, kThreads, smem, s>>>(fact, head, nvec, n, d, counts, bk, ctx->err);
+    const size_t fsmem = (size_t)kBucketRange * 4;
+    cudaFuncSetAttribute(k_hist_fold<CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
+    k_hist_fold<CT><<<grid_for(ctx, nb, 1, 1), kFoldThreads, fsmem, s>>>(bk, nb, d, counts);
+    ctx->launches += 2;
+  } else {
+    cudaFuncSetAttribute(k_histogram<CT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_histogram<CT, false><<<grid, kThreads, smem, s>>>(fact, head, nvec, n, d, counts, bk, ctx->err);
+    ctx->launches++;
+  }
+  SKX_CHECK_LAUNCH(ctx, "histogram");
+  return SKX_OK;
 }
 
 }  // namespace
@@ -150,35 +231,10 @@ int launch_histogram(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint32_t d,
   if (head > n) head = n;
   const uint64_t nvec = (n - head) / 4;
   ctx->last_domain = d;
-  const unsigned grid = grid_for(ctx, nvec ? nvec : 1, kThreads * kUnroll, 3);
-  const size_t smem = size_t(2) * kTable * sizeof(uint32_t);
   if (counter_bytes == 4)
-    cudaFuncSetAttribute(k_histogram<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  else
-    cudaFuncSetAttribute(k_histogram<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  // Optional key-range passes (SKX_HIST_RANGE ids per pass): each pass only
-  // updates counters of ids in [lo, hi) so cold-key atomics stay in L2, at
-  // the price of re-streaming the FK column per pass.  Measured on B200
-  // (profiles/): one pass wins at BASELINE sizes (D=2^26: 6.96 ms single vs
-  // 11.1 ms with 16M-key passes), so the default is a single pass.
-  uint64_t range = (uint64_t)d + 1;
-  if (const char* ev = getenv("SKX_HIST_RANGE")) range = strtoull(ev, nullptr, 10);
-  if (range < (1u << 20)) range = 1u << 20;
-  for (uint64_t lo = 0; lo < d || lo == 0; lo += range) {
-    const uint32_t hi = (uint32_t)((lo + range < d) ? lo + range : d);
-    const bool check = lo == 0;
-    if (counter_bytes == 4)
-      k_histogram<uint32_t><<<grid, kThreads, smem, s>>>(fact, head, nvec, n, d, (uint32_t)lo, hi,
-                                                         check, static_cast<uint32_t*>(counts), ctx->err);
-    else
-      k_histogram<unsigned long long><<<grid, kThreads, smem, s>>>(
-          fact, head, nvec, n, d, (uint32_t)lo, hi, check,
-          static_cast<unsigned long long*>(counts), ctx->err);
-    ctx->launches++;
-    if (hi >= d) break;
-  }
-  SKX_CHECK_LAUNCH(ctx, "histogram");
-  return SKX_OK;
+    return histogram_impl<uint32_t>(ctx, fact, head, nvec, n, d, static_cast<uint32_t*>(counts), s);
+  return histogram_impl<unsigned long long>(ctx, fact, head, nvec, n, d,
+                                            static_cast<unsigned long long*>(counts), s);
 }
 
 }  // namespace skx

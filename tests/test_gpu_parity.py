@@ -288,3 +288,28 @@ def test_aggregate_packed_tail_exactness(sx):
     se = np.zeros(49, np.uint64)
     np.add.at(se, f.astype(np.int64) - 1, m.view(np.uint64))
     assert np.array_equal(np_(c), ce) and np.array_equal(np_(s), se)
+
+
+@pytest.mark.parametrize("bucketed", [0, 1])
+@pytest.mark.parametrize("case", ["zipf", "uniform", "one_bucket"])
+def test_histogram_bucketed_large_domain(sx, oracle, case, bucketed):
+    """Domains whose counters exceed half of L2 take the bucketed cold path
+    (bucket.cuh); 'one_bucket' overflows a bucket and exercises the fallback."""
+    d, n = 1 << 25, (1 << 22) + 5
+    rng = np.random.default_rng(17)
+    if case == "zipf":
+        cdf = sx.zipf_cdf(d, 1.1)
+        f = np.ascontiguousarray(np_(sx.generate_zipf(cu(cdf), n, 3, rank_to_id=cu(sx.random_bijection(d, 3)))))
+    elif case == "uniform":
+        f = rng.integers(1, d + 1, size=n, dtype=np.uint32)
+    else:
+        f = rng.integers(1, 32769, size=n, dtype=np.uint32)
+    exp = oracle.count_frequencies(f, d)
+    ctx = sx.context(0)
+    ctx.check(ctx.lib.skx_set_histogram_mode(ctx.handle, bucketed))
+    assert np.array_equal(np_(sx.count_frequencies(cu(f), d).counts), exp)
+    assert np.array_equal(np_(sx.histogram_u32(cu(f), d)).astype(np.uint64), exp)
+    idx = sx.rebuild(cu(f), d)
+    ctx.check(ctx.lib.skx_set_histogram_mode(ctx.handle, 0))
+    off, rk = oracle.build_index(exp, n)
+    assert np.array_equal(np_(idx.offsets), off) and np.array_equal(np_(idx.ranks), rk)
