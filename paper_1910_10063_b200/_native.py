@@ -62,6 +62,7 @@ SIGNATURES = {
     "skx_device_info": (_int, [_vp, _vp, _int]),
     "skx_reset_persisting_l2": (_int, [_vp]),
     "skx_set_histogram_mode": (_int, [_vp, _int]),
+    "skx_set_aggregate_mode": (_int, [_vp, _int]),
     "skx_set_gather_tiers": (_int, [_vp, _u64, _u64, _dbl]),
     "skx_device_alloc": (_int, [_vp, _u64, C.POINTER(_vp)]),
     "skx_device_free": (_int, [_vp, _vp]),

@@ -27,6 +27,7 @@ namespace skx {
 namespace {
 
 constexpr int kThreads = 1024;
+constexpr int kMaxBuckets = 64;
 
 template <int MW>
 __device__ __forceinline__ void load_measure4(const void* measure, uint64_t row, bool vec,
@@ -75,6 +76,14 @@ struct HotBins {
 // : the caller's counts[limit] (one RED per tail row).
 struct Tail {
   unsigned long long* pairs;
+  // Staged tail (STG): rows of cold keys are appended per key-range bucket
+  // and folded by k_agg_fold while the bucket's pairs are L2-resident.
+  unsigned long long* cursors;  // [nb]
+  uint32_t* keys;               // [nb][cap]
+  unsigned long long* ms;       // [nb][cap]
+  uint64_t cap;
+  uint32_t nb;
+  uint32_t wshift;              // bucket = (idx - hot) >> wshift
 };
 
 __device__ __forceinline__ void hot_add(const HotBins& b, uint32_t idx, unsigned long long m,
@@ -168,6 +177,118 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// Staged variant (MW != 0, tail pairs >> L2): block-synchronous rounds of
+// kThreads x 4 rows.  Hot rows go to the shared bins; cold rows claim a slot
+// in their key-range bucket with a shared atomic, one thread per bucket
+// reserves the round's slots with ONE global atomic, and the rows are written
+// to the bucket buffers.  k_agg_fold later applies them bucket by bucket.
+template <int MW>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_aggregate_staged(const uint32_t* __restrict__ fact, const void* __restrict__ measure,
+                       uint64_t head, uint64_t nvec, uint64_t n, uint32_t d, uint32_t hot, bool mvec,
+                       Tail t, DevErr* err) {
+  extern __shared__ uint32_t smem_agg[];
+  HotBins b{smem_agg, smem_agg + hot, smem_agg + 2 * (size_t)hot};
+  __shared__ unsigned int s_cnt[kMaxBuckets];
+  __shared__ unsigned long long s_base[kMaxBuckets];
+  for (uint32_t i = threadIdx.x; i < hot; i += kThreads) {
+    b.cnt[i] = 0u;
+    b.lo[i] = 0u;
+    b.hi[i] = 0u;
+  }
+  const uint64_t pol = policy_evict_first();
+  const uint4* fv = reinterpret_cast<const uint4*>(fact + head);
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  const uint64_t nvec_round = (nvec + kThreads - 1) / kThreads * kThreads;
+  for (uint64_t base = (uint64_t)blockIdx.x * kThreads; base < nvec_round; base += stride) {
+    if (threadIdx.x < t.nb) s_cnt[threadIdx.x] = 0u;
+    __syncthreads();
+    const uint64_t vi = base + threadIdx.x;
+    const bool live = vi < nvec;
+    uint4 f = make_uint4(0, 0, 0, 0);
+    unsigned long long m[4] = {0, 0, 0, 0};
+    if (live) {
+      f = ld_stream_v4(fv + vi, pol);
+      load_measure4<MW>(measure, head + vi * 4, mvec, pol, m);
+    }
+    const uint32_t ids[4] = {f.x, f.y, f.z, f.w};
+    uint32_t slot[4], bk[4];
+    bool staged[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      staged[j] = false;
+      if (!live) continue;
+      const uint32_t idx = ids[j] - 1u;
+      if (idx >= d) {
+        record_violation(err, head + vi * 4 + j, ids[j]);
+      } else if (idx < hot) {
+        hot_add(b, idx, m[j], true);
+      } else {
+        bk[j] = (idx - hot) >> t.wshift;
+        slot[j] = atomicAdd(&s_cnt[bk[j]], 1u);
+        staged[j] = true;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < t.nb && s_cnt[threadIdx.x])
+      s_base[threadIdx.x] = atomicAdd(&t.cursors[threadIdx.x], (unsigned long long)s_cnt[threadIdx.x]);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (!staged[j]) continue;
+      const uint32_t idx = ids[j] - 1u;
+      const unsigned long long pos = s_base[bk[j]] + slot[j];
+      if (pos < t.cap) {
+        const uint64_t at = (uint64_t)bk[j] * t.cap + pos;
+        t.keys[at] = idx;
+        t.ms[at] = m[j];
+      } else {
+        tail_add(t, idx, m[j]);  // bucket full: direct update
+      }
+    }
+  }
+  if (blockIdx.x == 0) {
+    const uint64_t tail_b = head + nvec * 4;
+    const uint64_t extra = head + (n - tail_b);
+    for (uint64_t k0 = threadIdx.x; k0 < extra; k0 += kThreads) {
+      const uint64_t k = k0 < head ? k0 : tail_b + (k0 - head);
+      const uint32_t id = fact[k];
+      const uint32_t idx = id - 1u;
+      if (idx < d)
+        agg_row<MW>(idx, load_measure1<MW>(measure, k), hot, d, b, t);
+      else
+        record_violation(err, k, id);
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < hot; i += kThreads) {
+    const unsigned long long c = b.cnt[i];
+    if (c) {
+      atomicAdd(&t.pairs[2 * (uint64_t)i], c);
+      atomicAdd(&t.pairs[2 * (uint64_t)i + 1], ((unsigned long long)b.hi[i] << 32) | b.lo[i]);
+    }
+  }
+}
+
+// Apply the staged cold rows bucket by bucket: all CTAs sweep bucket b
+// together, so the 16 B/key pairs they update (one bucket's key range) stay
+// L2-resident instead of read-modify-writing HBM lines.
+__global__ void __launch_bounds__(512)
+    k_agg_fold(Tail t) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint32_t bk = 0; bk < t.nb; ++bk) {
+    const uint64_t m = t.cursors[bk] < t.cap ? t.cursors[bk] : t.cap;
+    const uint32_t* keys = t.keys + (uint64_t)bk * t.cap;
+    const unsigned long long* ms = t.ms + (uint64_t)bk * t.cap;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+      const uint32_t idx = __ldcs(keys + i);
+      const unsigned long long v = __ldcs(ms + i);
+      atomicAdd(&t.pairs[2 * (uint64_t)idx], 1ull);
+      atomicAdd(&t.pairs[2 * (uint64_t)idx + 1], v);
+    }
+  }
+}
+
 __global__ void k_deinterleave(const unsigned long long* __restrict__ pairs, uint32_t d,
                                unsigned long long* __restrict__ counts,
                                unsigned long long* __restrict__ sums) {
@@ -199,10 +320,34 @@ int aggregate_impl(skx_ctx* ctx, const uint32_t* fact, const void* measure, uint
   if (hot_req && hot_req < hot) hot = hot_req;
   if (hot > limit) hot = limit;
   const size_t smem = (size_t)hot * per_key;
-  cudaFuncSetAttribute(k_aggregate<MW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_aggregate<MW><<<grid, kThreads, smem, s>>>(fact, measure, head, nvec, n, d, limit, hot, mvec, t,
-                                               ctx->err);
-  ctx->launches++;
+  // Stage the cold tail when its pairs overflow half of L2 (MW != 0 only).
+  const uint64_t tail_keys = limit > hot ? limit - hot : 0;
+  if (MW && limit == d && ctx->agg_staged && tail_keys * 16 > ctx->l2_bytes / 2 &&
+      n >= (uint64_t(1) << 20)) {
+    uint32_t wshift = 20;  // 1M keys x 16 B = 16 MiB of pairs per bucket
+    while (((tail_keys + (uint64_t(1) << wshift) - 1) >> wshift) > (uint64_t)kMaxBuckets) ++wshift;
+    t.nb = (uint32_t)((tail_keys + (uint64_t(1) << wshift) - 1) >> wshift);
+    t.wshift = wshift;
+    t.cap = n / (2 * (uint64_t)t.nb) + 4096;
+    const uint64_t kb = ((uint64_t)t.nb * t.cap * 4 + 255) & ~uint64_t(255);
+    char* sp = static_cast<char*>(scratch(ctx, 0, 256 + kb + (uint64_t)t.nb * t.cap * 8));
+    if (!sp) return set_error(ctx, SKX_CUDA_ERROR, "aggregate: out of device memory for staging");
+    t.cursors = reinterpret_cast<unsigned long long*>(sp);
+    t.keys = reinterpret_cast<uint32_t*>(sp + 256);
+    t.ms = reinterpret_cast<unsigned long long*>(sp + 256 + kb);
+    cudaError_t e = cudaMemsetAsync(t.cursors, 0, 256, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "aggregate memset");
+    cudaFuncSetAttribute(k_aggregate_staged<MW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_aggregate_staged<MW><<<grid, kThreads, smem, s>>>(fact, measure, head, nvec, n, d, hot, mvec,
+                                                        t, ctx->err);
+    k_agg_fold<<<grid_for(ctx, n, 512, 4), 512, 0, s>>>(t);
+    ctx->launches += 2;
+  } else {
+    cudaFuncSetAttribute(k_aggregate<MW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_aggregate<MW><<<grid, kThreads, smem, s>>>(fact, measure, head, nvec, n, d, limit, hot, mvec,
+                                                 t, ctx->err);
+    ctx->launches++;
+  }
   SKX_CHECK_LAUNCH(ctx, "aggregate");
   return SKX_OK;
 }
@@ -224,7 +369,7 @@ int launch_aggregate(skx_ctx* ctx, const uint32_t* fact, const void* measure, in
     if (sums && e == cudaSuccess) e = cudaMemsetAsync(sums, 0, (size_t)d * 8, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "aggregate memset");
     if (n == 0) return SKX_OK;
-    Tail t{reinterpret_cast<unsigned long long*>(counts)};
+    Tail t{reinterpret_cast<unsigned long long*>(counts), nullptr, nullptr, nullptr, 0, 0, 0};
     return aggregate_impl<0>(ctx, fact, nullptr, n, d, d, hot, t, s);
   }
   unsigned long long* pairs =
@@ -232,7 +377,7 @@ int launch_aggregate(skx_ctx* ctx, const uint32_t* fact, const void* measure, in
   if (!pairs) return set_error(ctx, SKX_CUDA_ERROR, "aggregate: out of device memory");
   cudaError_t e = cudaMemsetAsync(pairs, 0, (size_t)d * 16, s);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "aggregate memset");
-  Tail t{pairs};
+  Tail t{pairs, nullptr, nullptr, nullptr, 0, 0, 0};
   int rc = SKX_OK;
   if (n > 0) {
     rc = mw == 8 ? aggregate_impl<8>(ctx, fact, measure, n, d, d, hot, t, s)
@@ -273,7 +418,7 @@ int skx_heavy_hitter_count(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint3
     if (e != cudaSuccess) return skx::cuda_fail(ctx, e, "heavy_hitter memset");
   }
   if (n == 0) return SKX_OK;
-  skx::Tail t{reinterpret_cast<unsigned long long*>(counts)};
+  skx::Tail t{reinterpret_cast<unsigned long long*>(counts), nullptr, nullptr, nullptr, 0, 0, 0};
   return skx::aggregate_impl<0>(ctx, fact, nullptr, n, d, cutoff, cutoff, t, s);
 }
 

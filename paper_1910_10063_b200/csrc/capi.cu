@@ -128,7 +128,7 @@ int skx_ctx_destroy(skx_ctx* ctx) {
 uint64_t skx_launch_count(const skx_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
 
 int skx_set_gather_policy(skx_ctx* ctx, int policy) {
-  if (!ctx || policy < 0 || policy > 1023) return SKX_INVALID_ARGUMENT;
+  if (!ctx || policy < 0 || policy > 2047) return SKX_INVALID_ARGUMENT;
   cudaSetDevice(ctx->device);
   const bool want = (policy & 4) != 0 && ctx->persist_max > 0;
   if (want != ctx->setaside_on) {
@@ -152,6 +152,12 @@ int skx_set_gather_tiers(skx_ctx* ctx, uint64_t smem_bytes, uint64_t l1_bytes, d
 int skx_set_histogram_mode(skx_ctx* ctx, int bucketed) {
   if (!ctx || bucketed < 0 || bucketed > 1) return SKX_INVALID_ARGUMENT;
   ctx->hist_bucketed = bucketed != 0;
+  return SKX_OK;
+}
+
+int skx_set_aggregate_mode(skx_ctx* ctx, int staged) {
+  if (!ctx || staged < 0 || staged > 1) return SKX_INVALID_ARGUMENT;
+  ctx->agg_staged = staged != 0;
   return SKX_OK;
 }
 

@@ -203,7 +203,11 @@ __global__ void __launch_bounds__((F & kPolHot) ? kThreadsHot : kThreads, (F & k
           } else if (NOL1) {
             v[u][j] = ld_dim_nol1<V>(dim + idx, pol_d);
           } else {
-            if constexpr ((F & 512) != 0 && sizeof(V) == 8) {  // .cg: cache in L2 only
+            if constexpr ((F & 1024) != 0 && sizeof(V) == 8) {  // coherent, no L1 allocation
+              uint64_t r;
+              asm volatile("ld.global.L1::no_allocate.u64 %0, [%1];" : "=l"(r) : "l"(dim + idx));
+              v[u][j] = (V)r;
+            } else if constexpr ((F & 512) != 0 && sizeof(V) == 8) {  // .cg: cache in L2 only
               v[u][j] = (V)__ldcg(reinterpret_cast<const unsigned long long*>(dim + idx));
             } else if constexpr ((F & 256) != 0 && sizeof(V) == 8) {  // coherent (non-.nc) load path
               uint64_t r;
@@ -319,7 +323,7 @@ cudaError_t dispatch_vec(skx_ctx* ctx, int F, const uint32_t* fact, uint64_t hea
                : launch_vec<V, OUT_VEC, (x)>(ctx, fact, head, nvec, dim, dim_len, out, t, s);
   SKX_F(0) SKX_F(1) SKX_F(3) SKX_F(9) SKX_F(17) SKX_F(19)
   SKX_F(33) SKX_F(35) SKX_F(49) SKX_F(51) SKX_F(65) SKX_F(97) SKX_F(69) SKX_F(129) SKX_F(128)
-  SKX_F(131) SKX_F(385) SKX_F(641)
+  SKX_F(131) SKX_F(385) SKX_F(641) SKX_F(1153)
 #undef SKX_F
   return cudaErrorInvalidValue;
 }

@@ -146,6 +146,7 @@ struct skx_ctx {
   size_t tier_l1_bytes = 160 * 1024;  // gather tier t1 (bytes of the dimension prefix)
   double tier_l2_frac = 0.6;          // gather tier t2 (share of L2)
   bool hist_bucketed = false;         // histogram cold keys via key-range buckets
+  bool agg_staged = false;            // group-by cold tail staged per key range (measured slower at s>=1)
   std::atomic<uint64_t> launches{0};
   skx_error_info last{};
   // scratch arenas (grow-only)

@@ -1,3 +1,2 @@
-python -m pytest tests/test_gpu_parity.py tests/test_gpu_refsuite.py -q -x 2>&1 | tail -3
-python tools/index_sweep.py 2>&1 | tail -1
-python tools/index_sweep.py --domain 134217728 --z 1.0 2>&1 | tail -1
+python tools/gather_sweep.py --z 1.0,1.5 --gran 0 --policies 129,641,1153 2>&1 | grep -v device_info | cut -c1-100
+python tools/gather_ceilings.py 129,1153 2>&1 | grep -E "L2_random|DRAM"
