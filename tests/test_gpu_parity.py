@@ -313,3 +313,21 @@ def test_histogram_bucketed_large_domain(sx, oracle, case, bucketed):
     ctx.check(ctx.lib.skx_set_histogram_mode(ctx.handle, 0))
     off, rk = oracle.build_index(exp, n)
     assert np.array_equal(np_(idx.offsets), off) and np.array_equal(np_(idx.ranks), rk)
+
+
+@pytest.mark.parametrize("staged", [0, 1])
+@pytest.mark.parametrize("z", [0.0, 0.8])
+def test_aggregate_large_domain_modes(sx, oracle, staged, z):
+    """Tail pairs larger than half of L2: direct reductions (default) and the
+    staged per-bucket path (uniform data overflows the buckets -> fallback)."""
+    d, n = 1 << 23, (1 << 22) + 3
+    fact = sx.generate_zipf(cu(sx.zipf_cdf(d, z)), n, 21)  # rank space
+    meas = np.random.default_rng(9).integers(1, 101, size=n, dtype=np.int64)
+    ctx = sx.context(0)
+    ctx.check(ctx.lib.skx_set_aggregate_mode(ctx.handle, staged))
+    try:
+        c, s = sx.aggregate_count_sum(fact, cu(meas), d)
+    finally:
+        ctx.check(ctx.lib.skx_set_aggregate_mode(ctx.handle, 0))
+    ce, se = oracle.aggregate_count_sum(np_(fact), meas.view(np.uint64), d)
+    assert np.array_equal(np_(c), ce) and np.array_equal(np_(s), se)
