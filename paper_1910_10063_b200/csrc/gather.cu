@@ -29,7 +29,7 @@ namespace {
 
 constexpr int kThreads = 256;      // plain variant: several CTAs per SM
 constexpr int kThreadsHot = 1024;  // hot-prefix variant: one CTA per SM owns the smem copy
-constexpr int kUnroll = 4;         // uint4 FK vectors per thread per iteration (16 rows)
+constexpr int kUnroll = 8;         // uint4 FK vectors per thread per iteration (32 rows)
 
 // Policy bits (skx_set_gather_policy).
 constexpr int kPolHints = 1;   // evict_first streams, evict_last dimension
@@ -133,7 +133,7 @@ __device__ __forceinline__ V ld_dim_l1p(const V* p, uint64_t pol) {
 // Vector body: rows [head, head + 4*nvec) where fact + head is 16B aligned.
 // OUT_VEC: out + head is aligned for Pack4 stores.
 template <typename V, bool OUT_VEC, int F>
-__global__ void __launch_bounds__((F & kPolHot) ? kThreadsHot : kThreads, (F & kPolHot) ? 1 : 4)
+__global__ void __launch_bounds__((F & kPolHot) ? kThreadsHot : kThreads, (F & kPolHot) ? 1 : 2)
     k_gather_vec(const uint32_t* __restrict__ fact, uint64_t head, uint64_t nvec,
                  const V* __restrict__ dim, uint64_t dim_len, V* __restrict__ out, DevErr* err,
                  GatherTiers tiers) {
@@ -280,7 +280,10 @@ cudaError_t launch_vec(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(HOT ? kThreadsHot : kThreads);
   cfg.gridDim = dim3(HOT ? grid_for(ctx, nvec, kThreadsHot * kUnroll, 1)
-                         : grid_for(ctx, nvec, kThreads * kUnroll, 8));
+                         // small columns: exactly the 2 resident CTAs/SM (no tail wave);
+                         // large ones: 8/SM so the scheduler balances SM speed differences
+                         : grid_for(ctx, nvec, kThreads * kUnroll,
+                                    nvec / (kThreads * kUnroll) < 16u * 2u * ctx->num_sms ? 2 : 8));
   cfg.dynamicSmemBytes = HOT ? (size_t)hot * sizeof(V) : 0;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
