@@ -1,3 +1,2 @@
-python tools/gather_sweep.py --z 1.0,1.5 --gran 0 --policies 129 > gpurun_out/gs.log 2>&1
-python tools/gather_sweep.py --z 1.0 --gran 0 --policies 129 --width 4 --domain 4194304 --rows 16777216 --steps 50 >> gpurun_out/gs.log 2>&1
-cut -c1-100 gpurun_out/gs.log
+timeout 120 python -m pytest tests/test_gpu_parity.py -q -x -k "aggregate or golden or kat" 2>&1 | tail -2
+timeout 120 python tools/groupby_sweep.py --z 1.0,1.5,0.5 --modes 0 2>&1 | grep count_sum | cut -c1-110
