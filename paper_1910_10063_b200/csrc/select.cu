@@ -80,13 +80,34 @@ __global__ void __launch_bounds__(kThreads)
   __syncthreads();
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint64_t row0 = tile * kTile + (uint64_t)w * (kItems * 32);
+    // All 16 FK loads first, then all 16 bitmap probes, then the ballots: two
+    // round trips per tile instead of sixteen dependent ones.
+    uint32_t fk[kItems];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      const uint64_t k = row0 + i * 32 + lane;
+      fk[i] = k < n ? ld_stream_u32(fact + k, pol) : 1u;
+    }
+    bool sel[kItems];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      const uint64_t k = row0 + i * 32 + lane;
+      const uint32_t idx = fk[i] - 1u;
+      sel[i] = false;
+      if (k < n) {
+        if (idx < bits) {
+          const uint32_t wi = idx >> 6;
+          const unsigned long long wv = wi < sw ? s_words[wi] : __ldg(words + wi);
+          sel[i] = (wv >> (idx & 63)) & 1ull;
+        } else {
+          record_violation(err, k, fk[i]);
+        }
+      }
+    }
     uint32_t c = 0, mine = 0;
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
-      uint32_t idx;
-      const uint32_t b = __ballot_sync(
-          0xffffffffu,
-          probe(fact, row0 + i * 32 + lane, n, words, bits, s_words, sw, pol, true, err, idx));
+      const uint32_t b = __ballot_sync(0xffffffffu, sel[i]);
       c += __popc(b);
       if (lane == i) mine = b;
     }
@@ -116,20 +137,24 @@ __global__ void __launch_bounds__(kThreads)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(smem_raw);             // [kTile]
   uint16_t* s_row = reinterpret_cast<uint16_t*>(s_idx + kTile);        // [kTile]
-  double* s_sums = reinterpret_cast<double*>(s_row + kTile);           // [kWarps][ncat] (FUSED)
   __shared__ uint32_t s_w[kWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const bool smem_sums = FUSED && cols.n_categories <= kSmemCategories;
-  if (smem_sums)
-    for (uint32_t i = threadIdx.x; i < kWarps * cols.n_categories; i += kThreads) s_sums[i] = 0.0;
   if (blockIdx.x == 0 && threadIdx.x == 0) *count_dev = *total;
   const uint64_t ntiles = (n + kTile - 1) / kTile;
   const uint64_t pol = policy_evict_first();
   const uint32_t lt = lanemask_lt();
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint64_t row0 = tile * kTile + (uint64_t)w * (kItems * 32);
-    // (A) this warp's 16 mask words: lane i holds word i
+    // (A) this warp's 16 mask words (lane i holds word i) and, in the same
+    // round trip, all 512 of its FK values (coalesced; at ~10% selectivity
+    // the selected rows' sectors would be fetched anyway).
     const uint32_t mw = lane < kItems ? __ldg(mask + (row0 >> 5) + lane) : 0u;
+    uint32_t fk[kItems];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      const uint64_t k = row0 + i * 32 + lane;
+      fk[i] = k < n ? ld_stream_u32(fact + k, pol) : 0u;
+    }
     uint32_t c = 0;
 #pragma unroll
     for (int i = 0; i < kItems; ++i) c += __popc(__shfl_sync(0xffffffffu, mw, i));
@@ -145,7 +170,7 @@ __global__ void __launch_bounds__(kThreads)
       if ((m >> lane) & 1u) {
         const uint32_t r = (uint32_t)(w * (kItems * 32) + i * 32 + lane);
         const uint32_t j = lpos + __popc(m & lt);
-        s_idx[j] = ld_stream_u32(fact + tile * kTile + r, pol) - 1u;
+        s_idx[j] = fk[i] - 1u;
         s_row[j] = (uint16_t)r;
       }
       lpos += __popc(m);
@@ -173,32 +198,62 @@ __global__ void __launch_bounds__(kThreads)
           cols.out_flag[p] = fl;
         }
       }
-      if (FUSED) {
-        // SUM(price) per category: lanes of one category elect a leader that
-        // adds the group's fp64 sum to its warp-private bin (no fp64 atomics).
-        const bool ok = live && (uint32_t)ct < cols.n_categories;
-        const uint32_t key = ok ? (uint32_t)ct : 0xFFFFFFFFu;
-        const uint32_t peers = __match_any_sync(0xffffffffu, key);
-        if (ok) {
-          double grp = 0.0;
-          for (uint32_t m = peers; m; m &= m - 1)
-            grp += __shfl_sync(peers, (double)pr, __ffs(m) - 1);
-          if (lane == __ffs(peers) - 1) {
-            if (smem_sums)
-              s_sums[(size_t)w * cols.n_categories + ct] += grp;
-            else
-              atomicAdd(&cols.sums[ct], grp);
-          }
-        }
-      }
     }
     __syncthreads();  // s_idx / s_row / s_w reused by the next tile
   }
-  if (smem_sums) {
-    for (uint32_t i = threadIdx.x; i < cols.n_categories; i += kThreads) {
+}
+
+// Pass 3 (C5): SUM(price) per category over the compacted selected rows --
+// a coalesced read of the gathered category/price columns.  Warp-private
+// fp64 shared bins; lanes of one category pre-sum with __match_any_sync +
+// shuffles (shared fp64 atomics are CAS spin loops on sm_100a); one native
+// global fp64 reduction per bin per CTA.
+__global__ void __launch_bounds__(kThreads)
+    k_category_sum(const int32_t* __restrict__ cat, const float* __restrict__ price,
+                   const uint32_t* __restrict__ total, uint32_t n_categories,
+                   double* __restrict__ sums) {
+  extern __shared__ double s_bins[];  // [kWarps][n_categories] when small
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const bool smem = n_categories <= kSmemCategories;
+  if (smem) {
+    for (uint32_t i = threadIdx.x; i < kWarps * n_categories; i += kThreads) s_bins[i] = 0.0;
+    __syncthreads();
+  }
+  constexpr int U = 8;  // rows per thread per iteration, loads issued first
+  const uint64_t cnt = *total;
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads * U;
+  for (uint64_t j0 = (uint64_t)blockIdx.x * kThreads * U; j0 < cnt; j0 += stride) {  // uniform trips
+    int32_t ct[U];
+    float pr[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t j = j0 + (uint64_t)u * kThreads + threadIdx.x;
+      ct[u] = j < cnt ? __ldcs(cat + j) : -1;
+      pr[u] = j < cnt ? __ldcs(price + j) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool ok = (uint32_t)ct[u] < n_categories;
+      const uint32_t peers = __match_any_sync(0xffffffffu, ok ? (uint32_t)ct[u] : 0xFFFFFFFFu);
+      if (ok) {
+        double grp = 0.0;
+        for (uint32_t m = peers; m; m &= m - 1)
+          grp += __shfl_sync(peers, (double)pr[u], __ffs(m) - 1);
+        if (lane == __ffs(peers) - 1) {
+          if (smem)
+            s_bins[(size_t)w * n_categories + ct[u]] += grp;
+          else
+            atomicAdd(&sums[ct[u]], grp);
+        }
+      }
+    }
+  }
+  if (smem) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n_categories; i += kThreads) {
       double v = 0.0;
-      for (int ww = 0; ww < kWarps; ++ww) v += s_sums[(size_t)ww * cols.n_categories + i];
-      if (v != 0.0) atomicAdd(&cols.sums[i], v);
+      for (int ww = 0; ww < kWarps; ++ww) v += s_bins[(size_t)ww * n_categories + i];
+      if (v != 0.0) atomicAdd(&sums[i], v);
     }
   }
 }
@@ -271,10 +326,7 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
   ctx->launches++;
   int rc = launch_exclusive_scan_u32(ctx, counts, offs, ntiles, total, 3, s);
   if (rc) return rc;
-  const size_t tile_smem = (size_t)kTile * (4 + 2);
-  const size_t smem = tile_smem + ((fused && cols.n_categories <= kSmemCategories)
-                                       ? (size_t)kWarps * cols.n_categories * 8
-                                       : 0);
+  const size_t smem = (size_t)kTile * (4 + 2);
   int per_sm = 0;
   if (fused) {
     cudaFuncSetAttribute(k_select_write<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -282,6 +334,16 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
     const unsigned grid2 = grid_for(ctx, ntiles, 1, per_sm < 1 ? 1 : per_sm);
     k_select_write<true><<<grid2, kThreads, smem, s>>>(fact, n, mask, base, offs, total, out, cols,
                                                       reinterpret_cast<unsigned long long*>(count_dev));
+    if (cols.n_categories) {
+      const size_t bsmem =
+          cols.n_categories <= kSmemCategories ? (size_t)kWarps * cols.n_categories * 8 : 0;
+      cudaFuncSetAttribute(k_category_sum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
+      int per_sm3 = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, k_category_sum, kThreads, bsmem);
+      k_category_sum<<<(unsigned)ctx->num_sms * (per_sm3 < 1 ? 1 : per_sm3), kThreads, bsmem, s>>>(
+          cols.out_cat, cols.out_price, total, cols.n_categories, cols.sums);
+      ctx->launches++;
+    }
   } else {
     cudaFuncSetAttribute(k_select_write<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_write<false>, kThreads, smem);
