@@ -8,17 +8,19 @@
 // permute_bitmap (operators.cpp:21-30), build_bitmap (operators.hpp:38-45).
 //
 // B200 design: two streaming passes over the
-// FK column with a device scan between them -- pass 1 counts each 4096-row
-// tile's selected rows (ballots), the scan turns the counts into tile
-// offsets, pass 2 re-probes and writes each selected row at
-// tile offset + rank in tile: ascending row order, exactly the reference's
-// chunk-ordered concatenation.  (A single-pass decoupled look-back version
-// was measured 8-10x slower on B200: CTAs stall on the look-back chain,
-// profiles/r1_experiments.md.)  Pass 2 of the C5 variant gathers category /
-// price / supplier / flag for the selected rows and sums price per category
-// in warp-private fp64 shared bins: lanes of one category are pre-summed
-// with __match_any_sync + shuffles, because shared fp64 atomics compile to
-// CAS spin loops on sm_100a.  Bins are flushed once per CTA.
+// FK column with a device scan between them -- pass 1 probes every row once,
+// writes a 1-bit/row selection mask and counts each 4096-row tile's selected
+// rows; the scan turns the counts into tile offsets; pass 2 reads the mask
+// and the FKs, compacts the tile's selected rows in shared memory and writes
+// each at tile offset + rank in tile: ascending row order, exactly the
+// reference's chunk-ordered concatenation.  (A single-pass decoupled
+// look-back version was measured ~2x slower on B200: CTAs stall behind the
+// look-back chain, profiles/r1_experiments.md.)  The C5 variant gathers
+// category / price / supplier / flag for the selected rows in pass 2, and a
+// third pass sums price per category over the compacted columns in
+// warp-private fp64 shared bins: lanes of one category are pre-summed with
+// __match_any_sync + shuffles, because shared fp64 atomics compile to CAS
+// spin loops on sm_100a.  Bins are flushed once per CTA.
 #include "scan.cuh"
 
 namespace skx {
