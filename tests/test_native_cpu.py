@@ -91,3 +91,22 @@ def test_error_taxonomy():
     assert isinstance(e, Error) and e.row() == 2 and e.value() == 4
     assert str(e) == "domain violation at row 2: value 4 outside 1..3"
     assert issubclass(InvalidArgument, Error)
+
+
+def test_cpp_dropin_exports_reference_api():
+    """libskewdx_b200.so provides the reference's C++ operator API (namespace
+    skewdx, same signatures) on top of libskx.so."""
+    so = os.path.join(ROOT, "paper_1910_10063_b200", "libskewdx_b200.so")
+    if not os.path.exists(so):
+        from paper_1910_10063_b200.build import build_shim
+        build_shim()
+    syms = os.popen(f"nm -DC --defined-only {so}").read()
+    for fn in ["skewdx::count_frequencies(", "skewdx::build_index(", "skewdx::recode_fact(",
+               "skewdx::permute_dimension(", "skewdx::rebuild(", "skewdx::materialize(",
+               "skewdx::select(", "skewdx::aggregate_count(", "skewdx::aggregate_sum(",
+               "skewdx::parallel_materialize(", "skewdx::parallel_select(",
+               "skewdx::parallel_aggregate(", "skewdx::chunk_spans(",
+               "skewdx::heavy_hitter_count(", "skewdx::permute_bitmap(",
+               "skewdx::generate_fact_column(", "skewdx::read_index(", "skewdx::write_index("]:
+        assert fn in syms, fn
+    assert "libskx.so" in os.popen(f"ldd {so}").read()
