@@ -237,10 +237,16 @@ int skx_set_gather_tiers(skx_ctx* ctx, uint64_t smem_bytes, uint64_t l1_bytes,
  * 0 = direct global reductions (default, faster as measured), 1 = key-range
  * buckets folded in shared memory (csrc/bucket.cuh). */
 int skx_set_histogram_mode(skx_ctx* ctx, int bucketed);
-/* Group-by cold tail when its {count,sum} pairs exceed half of L2:
- * 1 = staged per key-range bucket and folded while L2-resident (default),
- * 0 = direct global reductions. */
-int skx_set_aggregate_mode(skx_ctx* ctx, int staged);
+/* Group-by (measure_width 4/8) cold-tail strategy:
+ * 0 = packed (default): one 64-bit reduction of (1 << 40 | m) per cold row
+ *     into an 8 B/key accumulator, decoded and validated on the device
+ *     against exact per-launch totals; rows with m >= 2^16 or a failed check
+ *     rerun the call through mode 2 on the device (no host round trip);
+ * 1 = staged per key-range bucket and folded while L2-resident, when the
+ *     tail pairs exceed half of L2 (else mode 2);
+ * 2 = direct: two 64-bit reductions per cold row on an interleaved
+ *     {count, sum} pair. */
+int skx_set_aggregate_mode(skx_ctx* ctx, int mode);
 /* cudaCtxResetPersistingL2Cache: demote lines left persisting by windows. */
 int skx_reset_persisting_l2(skx_ctx* ctx);
 /* info[0..n): num_sms, smem_optin, l2_bytes, persisting-L2 max, access-policy

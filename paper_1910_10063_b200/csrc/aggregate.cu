@@ -15,12 +15,20 @@
 // serialises on the hottest keys), while 32-bit adds are native and merge
 // same-address lanes.  A 64-bit per-bin sum is kept as lo/hi words.
 //
-// Tail keys (id > H) go to global 64-bit reductions (RED, fire-and-forget)
-// on an interleaved {count, sum} pair, so both updates of a row land in the
-// same 32-byte sector: measured 1.46x faster than separate count/sum arrays
-// and 1.43x faster than a single packed (count << 40 | sum) word, whose
-// exactness needs the returning ATOM form.  A final pass de-interleaves the
-// pairs into the caller's counts[] / sums[].
+// Tail keys (id > H), default "packed" mode: ONE fire-and-forget 64-bit
+// reduction of (1 << 40 | m) per cold row into an 8 B/key accumulator, so a
+// key's count lands in bits 40..63 and its sum in bits 0..39.  That halves
+// both the reductions and the accumulator footprint of the {count, sum} pair
+// layout (tools/probe/agg_probe.cu: 9.6 -> 5.9 ms at C3).  Exactness is
+// proved on the device, not assumed: every CTA also counts its packed rows
+// and their measure sum exactly; the decode pass sums the decoded fields; a
+// key whose sum reached 2^40 (or whose count reached 2^24) makes the decoded
+// totals fall short, because every decoded field is <= its true value with
+// equality iff it did not overflow.  Rows with m >= 2^16 are not packed (so
+// the exact totals cannot wrap) and flag the launch.  On any flag or
+// mismatch three gated kernels, already queued behind the decode, redo the
+// whole call with two exact reductions per cold row on an interleaved
+// {count, sum} pair (mode 2); otherwise they exit at once.  No host sync.
 #include "skx_internal.cuh"
 
 namespace skx {
@@ -39,7 +47,7 @@ __device__ __forceinline__ void load_measure4(const void* measure, uint64_t row,
   if (MW == 8) {
     const unsigned long long* p = static_cast<const unsigned long long*>(measure) + row;
     if (vec) {
-      const uint4 a = ld_stream_v4(p, pol), b = ld_stream_v4(p + 2, pol);
+      const uint4 a = ld_cs_v4(p), b = ld_cs_v4(p + 2);
       m[0] = a.x | ((unsigned long long)a.y << 32);
       m[1] = a.z | ((unsigned long long)a.w << 32);
       m[2] = b.x | ((unsigned long long)b.y << 32);
@@ -51,7 +59,7 @@ __device__ __forceinline__ void load_measure4(const void* measure, uint64_t row,
   } else if (MW == 4) {
     const uint32_t* p = static_cast<const uint32_t*>(measure) + row;
     if (vec) {
-      const uint4 a = ld_stream_v4(p, pol);
+      const uint4 a = ld_cs_v4(p);
       m[0] = a.x, m[1] = a.y, m[2] = a.z, m[3] = a.w;
     } else {
 #pragma unroll
@@ -76,10 +84,30 @@ struct HotBins {
   uint32_t* hi;
 };
 
-// Global accumulators: MW ? interleaved {count, sum} pairs[limit][2]
-// : the caller's counts[limit] (one RED per tail row).
+// Device-side exactness check of the packed tail (see the header).
+struct AggCheck {
+  unsigned long long tail_rows;  // rows reduced into acc (exact)
+  unsigned long long tail_sum;   // their measure sum (exact, < 2^50)
+  unsigned long long dec_rows;   // sum of decoded counts
+  unsigned long long dec_sum;    // sum of decoded sums
+  unsigned int big;              // a cold row had m >= 2^16 (not packed)
+  unsigned int pad[7];
+};
+constexpr unsigned long long kPackOne = 1ull << 40;
+constexpr unsigned long long kPackMax = 1ull << 16;  // packed measures are < 2^16
+constexpr unsigned long long kPackMask = kPackOne - 1;
+
+__device__ __forceinline__ bool agg_ok(const AggCheck* c) {
+  return c->big == 0 && c->dec_rows == c->tail_rows && c->dec_sum == c->tail_sum;
+}
+
+// Global accumulators: MW ? interleaved {count, sum} pairs[limit][2] (packed
+// mode: the hot keys' pairs only) : the caller's counts[limit] (one RED per
+// tail row).
 struct Tail {
   unsigned long long* pairs;
+  unsigned long long* acc;  // packed mode: [d] (count << 40 | sum)
+  AggCheck* chk;            // packed mode
   // Staged tail (STG): rows of cold keys are appended per key-range bucket
   // and folded by k_agg_fold while the bucket's pairs are L2-resident.
   unsigned long long* cursors;  // [nb]
@@ -106,26 +134,46 @@ __device__ __forceinline__ void tail_add(const Tail& t, uint32_t idx, unsigned l
   atomicAdd(&t.pairs[2 * (uint64_t)idx + 1], m);
 }
 
+// Per-thread exact totals of the packed rows.
+struct PackTally {
+  uint32_t rows = 0;
+  unsigned long long sum = 0;
+  bool big = false;
+};
+
 // One row: idx = id - 1 already domain-checked (idx < d).
-template <int MW>
+template <int MW, bool PACK>
 __device__ __forceinline__ void agg_row(uint32_t idx, unsigned long long m, uint32_t hot,
-                                        uint32_t limit, const HotBins& b, const Tail& t) {
+                                        uint32_t limit, const HotBins& b, const Tail& t,
+                                        PackTally& pt) {
   if (idx < hot) {
     hot_add(b, idx, m, MW != 0);
   } else if (idx < limit) {
-    if (MW)
-      tail_add(t, idx, m);
-    else
+    if (!MW) {
       atomicAdd(&t.pairs[idx], 1ull);
+    } else if (PACK) {
+      if (m < kPackMax) {
+        atomicAdd(&t.acc[idx], kPackOne | m);
+        ++pt.rows;
+        pt.sum += m;
+      } else {
+        pt.big = true;
+      }
+    } else {
+      tail_add(t, idx, m);
+    }
   }
 }
 
-template <int MW>
+template <int MW, bool PACK>
 __global__ void __launch_bounds__(kThreads, 1)
     k_aggregate(const uint32_t* __restrict__ fact, const void* __restrict__ measure, uint64_t head,
                 uint64_t nvec, uint64_t n, uint32_t d, uint32_t limit, uint32_t hot, bool mvec,
-                Tail t, DevErr* err) {
+                Tail t, DevErr* err, const AggCheck* gate) {
+  // Exact fallback of the packed mode: nothing to do when the check passed.
+  if (gate && agg_ok(gate)) return;
   extern __shared__ uint32_t smem_agg[];
+  PackTally pt;
   HotBins b{smem_agg, smem_agg + hot, smem_agg + 2 * (size_t)hot};  // lo/hi only if MW
   for (uint32_t i = threadIdx.x; i < hot; i += kThreads) {
     b.cnt[i] = 0u;
@@ -149,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int u = 0; u < kAggUnroll; ++u) {
       const uint64_t vi = vb + (uint64_t)u * kThreads;
       if (vi < nvec) {
-        f[u] = ld_stream_v4(fv + vi, pol);
+        f[u] = ld_cs_v4(fv + vi);
         load_measure4<MW>(measure, head + vi * 4, mvec, pol, m[u]);
       }
     }
@@ -166,7 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // (Warp pre-aggregation of equal hot keys with __match_any_sync +
         // __reduce_add_sync was measured 3.4x slower at Zipf 1.5: the
         // hardware already merges same-address 32-bit shared adds.)
-        if (ok) agg_row<MW>(idx, m[u][j], hot, limit, b, t);
+        if (ok) agg_row<MW, PACK>(idx, m[u][j], hot, limit, b, t, pt);
       }
     }
   }
@@ -178,9 +226,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t id = fact[k];
       const uint32_t idx = id - 1u;
       if (idx < d)
-        agg_row<MW>(idx, load_measure1<MW>(measure, k), hot, limit, b, t);
+        agg_row<MW, PACK>(idx, load_measure1<MW>(measure, k), hot, limit, b, t, pt);
       else
         record_violation(err, k, id);
+    }
+  }
+  if (PACK) {
+    unsigned long long r = pt.rows, sm = pt.sum;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      r += __shfl_down_sync(0xffffffffu, r, o);
+      sm += __shfl_down_sync(0xffffffffu, sm, o);
+    }
+    const bool big = __any_sync(0xffffffffu, pt.big);
+    if ((threadIdx.x & 31) == 0) {
+      if (r) atomicAdd(&t.chk->tail_rows, r);
+      if (sm) atomicAdd(&t.chk->tail_sum, sm);
+      if (big) atomicOr(&t.chk->big, 1u);
     }
   }
   __syncthreads();
@@ -276,8 +338,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t k = k0 < head ? k0 : tail_b + (k0 - head);
       const uint32_t id = fact[k];
       const uint32_t idx = id - 1u;
+      PackTally unused;
       if (idx < d)
-        agg_row<MW>(idx, load_measure1<MW>(measure, k), hot, d, b, t);
+        agg_row<MW, false>(idx, load_measure1<MW>(measure, k), hot, d, b, t, unused);
       else
         record_violation(err, k, id);
     }
@@ -313,7 +376,8 @@ __global__ void __launch_bounds__(512)
 
 __global__ void k_deinterleave(const unsigned long long* __restrict__ pairs, uint32_t d,
                                unsigned long long* __restrict__ counts,
-                               unsigned long long* __restrict__ sums) {
+                               unsigned long long* __restrict__ sums, const AggCheck* gate) {
+  if (gate && agg_ok(gate)) return;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d; i += stride) {
     const ulonglong2 p = reinterpret_cast<const ulonglong2*>(pairs)[i];
@@ -322,9 +386,64 @@ __global__ void k_deinterleave(const unsigned long long* __restrict__ pairs, uin
   }
 }
 
-template <int MW>
+// Packed mode: counts/sums from the hot pairs (ids < hot) and the packed
+// accumulators (ids >= hot), plus the decoded totals for the exactness check.
+__global__ void __launch_bounds__(256)
+    k_agg_decode(const unsigned long long* __restrict__ hotpairs,
+                 const unsigned long long* __restrict__ acc, uint32_t hot, uint32_t d,
+                 unsigned long long* __restrict__ counts, unsigned long long* __restrict__ sums,
+                 AggCheck* chk) {
+  unsigned long long lr = 0, ls = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d; i += stride) {
+    unsigned long long c, sm;
+    if (i < hot) {
+      const ulonglong2 p = reinterpret_cast<const ulonglong2*>(hotpairs)[i];
+      c = p.x;
+      sm = p.y;
+    } else {
+      const unsigned long long x = __ldcs(acc + i);
+      c = x >> 40;
+      sm = x & kPackMask;
+      lr += c;
+      ls += sm;
+    }
+    if (counts) __stcs(counts + i, c);
+    if (sums) __stcs(sums + i, sm);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lr += __shfl_down_sync(0xffffffffu, lr, o);
+    ls += __shfl_down_sync(0xffffffffu, ls, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (lr) atomicAdd(&chk->dec_rows, lr);
+    if (ls) atomicAdd(&chk->dec_sum, ls);
+  }
+}
+
+// Exact fallback, step 1: clear the pair accumulators unless the check passed.
+__global__ void __launch_bounds__(256)
+    k_agg_zero_if_failed(ulonglong2* __restrict__ pairs, uint64_t n2, const AggCheck* gate) {
+  if (agg_ok(gate)) return;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride)
+    pairs[i] = make_ulonglong2(0ull, 0ull);
+}
+
+uint32_t hot_keys(const skx_ctx* ctx, int mw, uint32_t hot_req, uint32_t limit) {
+  const size_t per_key = mw ? 12 : 4;
+  const size_t budget = ctx->smem_optin > 2048 ? ctx->smem_optin - 2048 : 0;
+  uint32_t hot = (uint32_t)(budget / per_key);
+  if (hot_req && hot_req < hot) hot = hot_req;
+  if (hot > limit) hot = limit;
+  return hot;
+}
+
+template <int MW, bool PACK>
 int aggregate_impl(skx_ctx* ctx, const uint32_t* fact, const void* measure, uint64_t n, uint32_t d,
-                   uint32_t limit, uint32_t hot_req, Tail t, cudaStream_t s) {
+                   uint32_t limit, uint32_t hot_req, Tail t, cudaStream_t s,
+                   const AggCheck* gate = nullptr) {
   const uintptr_t fa = reinterpret_cast<uintptr_t>(fact);
   if (fa % 4 != 0) return set_error(ctx, SKX_INVALID_ARGUMENT, "fact pointer not 4-byte aligned");
   uint64_t head = ((16 - fa % 16) % 16) / 4;
@@ -336,16 +455,12 @@ int aggregate_impl(skx_ctx* ctx, const uint32_t* fact, const void* measure, uint
   // Per-CTA counts must fit the u32 bins.
   if (n / grid + 4 * (uint64_t)kThreads >= (uint64_t(1) << 32))
     return set_error(ctx, SKX_INVALID_ARGUMENT, "aggregate: too many rows per call");
-  const size_t per_key = MW ? 12 : 4;
-  const size_t budget = ctx->smem_optin > 2048 ? ctx->smem_optin - 2048 : 0;
-  uint32_t hot = (uint32_t)(budget / per_key);
-  if (hot_req && hot_req < hot) hot = hot_req;
-  if (hot > limit) hot = limit;
-  const size_t smem = (size_t)hot * per_key;
+  const uint32_t hot = hot_keys(ctx, MW, hot_req, limit);
+  const size_t smem = (size_t)hot * (MW ? 12 : 4);
   // Stage the cold tail when its pairs overflow half of L2 (MW != 0 only).
   const uint64_t tail_keys = limit > hot ? limit - hot : 0;
-  if (MW && limit == d && ctx->agg_staged && tail_keys * 16 > ctx->l2_bytes / 2 &&
-      n >= (uint64_t(1) << 20)) {
+  if (MW && !PACK && !gate && limit == d && ctx->agg_mode == 1 &&
+      tail_keys * 16 > ctx->l2_bytes / 2 && n >= (uint64_t(1) << 20)) {
     uint32_t wshift = 20;  // 1M keys x 16 B = 16 MiB of pairs per bucket
     while (((tail_keys + (uint64_t(1) << wshift) - 1) >> wshift) > (uint64_t)kMaxBuckets) ++wshift;
     t.nb = (uint32_t)((tail_keys + (uint64_t(1) << wshift) - 1) >> wshift);
@@ -365,9 +480,10 @@ int aggregate_impl(skx_ctx* ctx, const uint32_t* fact, const void* measure, uint
     k_agg_fold<<<grid_for(ctx, n, 512, 4), 512, 0, s>>>(t);
     ctx->launches += 2;
   } else {
-    cudaFuncSetAttribute(k_aggregate<MW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_aggregate<MW><<<grid, kThreads, smem, s>>>(fact, measure, head, nvec, n, d, limit, hot, mvec,
-                                                 t, ctx->err);
+    cudaFuncSetAttribute(k_aggregate<MW, PACK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    k_aggregate<MW, PACK><<<grid, kThreads, smem, s>>>(fact, measure, head, nvec, n, d, limit, hot,
+                                                       mvec, t, ctx->err, gate);
     ctx->launches++;
   }
   SKX_CHECK_LAUNCH(ctx, "aggregate");
@@ -377,7 +493,8 @@ int aggregate_impl(skx_ctx* ctx, const uint32_t* fact, const void* measure, uint
 }  // namespace
 
 int launch_aggregate(skx_ctx* ctx, const uint32_t* fact, const void* measure, int mw, uint64_t n,
-                     uint32_t d, uint32_t hot, uint64_t* counts, uint64_t* sums, cudaStream_t s) {
+                     uint32_t d, uint32_t hot_req, uint64_t* counts, uint64_t* sums,
+                     cudaStream_t s) {
   if (mw != 0 && mw != 4 && mw != 8)
     return set_error(ctx, SKX_INVALID_ARGUMENT, "aggregate: measure width must be 0, 4 or 8");
   if (mw && !measure && n) return set_error(ctx, SKX_INVALID_ARGUMENT, "aggregate: null measure");
@@ -391,25 +508,57 @@ int launch_aggregate(skx_ctx* ctx, const uint32_t* fact, const void* measure, in
     if (sums && e == cudaSuccess) e = cudaMemsetAsync(sums, 0, (size_t)d * 8, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "aggregate memset");
     if (n == 0) return SKX_OK;
-    Tail t{reinterpret_cast<unsigned long long*>(counts), nullptr, nullptr, nullptr, 0, 0, 0};
-    return aggregate_impl<0>(ctx, fact, nullptr, n, d, d, hot, t, s);
+    Tail t{reinterpret_cast<unsigned long long*>(counts), nullptr, nullptr, nullptr, nullptr,
+           nullptr, 0, 0, 0};
+    return aggregate_impl<0, false>(ctx, fact, nullptr, n, d, d, hot_req, t, s);
   }
-  unsigned long long* pairs =
-      static_cast<unsigned long long*>(scratch(ctx, 1, (size_t)d * 16 + 16));
-  if (!pairs) return set_error(ctx, SKX_CUDA_ERROR, "aggregate: out of device memory");
+  const bool pack = ctx->agg_mode == 0 && n > 0;
+  const uint32_t hot = hot_keys(ctx, mw, hot_req, d);
+  // Slot-1 layout: [AggCheck 256 B][hot pairs hot x 16 B][acc d x 8 B][pairs d x 16 B]
+  auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t chk_b = 256, hp_b = up((size_t)hot * 16), acc_b = up((size_t)d * 8);
+  const size_t pairs_off = pack ? chk_b + hp_b + acc_b : 0;
+  char* base = static_cast<char*>(scratch(ctx, 1, pairs_off + (size_t)d * 16 + 16));
+  if (!base) return set_error(ctx, SKX_CUDA_ERROR, "aggregate: out of device memory");
+  unsigned long long* pairs = reinterpret_cast<unsigned long long*>(base + pairs_off);
+  unsigned long long* counts64 = reinterpret_cast<unsigned long long*>(counts);
+  unsigned long long* sums64 = reinterpret_cast<unsigned long long*>(sums);
+  if (pack) {
+    AggCheck* chk = reinterpret_cast<AggCheck*>(base);
+    unsigned long long* hotpairs = reinterpret_cast<unsigned long long*>(base + chk_b);
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(base + chk_b + hp_b);
+    cudaError_t e = cudaMemsetAsync(base, 0, pairs_off, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "aggregate memset");
+    Tail tp{hotpairs, acc, chk, nullptr, nullptr, nullptr, 0, 0, 0};
+    int rc = mw == 8 ? aggregate_impl<8, true>(ctx, fact, measure, n, d, d, hot_req, tp, s)
+                     : aggregate_impl<4, true>(ctx, fact, measure, n, d, d, hot_req, tp, s);
+    if (rc) return rc;
+    k_agg_decode<<<grid_for(ctx, d, 256, 8), 256, 0, s>>>(hotpairs, acc, hot, d, counts64,
+                                                         sums64, chk);
+    // Exact fallback, queued now and skipped on the device when the check passed.
+    k_agg_zero_if_failed<<<grid_for(ctx, d, 256, 8), 256, 0, s>>>(
+        reinterpret_cast<ulonglong2*>(pairs), d, chk);
+    ctx->launches += 2;
+    Tail t{pairs, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, 0};
+    rc = mw == 8 ? aggregate_impl<8, false>(ctx, fact, measure, n, d, d, hot_req, t, s, chk)
+                 : aggregate_impl<4, false>(ctx, fact, measure, n, d, d, hot_req, t, s, chk);
+    if (rc) return rc;
+    k_deinterleave<<<grid_for(ctx, d, 256, 8), 256, 0, s>>>(pairs, d, counts64, sums64, chk);
+    ctx->launches++;
+    SKX_CHECK_LAUNCH(ctx, "aggregate decode");
+    return SKX_OK;
+  }
   cudaError_t e = cudaMemsetAsync(pairs, 0, (size_t)d * 16, s);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "aggregate memset");
-  Tail t{pairs, nullptr, nullptr, nullptr, 0, 0, 0};
+  Tail t{pairs, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, 0};
   int rc = SKX_OK;
   if (n > 0) {
-    rc = mw == 8 ? aggregate_impl<8>(ctx, fact, measure, n, d, d, hot, t, s)
-                 : aggregate_impl<4>(ctx, fact, measure, n, d, d, hot, t, s);
+    rc = mw == 8 ? aggregate_impl<8, false>(ctx, fact, measure, n, d, d, hot_req, t, s)
+                 : aggregate_impl<4, false>(ctx, fact, measure, n, d, d, hot_req, t, s);
     if (rc) return rc;
   }
   if (d > 0) {
-    k_deinterleave<<<grid_for(ctx, d, 256, 8), 256, 0, s>>>(
-        pairs, d, reinterpret_cast<unsigned long long*>(counts),
-        reinterpret_cast<unsigned long long*>(sums));
+    k_deinterleave<<<grid_for(ctx, d, 256, 8), 256, 0, s>>>(pairs, d, counts64, sums64, nullptr);
     ctx->launches++;
   }
   SKX_CHECK_LAUNCH(ctx, "aggregate deinterleave");
@@ -440,8 +589,9 @@ int skx_heavy_hitter_count(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint3
     if (e != cudaSuccess) return skx::cuda_fail(ctx, e, "heavy_hitter memset");
   }
   if (n == 0) return SKX_OK;
-  skx::Tail t{reinterpret_cast<unsigned long long*>(counts), nullptr, nullptr, nullptr, 0, 0, 0};
-  return skx::aggregate_impl<0>(ctx, fact, nullptr, n, d, cutoff, cutoff, t, s);
+  skx::Tail t{reinterpret_cast<unsigned long long*>(counts), nullptr, nullptr, nullptr, nullptr,
+              nullptr, 0, 0, 0};
+  return skx::aggregate_impl<0, false>(ctx, fact, nullptr, n, d, cutoff, cutoff, t, s);
 }
 
 }  // extern "C"

@@ -155,9 +155,9 @@ int skx_set_histogram_mode(skx_ctx* ctx, int bucketed) {
   return SKX_OK;
 }
 
-int skx_set_aggregate_mode(skx_ctx* ctx, int staged) {
-  if (!ctx || staged < 0 || staged > 1) return SKX_INVALID_ARGUMENT;
-  ctx->agg_staged = staged != 0;
+int skx_set_aggregate_mode(skx_ctx* ctx, int mode) {
+  if (!ctx || mode < 0 || mode > 2) return SKX_INVALID_ARGUMENT;
+  ctx->agg_mode = mode;
   return SKX_OK;
 }
 

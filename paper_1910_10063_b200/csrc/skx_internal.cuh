@@ -55,6 +55,14 @@ __device__ __forceinline__ uint4 ld_stream_v4(const void* ptr, uint64_t pol) {
                : "l"(ptr), "l"(pol));
   return r;
 }
+// Streaming loads with the .cs cache operator (evict-first in L1 and L2).
+__device__ __forceinline__ uint4 ld_cs_v4(const void* ptr) {
+  uint4 r;
+  asm volatile("ld.global.cs.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(ptr));
+  return r;
+}
 __device__ __forceinline__ uint32_t ld_stream_u32(const void* ptr, uint64_t pol) {
   uint32_t r;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
@@ -146,7 +154,7 @@ struct skx_ctx {
   size_t tier_l1_bytes = 160 * 1024;  // gather tier t1 (bytes of the dimension prefix)
   double tier_l2_frac = 0.6;          // gather tier t2 (share of L2)
   bool hist_bucketed = false;         // histogram cold keys via key-range buckets
-  bool agg_staged = false;            // group-by cold tail staged per key range (measured slower at s>=1)
+  int agg_mode = 0;  // group-by cold tail: 0 packed + exact fallback, 1 staged, 2 direct pairs
   std::atomic<uint64_t> launches{0};
   skx_error_info last{};
   // scratch arenas (grow-only)

@@ -315,19 +315,57 @@ def test_histogram_bucketed_large_domain(sx, oracle, case, bucketed):
     assert np.array_equal(np_(idx.offsets), off) and np.array_equal(np_(idx.ranks), rk)
 
 
-@pytest.mark.parametrize("staged", [0, 1])
+@pytest.mark.parametrize("mode", [0, 1, 2])
 @pytest.mark.parametrize("z", [0.0, 0.8])
-def test_aggregate_large_domain_modes(sx, oracle, staged, z):
-    """Tail pairs larger than half of L2: direct reductions (default) and the
-    staged per-bucket path (uniform data overflows the buckets -> fallback)."""
+def test_aggregate_large_domain_modes(sx, oracle, mode, z):
+    """Tail pairs larger than half of L2: packed tail (default), the staged
+    per-bucket path (uniform data overflows the buckets -> fallback) and the
+    direct pair reductions."""
     d, n = 1 << 23, (1 << 22) + 3
     fact = sx.generate_zipf(cu(sx.zipf_cdf(d, z)), n, 21)  # rank space
     meas = np.random.default_rng(9).integers(1, 101, size=n, dtype=np.int64)
     ctx = sx.context(0)
-    ctx.check(ctx.lib.skx_set_aggregate_mode(ctx.handle, staged))
+    ctx.check(ctx.lib.skx_set_aggregate_mode(ctx.handle, mode))
     try:
         c, s = sx.aggregate_count_sum(fact, cu(meas), d)
     finally:
         ctx.check(ctx.lib.skx_set_aggregate_mode(ctx.handle, 0))
     ce, se = oracle.aggregate_count_sum(np_(fact), meas.view(np.uint64), d)
     assert np.array_equal(np_(c), ce) and np.array_equal(np_(s), se)
+
+
+@pytest.mark.parametrize("case", ["big_measure", "count_wrap", "sum_carry", "mixed"])
+def test_aggregate_packed_tail_fallback(sx, oracle, case):
+    """The packed tail (count << 40 | sum) must detect every overflow on the
+    device and redo the call exactly: measures >= 2^16, a cold key with
+    >= 2^24 rows (count field wraps), a cold key whose sum reaches 2^40."""
+    d, hot = 1000, 16
+    rng = np.random.default_rng(5)
+    if case == "big_measure":
+        n = 100_003
+        fact = rng.integers(1, d + 1, size=n, dtype=np.uint32)
+        meas = rng.integers(0, 2**63, size=n, dtype=np.int64)
+    elif case == "count_wrap":
+        n = (1 << 24) + 77
+        fact = np.full(n, 500, np.uint32)
+        fact[::3] = rng.integers(1, d + 1, size=len(fact[::3]), dtype=np.uint32)
+        fact[: (1 << 24) + 5] = 500
+        meas = np.ones(n, np.int64)
+    elif case == "sum_carry":
+        n = (1 << 25) + 2
+        fact = np.full(n, 700, np.uint32)
+        meas = np.full(n, 65535, np.int64)
+    else:
+        n = 1 << 20
+        fact = rng.integers(1, d + 1, size=n, dtype=np.uint32)
+        meas = rng.integers(1, 101, size=n, dtype=np.int64)
+        meas[12345] = 1 << 40  # one cold row that cannot be packed
+    c, s = sx.aggregate_count_sum(cu(fact), cu(meas), d, hot_threshold=hot)
+    ce, se = oracle.aggregate_count_sum(fact, meas.view(np.uint64), d)
+    assert np.array_equal(np_(c), ce) and np.array_equal(np_(s), se)
+    # u32 measure (the reference's own Column type) through the same path
+    if case in ("count_wrap", "mixed"):
+        m32 = meas.astype(np.uint32)
+        c, s = sx.aggregate_count_sum(cu(fact), cu(m32), d, hot_threshold=hot)
+        ce, se = oracle.aggregate_count_sum(fact, m32, d)
+        assert np.array_equal(np_(c), ce) and np.array_equal(np_(s), se)

@@ -15,7 +15,7 @@ p.add_argument("--z", default="1.0")
 p.add_argument("--hot", default="0")
 p.add_argument("--rows", type=int, default=1 << 30)
 p.add_argument("--domain", type=int, default=1 << 24)
-p.add_argument("--modes", default="1,0", help="skx_set_aggregate_mode values")
+p.add_argument("--modes", default="0,2", help="skx_set_aggregate_mode values")
 a = p.parse_args()
 ctx = sx.context(0)
 for z in [float(x) for x in a.z.split(",")]:
@@ -43,7 +43,7 @@ for z in [float(x) for x in a.z.split(",")]:
             if ref is None:
                 ref = c.clone()
             bytes_ = a.rows * (12 if mode == "count_sum" else 4) + a.domain * (16 if mode == "count_sum" else 8)
-            print(json.dumps({"z": z, "hot": hot, "staged": amode, "mode": mode, "ms": round(ms, 3),
+            print(json.dumps({"z": z, "hot": hot, "agg_mode": amode, "mode": mode, "ms": round(ms, 3),
                               "rows_per_s": a.rows / (ms * 1e-3),
                               "frac": round(bytes_ / (ms * 1e-3) / 6545.3e9, 4),
                               "counts_equal": bool(torch.equal(c, ref))}), flush=True)
