@@ -1,6 +1,6 @@
 // select.cu -- Q2 selection (K8 in SURVEY.md §2.1): bitmap probe plus
 // order-preserving compaction, optionally fused with the config-5 four-column
-// gather and per-category fp64 SUM(price); plus the bitmap helpers.
+// gather and per-category SUM(price); plus the bitmap helpers.
 //
 // Reference: KernelTable::select_offsets (proj/src/kernels/scalar.cpp:31-42,
 // avx2.cpp:59-98), select (operators.cpp:87-98), parallel_select
@@ -8,29 +8,44 @@
 // permute_bitmap (operators.cpp:21-30), build_bitmap (operators.hpp:38-45).
 //
 // B200 design: two streaming passes over the
-// FK column with a device scan between them -- pass 1 probes every row once,
-// writes a 1-bit/row selection mask and counts each 4096-row tile's selected
-// rows; the scan turns the counts into tile offsets; pass 2 reads the mask
-// and the FKs, compacts the tile's selected rows in shared memory and writes
-// each at tile offset + rank in tile: ascending row order, exactly the
-// reference's chunk-ordered concatenation.  (A single-pass decoupled
-// look-back version was measured ~2x slower on B200: CTAs stall behind the
-// look-back chain, profiles/r1_experiments.md.)  The C5 variant gathers
-// category / price / supplier / flag for the selected rows in pass 2, and a
-// third pass sums price per category over the compacted columns in
-// warp-private fp64 shared bins: lanes of one category are pre-summed with
-// __match_any_sync + shuffles, because shared fp64 atomics compile to CAS
-// spin loops on sm_100a.  Bins are flushed once per CTA.
+// FK column with a device scan between them.  Pass 1 probes every row once
+// (128-bit FK loads, 4 rows per lane; the bitmap prefix that holds the hot
+// ids of a reordered column sits in shared memory), writes a 1-bit/row
+// selection mask and counts each 4096-row tile's selected rows; the scan
+// turns the counts into tile offsets; pass 2 reads the mask and the FKs,
+// compacts the tile's selected rows in shared memory and writes each at tile
+// offset + rank in tile: ascending row order, exactly the reference's
+// chunk-ordered concatenation.  (A single-pass decoupled look-back version
+// was measured ~2x slower on B200, profiles/r1_experiments.md.)
+//
+// The C5 variant first interleaves the four dimension columns into 32-byte
+// records (one 256-bit load and one sector per selected row instead of four
+// separate lines -- an L2 miss costs a whole 128-byte line on B200) and sums
+// price per category inside pass 2 in exact 96-bit fixed point: per-CTA
+// shared bins updated with native 32-bit atomics (carries via the returned
+// old value), folded once per CTA, converted to fp64 at the end.  The scale
+// 2^S comes from the price column's exponent range (|price * 2^S| < 2^62);
+// non-finite prices, an exponent span above 2^30 or more than 4096
+// categories switch, on the device, to the fp64 pass over the compacted
+// columns (warp-private fp64 bins, __match_any_sync pre-sums).
 #include "scan.cuh"
 
 namespace skx {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kItems = 16;
-constexpr int kTile = kThreads * kItems;  // 4096 rows
+constexpr int kThreads = 256;                  // pass 2: one 4096-row tile per CTA iteration
 constexpr int kWarps = kThreads / 32;
-constexpr uint32_t kSmemCategories = 2048;  // per-warp fp64 bins: 8 x 2048 x 8 B = 128 KB
+constexpr int kTile = 4096;
+constexpr int kWarpRows = kTile / kWarps;      // 512 rows per warp
+constexpr int kItems = kWarpRows / 128;        // 4 items of 128 rows (4 per lane)
+constexpr int kThreads1 = 1024;                // pass 1: four tiles per CTA iteration
+constexpr int kSub = kThreads1 / kThreads;
+constexpr uint32_t kSmemCategories = 2048;     // fp64 fallback: 8 warps x 2048 x 8 B
+constexpr uint32_t kFixedCategories = 4096;    // fixed point: 3 x 4096 x 4 B per CTA
+constexpr int kRangeLimit = 30;                // max exponent span for fixed point
+#ifndef SKX_SEL_SMEM_KB
+#define SKX_SEL_SMEM_KB 128
+#endif
 
 struct Cols {
   const int32_t* cat;
@@ -43,165 +58,279 @@ struct Cols {
   uint16_t* out_flag;
   double* sums;
   uint32_t n_categories;
+  const uint4* rec;          // [d][2]: {cat, price, supp lo, supp hi}, {flag, 0, 0, 0}
+  struct SumCtl* ctl;
+  unsigned int* acc96;       // [n_categories][4]: lo, mid, hi, pad
 };
 
-// Probe one warp-striped item: row = tile*4096 + w*512 + i*32 + lane.  The
-// first `sw` bitmap words live in shared memory: on a skew-reordered column
-// the hot ids -- most probes -- fall in that prefix.
-__device__ __forceinline__ bool probe(const uint32_t* __restrict__ fact, uint64_t k, uint64_t n,
-                                      const unsigned long long* __restrict__ words, uint64_t bits,
-                                      const unsigned long long* s_words, uint32_t sw, uint64_t pol,
-                                      bool check, DevErr* err, uint32_t& idx) {
-  idx = 0;
-  if (k >= n) return false;
-  const uint32_t id = ld_stream_u32(fact + k, pol);
-  idx = id - 1u;
-  if (idx < bits) {
-    const uint32_t wi = idx >> 6;
-    const unsigned long long wv = wi < sw ? s_words[wi] : __ldg(words + wi);
-    return (wv >> (idx & 63)) & 1ull;
-  }
-  if (check) record_violation(err, k, id);
-  return false;
+// Price exponent range for the fixed-point sums (frexp exponent + 1024).
+struct SumCtl {
+  unsigned int emax_b;    // max over finite nonzero |price|; 0 = none
+  unsigned int emin_neg;  // max of 2048 - e_b (i.e. 2048 - min e_b); 0 = none
+  unsigned int nonfinite;
+  unsigned int pad;
+};
+
+__device__ __forceinline__ bool fixed_ok(const SumCtl* c, uint32_t ncat, int& S) {
+  S = 0;
+  if (c->nonfinite || ncat == 0 || ncat > kFixedCategories) return false;
+  if (c->emax_b == 0) return true;  // every price is zero
+  const int emax = (int)c->emax_b - 1024;
+  const int emin = (int)(2048u - c->emin_neg) - 1024;
+  if (emax - emin > kRangeLimit) return false;
+  S = 62 - emax;  // |price| < 2^emax  =>  |price * 2^S| < 2^62
+  return true;
 }
 
-// Pass 1: probe every row once, store the selection as one 32-bit mask word
-// per warp-item (1 bit per row, coalesced), count selected rows per tile
-// (grid-stride over tiles) and check the domain.
-__global__ void __launch_bounds__(kThreads)
+// C5 prologue: interleave the four dimension columns into 32-byte records
+// and record the price exponent range.
+__global__ void __launch_bounds__(256)
+    k_pack_records(const int32_t* __restrict__ cat, const float* __restrict__ price,
+                   const unsigned long long* __restrict__ supp, const uint16_t* __restrict__ flag,
+                   uint32_t d, uint4* __restrict__ rec, SumCtl* ctl) {
+  unsigned int emax = 0, eneg = 0, nf = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d; i += stride) {
+    const float p = __ldcs(price + i);
+    const unsigned long long sp = __ldcs(supp + i);
+    rec[2 * i] = make_uint4((uint32_t)__ldcs(cat + i), __float_as_uint(p), (uint32_t)sp,
+                            (uint32_t)(sp >> 32));
+    rec[2 * i + 1] = make_uint4((uint32_t)__ldcs(reinterpret_cast<const unsigned short*>(flag) + i),
+                                0u, 0u, 0u);
+    if (!isfinite(p)) {
+      nf = 1;
+    } else if (p != 0.f) {
+      int e;
+      frexpf(p, &e);
+      const unsigned int eb = (unsigned int)(e + 1024);
+      emax = max(emax, eb);
+      eneg = max(eneg, 2048u - eb);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+    eneg = max(eneg, __shfl_xor_sync(0xffffffffu, eneg, o));
+    nf |= __shfl_xor_sync(0xffffffffu, nf, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (emax) atomicMax(&ctl->emax_b, emax);
+    if (eneg) atomicMax(&ctl->emin_neg, eneg);
+    if (nf) atomicOr(&ctl->nonfinite, 1u);
+  }
+}
+
+// 96-bit two's-complement add of v into {lo, mid, hi}[c] (shared or global):
+// the carry out of each word is decided from the value the atomic returned.
+__device__ __forceinline__ void add96(unsigned int* lo, unsigned int* mid, unsigned int* hi,
+                                      long long v) {
+  const unsigned int vl = (unsigned int)v;
+  const unsigned int old = atomicAdd(lo, vl);
+  const long long up = (v >> 32) + ((unsigned int)(old + vl) < old ? 1 : 0);
+  if (up) {
+    const unsigned int um = (unsigned int)up, uh = (unsigned int)((unsigned long long)up >> 32);
+    const unsigned int old2 = atomicAdd(mid, um);
+    const unsigned int h = uh + ((unsigned int)(old2 + um) < old2 ? 1u : 0u);
+    if (h) atomicAdd(hi, h);
+  }
+}
+
+// Pass 1: probe every row once, store the selection as 1 bit per row (per
+// warp: 16 words, word 4i+j bit L = row 128i + 4L + j of the warp's 512),
+// count selected rows per tile and check the domain.
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads1, 1)
     k_select_count(const uint32_t* __restrict__ fact, uint64_t n,
-                   const unsigned long long* __restrict__ words, uint64_t bits,
+                   const uint32_t* __restrict__ words32, uint64_t bits,
                    uint32_t* __restrict__ mask, uint32_t* __restrict__ tile_counts, uint32_t sw,
                    DevErr* err) {
-  extern __shared__ __align__(16) unsigned long long s_words[];  // bitmap prefix [sw]
-  __shared__ uint32_t s_w[kWarps];
+  extern __shared__ __align__(16) uint32_t s_words[];  // bitmap prefix [sw]
+  __shared__ uint32_t s_w[kThreads1 / 32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int sub = w / kWarps, ws = w % kWarps;
   const uint64_t ntiles = (n + kTile - 1) / kTile;
-  const uint64_t pol = policy_evict_first();
-  for (uint32_t i = threadIdx.x; i < sw; i += kThreads) s_words[i] = __ldg(words + i);
+  for (uint32_t i = threadIdx.x; i < sw; i += kThreads1) s_words[i] = __ldg(words32 + i);
   __syncthreads();
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint64_t row0 = tile * kTile + (uint64_t)w * (kItems * 32);
-    // All 16 FK loads first, then all 16 bitmap probes, then the ballots: two
-    // round trips per tile instead of sixteen dependent ones.
-    uint32_t fk[kItems];
+  for (uint64_t t0 = (uint64_t)blockIdx.x * kSub; t0 < ntiles; t0 += (uint64_t)gridDim.x * kSub) {
+    const uint64_t tile = t0 + sub;
+    const uint64_t wrow0 = tile * kTile + (uint64_t)ws * kWarpRows;
+    const bool full = wrow0 + kWarpRows <= n;  // warp-uniform
+    uint32_t fk[kItems][4];
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
-      const uint64_t k = row0 + i * 32 + lane;
-      fk[i] = k < n ? ld_stream_u32(fact + k, pol) : 1u;
-    }
-    bool sel[kItems];
+      const uint64_t r = wrow0 + (uint64_t)i * 128 + 4 * lane;
+      if (VEC && full) {
+        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(fact + r));
+        fk[i][0] = v.x, fk[i][1] = v.y, fk[i][2] = v.z, fk[i][3] = v.w;
+      } else {
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-      const uint64_t k = row0 + i * 32 + lane;
-      const uint32_t idx = fk[i] - 1u;
-      sel[i] = false;
-      if (k < n) {
-        if (idx < bits) {
-          const uint32_t wi = idx >> 6;
-          const unsigned long long wv = wi < sw ? s_words[wi] : __ldg(words + wi);
-          sel[i] = (wv >> (idx & 63)) & 1ull;
-        } else {
-          record_violation(err, k, fk[i]);
-        }
+        for (int j = 0; j < 4; ++j) fk[i][j] = r + j < n ? __ldcs(fact + r + j) : 1u;
       }
     }
     uint32_t c = 0, mine = 0;
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
-      const uint32_t b = __ballot_sync(0xffffffffu, sel[i]);
-      c += __popc(b);
-      if (lane == i) mine = b;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t k = wrow0 + (uint64_t)i * 128 + 4 * lane + j;
+        const uint32_t idx = fk[i][j] - 1u;
+        bool sel = false;
+        if (full || k < n) {
+          if (idx < bits) {
+            const uint32_t wi = idx >> 5;
+            const uint32_t wv = wi < sw ? s_words[wi] : __ldg(words32 + wi);
+            sel = (wv >> (idx & 31)) & 1u;
+          } else {
+            record_violation(err, k, fk[i][j]);
+          }
+        }
+        const uint32_t b = __ballot_sync(0xffffffffu, sel);
+        c += __popc(b);
+        if (lane == i * 4 + j) mine = b;
+      }
     }
-    if (lane < kItems) mask[(row0 >> 5) + lane] = mine;  // 16 consecutive words per warp
+    if (tile < ntiles && lane < kItems * 4) mask[(wrow0 >> 5) + lane] = mine;
     if (lane == 0) s_w[w] = c;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < kSub && t0 + threadIdx.x < ntiles) {
       uint32_t t = 0;
-      for (int i = 0; i < kWarps; ++i) t += s_w[i];
-      tile_counts[tile] = t;
+      for (int i = 0; i < kWarps; ++i) t += s_w[threadIdx.x * kWarps + i];
+      tile_counts[t0 + threadIdx.x] = t;
     }
     __syncthreads();
   }
 }
 
-// Pass 2, per tile: (A) read the mask words, load the FK of selected rows
-// and compact (dimension index, row in tile) into shared memory in row order;
-// (B) process the compacted rows densely -- consecutive threads take
+// Pass 2, per tile: (A) decode the mask, load the FKs (128-bit, all rows:
+// at ~10% selectivity nearly every sector holds a selected row) and compact
+// (dimension index, row in tile) into shared memory in row order; (B)
+// process the compacted rows densely -- consecutive threads take
 // consecutive selected rows, so the gathers are independent and the output
-// stores coalesce.  FUSED adds the 4-column gather and per-category sums.
-template <bool FUSED>
+// stores coalesce.  FUSED adds the record gather and the per-category sums.
+template <bool FUSED, bool VEC>
 __global__ void __launch_bounds__(kThreads)
     k_select_write(const uint32_t* __restrict__ fact, uint64_t n, const uint32_t* __restrict__ mask,
                    uint32_t base_off, const uint32_t* __restrict__ tile_off,
                    const uint32_t* __restrict__ total, uint32_t* __restrict__ out_off, Cols cols,
                    unsigned long long* __restrict__ count_dev) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint32_t* s_idx = reinterpret_cast<uint32_t*>(smem_raw);             // [kTile]
-  uint16_t* s_row = reinterpret_cast<uint16_t*>(s_idx + kTile);        // [kTile]
+  uint32_t* s_idx = reinterpret_cast<uint32_t*>(smem_raw);       // [kTile]
+  uint16_t* s_row = reinterpret_cast<uint16_t*>(s_idx + kTile);  // [kTile]
+  unsigned int* s_acc = reinterpret_cast<unsigned int*>(s_row + kTile);  // [3][ncat] (fixed)
   __shared__ uint32_t s_w[kWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (blockIdx.x == 0 && threadIdx.x == 0) *count_dev = *total;
+  const uint32_t ncat = cols.n_categories;
+  int S = 0;
+  const bool fixed = FUSED && cols.sums && fixed_ok(cols.ctl, ncat, S);
+  if (fixed) {
+    for (uint32_t i = threadIdx.x; i < 3 * ncat; i += kThreads) s_acc[i] = 0u;
+  }
   const uint64_t ntiles = (n + kTile - 1) / kTile;
-  const uint64_t pol = policy_evict_first();
   const uint32_t lt = lanemask_lt();
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint64_t row0 = tile * kTile + (uint64_t)w * (kItems * 32);
-    // (A) this warp's 16 mask words (lane i holds word i) and, in the same
-    // round trip, all 512 of its FK values (coalesced; at ~10% selectivity
-    // the selected rows' sectors would be fetched anyway).
-    const uint32_t mw = lane < kItems ? __ldg(mask + (row0 >> 5) + lane) : 0u;
-    uint32_t fk[kItems];
+    const uint64_t wrow0 = tile * kTile + (uint64_t)w * kWarpRows;
+    const bool full = wrow0 + kWarpRows <= n;
+    const bool any = wrow0 < n;
+    const uint32_t mw = (any && lane < kItems * 4) ? __ldg(mask + (wrow0 >> 5) + lane) : 0u;
+    uint32_t fk[kItems][4];
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
-      const uint64_t k = row0 + i * 32 + lane;
-      fk[i] = k < n ? ld_stream_u32(fact + k, pol) : 0u;
+      const uint64_t r = wrow0 + (uint64_t)i * 128 + 4 * lane;
+      if (VEC && full) {
+        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(fact + r));
+        fk[i][0] = v.x, fk[i][1] = v.y, fk[i][2] = v.z, fk[i][3] = v.w;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) fk[i][j] = r + j < n ? __ldcs(fact + r + j) : 0u;
+      }
     }
     uint32_t c = 0;
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) c += __popc(__shfl_sync(0xffffffffu, mw, i));
+    for (int q = 0; q < kItems * 4; ++q) c += __popc(__shfl_sync(0xffffffffu, mw, q));
     if (lane == 0) s_w[w] = c;
     __syncthreads();
-    uint32_t lpos = 0;
-    for (int i = 0; i < w; ++i) lpos += s_w[i];
-    uint32_t cnt_tile = 0;
-    for (int i = 0; i < kWarps; ++i) cnt_tile += s_w[i];
+    uint32_t lpos = 0, cnt_tile = 0;
+    for (int i = 0; i < kWarps; ++i) {
+      lpos += i < w ? s_w[i] : 0u;
+      cnt_tile += s_w[i];
+    }
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
-      const uint32_t m = __shfl_sync(0xffffffffu, mw, i);
-      if ((m >> lane) & 1u) {
-        const uint32_t r = (uint32_t)(w * (kItems * 32) + i * 32 + lane);
-        const uint32_t j = lpos + __popc(m & lt);
-        s_idx[j] = fk[i] - 1u;
-        s_row[j] = (uint16_t)r;
+      uint32_t m[4], before = 0, cnt = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        m[j] = __shfl_sync(0xffffffffu, mw, i * 4 + j);
+        before += __popc(m[j] & lt);
+        cnt += __popc(m[j]);
       }
-      lpos += __popc(m);
+      uint32_t pos = lpos + before;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if ((m[j] >> lane) & 1u) {
+          s_idx[pos] = fk[i][j] - 1u;
+          s_row[pos] = (uint16_t)(w * kWarpRows + i * 128 + 4 * lane + j);
+          ++pos;
+        }
+      }
+      lpos += cnt;
     }
     __syncthreads();
     // (B) dense pass over the tile's selected rows
     const uint64_t obase = tile_off[tile];
     for (uint32_t j0 = 0; j0 < cnt_tile; j0 += kThreads) {
       const uint32_t j = j0 + threadIdx.x;
-      const bool live = j < cnt_tile;
-      int32_t ct = -1;
-      float pr = 0.f;
-      if (live) {
+      if (j < cnt_tile) {
         const uint64_t p = obase + j;
         out_off[p] = base_off + (uint32_t)(tile * kTile + s_row[j]);
         if (FUSED) {
-          const uint32_t idx = s_idx[j];
-          ct = __ldg(cols.cat + idx);
-          pr = __ldg(cols.price + idx);
-          const unsigned long long sp = __ldg(cols.supp + idx);
-          const unsigned short fl = __ldg(reinterpret_cast<const unsigned short*>(cols.flag) + idx);
+          const uint4* rp = cols.rec + 2 * (uint64_t)s_idx[j];
+          uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
+          asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3), "=r"(b0), "=r"(b1), "=r"(b2),
+                         "=r"(b3)
+                       : "l"(rp));
+          const int32_t ct = (int32_t)a0;
+          const float pr = __uint_as_float(a1);
           cols.out_cat[p] = ct;
           cols.out_price[p] = pr;
-          cols.out_supp[p] = sp;
-          cols.out_flag[p] = fl;
+          cols.out_supp[p] = (unsigned long long)a2 | ((unsigned long long)a3 << 32);
+          cols.out_flag[p] = (uint16_t)b0;
+          if (fixed && (uint32_t)ct < ncat) {
+            const long long v = __double2ll_rn(ldexp((double)pr, S));
+            add96(&s_acc[ct], &s_acc[ncat + ct], &s_acc[2 * ncat + ct], v);
+          }
         }
       }
     }
     __syncthreads();  // s_idx / s_row / s_w reused by the next tile
+  }
+  if (fixed) {
+    // s_acc was last touched before the loop's trailing barrier.
+    for (uint32_t c2 = threadIdx.x; c2 < ncat; c2 += kThreads) {
+      const unsigned int L = s_acc[c2], M = s_acc[ncat + c2], H = s_acc[2 * ncat + c2];
+      if ((L | M | H) == 0u) continue;
+      unsigned int* g = cols.acc96 + 4 * (uint64_t)c2;
+      const unsigned int old = atomicAdd(&g[0], L);
+      const unsigned int c1 = (unsigned int)(old + L) < old ? 1u : 0u;
+      const unsigned int m2 = M + c1;
+      unsigned int h = H + (m2 < M ? 1u : 0u);
+      const unsigned int old2 = atomicAdd(&g[1], m2);
+      h += (unsigned int)(old2 + m2) < old2 ? 1u : 0u;
+      if (h) atomicAdd(&g[2], h);
+    }
+  }
+}
+
+// C5 epilogue (fixed point): 96-bit sums -> fp64.  No-op on the fp64 path.
+__global__ void k_sum_finalize(const unsigned int* __restrict__ acc96, const SumCtl* ctl,
+                               uint32_t ncat, double* __restrict__ sums) {
+  int S = 0;
+  if (!fixed_ok(ctl, ncat, S)) return;
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < ncat; c += gridDim.x * blockDim.x) {
+    const unsigned int* g = acc96 + 4 * (uint64_t)c;
+    const long long hi64 = (long long)(((unsigned long long)g[2] << 32) | g[1]);  // bits 32..95
+    sums[c] = ldexp(ldexp((double)hi64, 32) + (double)g[0], -S);
   }
 }
 
@@ -213,7 +342,9 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void __launch_bounds__(kThreads)
     k_category_sum(const int32_t* __restrict__ cat, const float* __restrict__ price,
                    const uint32_t* __restrict__ total, uint32_t n_categories,
-                   double* __restrict__ sums) {
+                   double* __restrict__ sums, const SumCtl* ctl) {
+  int S_unused = 0;
+  if (fixed_ok(ctl, n_categories, S_unused)) return;  // summed in pass 2
   extern __shared__ double s_bins[];  // [kWarps][n_categories] when small
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const bool smem = n_categories <= kSmemCategories;
@@ -298,7 +429,8 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
   if (!count_dev) return set_error(ctx, SKX_INVALID_ARGUMENT, "select: null count pointer");
   ctx->last_domain = bits;
   cudaError_t e;
-  if (fused && cols.sums && cols.n_categories) {
+  const bool sums_on = fused && cols.sums && cols.n_categories;
+  if (sums_on) {
     e = cudaMemsetAsync(cols.sums, 0, (size_t)cols.n_categories * 8, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "select memset");
   }
@@ -307,53 +439,71 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
     return e == cudaSuccess ? SKX_OK : cuda_fail(ctx, e, "select memset");
   }
   const uint64_t ntiles = (n + kTile - 1) / kTile;
-  // scratch: mask words [ntiles * 128] | tile counts | tile offsets | total
-  uint32_t* sp = static_cast<uint32_t*>(scratch(ctx, 2, ntiles * (kTile / 32 + 2) * 4 + 256));
-  if (!sp) return set_error(ctx, SKX_CUDA_ERROR, "select: out of device memory");
+  // scratch: mask words [ntiles * 128] | tile counts | tile offsets | total |
+  //          (fused) SumCtl 256 B | acc96 [ncat][4] | records [d][32 B]
+  const uint64_t base_b = (ntiles * (kTile / 32 + 2) * 4 + 256 + 255) & ~uint64_t(255);
+  const uint64_t acc_b = fused ? (((uint64_t)cols.n_categories * 16 + 255) & ~uint64_t(255)) : 0;
+  const uint64_t rec_b = fused ? bits * 32 : 0;
+  char* raw = static_cast<char*>(scratch(ctx, 2, base_b + (fused ? 256 : 0) + acc_b + rec_b));
+  if (!raw) return set_error(ctx, SKX_CUDA_ERROR, "select: out of device memory");
+  uint32_t* sp = reinterpret_cast<uint32_t*>(raw);
   uint32_t* mask = sp;
   uint32_t* counts = sp + ntiles * (kTile / 32);
   uint32_t* offs = counts + ntiles;
   uint32_t* total = offs + ntiles;
-  const auto* wd = reinterpret_cast<const unsigned long long*>(words);
-  // Optional bitmap prefix staged per CTA in shared memory.  Off: measured on
-  // B200 at C5 (96 KB prefix, 2 CTAs/SM) 20.5 -> 38.2 ms -- the lost
-  // occupancy and L1 capacity cost more than the on-chip probes save.
-  const uint32_t sw = 0;
-  const size_t smem1 = (size_t)sw * 8;
-  cudaFuncSetAttribute(k_select_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
-  int per_sm1 = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm1, k_select_count, kThreads, smem1);
-  const unsigned grid1 = grid_for(ctx, ntiles, 1, per_sm1 < 1 ? 1 : per_sm1);
-  k_select_count<<<grid1, kThreads, smem1, s>>>(fact, n, wd, bits, mask, counts, sw, ctx->err);
+  if (fused) {
+    cols.ctl = reinterpret_cast<SumCtl*>(raw + base_b);
+    cols.acc96 = reinterpret_cast<unsigned int*>(raw + base_b + 256);
+    cols.rec = reinterpret_cast<const uint4*>(raw + base_b + 256 + acc_b);
+    e = cudaMemsetAsync(raw + base_b, 0, 256 + acc_b, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "select memset");
+    if (bits) {
+      k_pack_records<<<grid_for(ctx, bits, 256, 8), 256, 0, s>>>(
+          cols.cat, cols.price, cols.supp, cols.flag, (uint32_t)bits,
+          const_cast<uint4*>(cols.rec), cols.ctl);
+      ctx->launches++;
+    }
+  }
+  const bool vec = reinterpret_cast<uintptr_t>(fact) % 16 == 0;
+  // Pass 1 with the bitmap prefix staged per CTA in shared memory.
+  const uint64_t nw32 = (bits + 31) / 32;
+  size_t sbytes = (size_t)SKX_SEL_SMEM_KB * 1024;
+  if (sbytes > ctx->smem_optin - 1024) sbytes = ctx->smem_optin - 1024;
+  const uint32_t sw = (uint32_t)(nw32 < sbytes / 4 ? nw32 : sbytes / 4);
+  const size_t smem1 = (size_t)sw * 4;
+  auto k1 = vec ? k_select_count<true> : k_select_count<false>;
+  cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+  const uint64_t iters = (ntiles + kSub - 1) / kSub;
+  const unsigned grid1 = (unsigned)(iters < (uint64_t)ctx->num_sms ? iters : ctx->num_sms);
+  k1<<<grid1, kThreads1, smem1, s>>>(fact, n, reinterpret_cast<const uint32_t*>(words), bits, mask,
+                                     counts, sw, ctx->err);
   ctx->launches++;
   int rc = launch_exclusive_scan_u32(ctx, counts, offs, ntiles, total, 3, s);
   if (rc) return rc;
-  const size_t smem = (size_t)kTile * (4 + 2);
+  const size_t smem = (size_t)kTile * (4 + 2) +
+                      (sums_on && cols.n_categories <= kFixedCategories ? (size_t)cols.n_categories * 12 : 0);
+  auto k2 = fused ? (vec ? k_select_write<true, true> : k_select_write<true, false>)
+                  : (vec ? k_select_write<false, true> : k_select_write<false, false>);
+  cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
-  if (fused) {
-    cudaFuncSetAttribute(k_select_write<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_write<true>, kThreads, smem);
-    const unsigned grid2 = grid_for(ctx, ntiles, 1, per_sm < 1 ? 1 : per_sm);
-    k_select_write<true><<<grid2, kThreads, smem, s>>>(fact, n, mask, base, offs, total, out, cols,
-                                                      reinterpret_cast<unsigned long long*>(count_dev));
-    if (cols.n_categories) {
-      const size_t bsmem =
-          cols.n_categories <= kSmemCategories ? (size_t)kWarps * cols.n_categories * 8 : 0;
-      cudaFuncSetAttribute(k_category_sum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
-      int per_sm3 = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, k_category_sum, kThreads, bsmem);
-      k_category_sum<<<(unsigned)ctx->num_sms * (per_sm3 < 1 ? 1 : per_sm3), kThreads, bsmem, s>>>(
-          cols.out_cat, cols.out_price, total, cols.n_categories, cols.sums);
-      ctx->launches++;
-    }
-  } else {
-    cudaFuncSetAttribute(k_select_write<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_write<false>, kThreads, smem);
-    const unsigned grid2 = grid_for(ctx, ntiles, 1, per_sm < 1 ? 1 : per_sm);
-    k_select_write<false><<<grid2, kThreads, smem, s>>>(fact, n, mask, base, offs, total, out, cols,
-                                                       reinterpret_cast<unsigned long long*>(count_dev));
-  }
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2, kThreads, smem);
+  const unsigned grid2 = grid_for(ctx, ntiles, 1, per_sm < 1 ? 1 : per_sm);
+  k2<<<grid2, kThreads, smem, s>>>(fact, n, mask, base, offs, total, out, cols,
+                                   reinterpret_cast<unsigned long long*>(count_dev));
   ctx->launches++;
+  if (sums_on) {
+    k_sum_finalize<<<(cols.n_categories + 255) / 256, 256, 0, s>>>(cols.acc96, cols.ctl,
+                                                                   cols.n_categories, cols.sums);
+    // fp64 fallback over the compacted columns; exits at once on the fixed path.
+    const size_t bsmem =
+        cols.n_categories <= kSmemCategories ? (size_t)kWarps * cols.n_categories * 8 : 0;
+    cudaFuncSetAttribute(k_category_sum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
+    int per_sm3 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, k_category_sum, kThreads, bsmem);
+    k_category_sum<<<(unsigned)ctx->num_sms * (per_sm3 < 1 ? 1 : per_sm3), kThreads, bsmem, s>>>(
+        cols.out_cat, cols.out_price, total, cols.n_categories, cols.sums, cols.ctl);
+    ctx->launches += 2;
+  }
   SKX_CHECK_LAUNCH(ctx, "select");
   return SKX_OK;
 }
@@ -384,7 +534,7 @@ int skx_select_gather_sum(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const 
     return skx::set_error(ctx, SKX_INVALID_ARGUMENT, "select_gather_sum: null column pointer");
   skx::Cols cols{cat, price, reinterpret_cast<const unsigned long long*>(supp), flag,
                  out_cat, out_price, reinterpret_cast<unsigned long long*>(out_supp), out_flag,
-                 sums, n_categories};
+                 sums, n_categories, nullptr, nullptr, nullptr};
   return skx::select_impl(ctx, true, fact, n, words, d, base, out_off, cols, count_dev,
                           skx::as_stream(stream));
 }

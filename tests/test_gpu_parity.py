@@ -247,6 +247,42 @@ def test_select_gather_sum_vs_oracle(sx, oracle):
     assert np.array_equal(np_(sx.select(fact, bm)), oracle.select_offsets(np_(fact), np_(bm.words), d))
 
 
+@pytest.mark.parametrize("case", ["neg", "wide", "nan", "zero", "many_cats", "unaligned",
+                                  "ragged"])
+def test_select_gather_sum_paths(sx, oracle, case):
+    """Fixed-point category sums (default) and the on-device fp64 fallback
+    (non-finite price, exponent span > 2^30, > 4096 categories), signed
+    prices, unaligned and ragged FK columns."""
+    d = 1 << 14
+    n = (1 << 20) + (4093 if case == "ragged" else 0)
+    rng = np.random.default_rng(11)
+    ncat = 5000 if case == "many_cats" else 1000
+    cat = rng.integers(0, ncat, size=d, dtype=np.int32)
+    price = np.exp(3 + rng.standard_normal(d)).astype(np.float32)
+    if case == "neg":
+        price *= np.where(rng.random(d) < 0.5, -1, 1).astype(np.float32)
+    elif case == "wide":
+        price = np.exp2(rng.uniform(-20, 20, size=d)).astype(np.float32)
+    elif case == "nan":
+        price[np.flatnonzero(cat < 100)[3]] = np.nan
+    elif case == "zero":
+        price[:] = 0
+    supp = rng.integers(0, 2**63, size=d, dtype=np.uint64)
+    flag = rng.integers(0, 2**16, size=d, dtype=np.uint16)
+    fact = sx.generate_zipf(cu(sx.zipf_cdf(d, 1.0)), n + 1, 7)
+    fact = fact[1:] if case == "unaligned" else fact[:n]
+    thr = 700 if case == "many_cats" else 100
+    bm = sx.build_bitmap_lt(cu(cat), thr)
+    got = sx.select_gather_sum(fact, bm, cu(cat), cu(price), cu(supp), cu(flag), ncat, base=5)
+    exp = oracle.select_gather_sum(np_(fact), np_(bm.words), cat, price, supp, flag, ncat, base=5)
+    for g, e in zip(got[:5], exp[:5]):  # bit-exact (NaN payloads included)
+        assert np.array_equal(np_(g).view(np.uint8), np.ascontiguousarray(e).view(np.uint8))
+    s, se = np_(got[5]), exp[5]
+    assert np.allclose(s, se, rtol=1e-6, atol=0, equal_nan=True)
+    if case == "nan":
+        assert np.isnan(s).sum() == 1
+
+
 def test_reorder_invariants_at_scale(sx):
     """Size-independent properties at 2^26 rows: gather equality across
     layouts, rank-space counts map back through offsets, multiset of counts
