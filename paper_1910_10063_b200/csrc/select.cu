@@ -7,16 +7,19 @@
 // (parallel.cpp:102-129: per-thread results concatenated in chunk order),
 // permute_bitmap (operators.cpp:21-30), build_bitmap (operators.hpp:38-45).
 //
-// B200 design: two streaming passes over the
-// FK column with a device scan between them.  Pass 1 probes every row once
-// (128-bit FK loads, 4 rows per lane; the bitmap prefix that holds the hot
-// ids of a reordered column sits in shared memory), writes a 1-bit/row
-// selection mask and counts each 4096-row tile's selected rows; the scan
-// turns the counts into tile offsets; pass 2 reads the mask and the FKs,
-// compacts the tile's selected rows in shared memory and writes each at tile
-// offset + rank in tile: ascending row order, exactly the reference's
-// chunk-ordered concatenation.  (A single-pass decoupled look-back version
-// was measured ~2x slower on B200, profiles/r1_experiments.md.)
+// B200 design: two passes with a device scan
+// between them, no inter-CTA ordering inside a kernel.  Pass 1 streams the
+// FK column once (128-bit loads, 4 rows per lane; the bitmap prefix that
+// holds the hot ids of a reordered column sits in shared memory), and every
+// warp compacts the selected rows of its 512-row slice in row order into a
+// private slot of up to 128 (dimension index, row) entries plus a count.  The
+// scan turns the 2^k slice counts into output offsets.  Pass 2 walks the
+// slices: each warp copies its entries to offset + rank -- ascending row
+// order, exactly the reference's chunk-ordered concatenation -- so the FK
+// column is read once.  A slice with more than 128 selected rows (dense
+// selections) is re-derived in pass 2 from the FK column and the bitmap.
+// (A single-pass decoupled look-back version was measured ~2x slower on
+// B200, profiles/r1_experiments.md.)
 //
 // The C5 variant first interleaves the four dimension columns into 32-byte
 // records (one 256-bit load and one sector per selected row instead of four
@@ -26,20 +29,19 @@
 // old value), folded once per CTA, converted to fp64 at the end.  The scale
 // 2^S comes from the price column's exponent range (|price * 2^S| < 2^62);
 // non-finite prices, an exponent span above 2^30 or more than 4096
-// categories switch, on the device, to the fp64 pass over the compacted
+// categories switch, on the device, to an fp64 pass over the compacted
 // columns (warp-private fp64 bins, __match_any_sync pre-sums).
 #include "scan.cuh"
 
 namespace skx {
 namespace {
 
-constexpr int kThreads = 256;                  // pass 2: one 4096-row tile per CTA iteration
+constexpr int kThreads = 256;                  // pass 2 / fallback sum CTAs
 constexpr int kWarps = kThreads / 32;
-constexpr int kTile = 4096;
-constexpr int kWarpRows = kTile / kWarps;      // 512 rows per warp
+constexpr int kWarpRows = 256;                 // rows per warp slice
 constexpr int kItems = kWarpRows / 128;        // 4 items of 128 rows (4 per lane)
-constexpr int kThreads1 = 1024;                // pass 1: four tiles per CTA iteration
-constexpr int kSub = kThreads1 / kThreads;
+constexpr uint32_t kCap = 64;                  // compacted entries kept per slice
+constexpr int kThreads1 = 1024;                // pass 1 CTA (shares one bitmap prefix)
 constexpr uint32_t kSmemCategories = 2048;     // fp64 fallback: 8 warps x 2048 x 8 B
 constexpr uint32_t kFixedCategories = 4096;    // fixed point: 3 x 4096 x 4 B per CTA
 constexpr int kRangeLimit = 30;                // max exponent span for fixed point
@@ -135,178 +137,225 @@ __device__ __forceinline__ void add96(unsigned int* lo, unsigned int* mid, unsig
   }
 }
 
-// Pass 1: probe every row once, store the selection as 1 bit per row (per
-// warp: 16 words, word 4i+j bit L = row 128i + 4L + j of the warp's 512),
-// count selected rows per tile and check the domain.
+// Probe helpers.  ids are u32: idx = id - 1 < bits32 <=> in domain (id 0
+// wraps to 2^32 - 1).  One predicated shared or global load per probe.
+__device__ __forceinline__ uint32_t probe_word(uint32_t wi, uint32_t sw, uint32_t s_base,
+                                               const uint32_t* words32) {
+  uint32_t wv;
+  asm volatile(
+      "{\n.reg .pred ps;\nsetp.lt.u32 ps, %1, %2;\n"
+      "@ps ld.shared.u32 %0, [%3];\n@!ps ld.global.nc.u32 %0, [%4];\n}"
+      : "=r"(wv)
+      : "r"(wi), "r"(sw), "r"(s_base + 4 * wi), "l"(words32 + wi));
+  return wv;
+}
+
+// Load the 16 FKs of lane `lane` in slice row0 (rows 128i + 4*lane + j):
+// 128-bit loads when the slice is full and the column 16-byte aligned.
+template <bool VEC>
+__device__ __forceinline__ void load_slice(const uint32_t* __restrict__ fact, uint64_t n,
+                                           uint64_t row0, bool full, int lane,
+                                           uint32_t (&fk)[kItems][4]) {
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    const uint64_t r = row0 + (uint64_t)i * 128 + 4 * lane;
+    if (VEC && full) {
+      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(fact + r));
+      fk[i][0] = v.x, fk[i][1] = v.y, fk[i][2] = v.z, fk[i][3] = v.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) fk[i][j] = r + j < n ? __ldcs(fact + r + j) : 1u;
+    }
+  }
+}
+
+// Selection bits of one slice: sel[i] bit j = row 128i + 4*lane + j selected.
+// Records the first out-of-domain row of the slice.
+__device__ __forceinline__ void probe_slice(const uint32_t (&fk)[kItems][4], uint64_t row0,
+                                            uint64_t n, bool full, uint32_t bits32, uint32_t sw,
+                                            uint32_t s_base, const uint32_t* words32, int lane,
+                                            DevErr* err, uint32_t (&sel)[kItems]) {
+  bool anybad = false;
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    sel[i] = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t idx = fk[i][j] - 1u;
+      const bool live = full || row0 + (uint64_t)i * 128 + 4 * lane + j < n;
+      const bool bad = live && idx >= bits32;
+      const uint32_t wi = (live && !bad) ? idx >> 5 : 0u;
+      const uint32_t wv = probe_word(wi, sw, s_base, words32);
+      if (live && !bad && ((wv >> (idx & 31)) & 1u)) sel[i] |= 1u << j;
+      anybad |= bad;
+    }
+  }
+  if (err != nullptr && __any_sync(0xffffffffu, anybad)) {
+#pragma unroll
+    for (int i = 0; i < kItems; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t k = row0 + (uint64_t)i * 128 + 4 * lane + j;
+        if ((full || k < n) && fk[i][j] - 1u >= bits32) record_violation(err, k, fk[i][j]);
+      }
+  }
+}
+
+// Row-order rank of this lane's j-th row within item i, given the four
+// ballots of the item: rows before it are lanes < lane (any j) and this
+// lane's rows j' < j.
+__device__ __forceinline__ uint32_t item_rank(const uint32_t (&b)[4], uint32_t lt, uint32_t mysel,
+                                              int j) {
+  return __popc(b[0] & lt) + __popc(b[1] & lt) + __popc(b[2] & lt) + __popc(b[3] & lt) +
+         __popc(mysel & ((1u << j) - 1u));
+}
+
+// Pass 1: probe every row once; each warp compacts its slice's selected rows
+// (dimension index, row) in row order into entries[slice][kCap] and writes
+// the slice count.
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads1, 1)
     k_select_count(const uint32_t* __restrict__ fact, uint64_t n,
                    const uint32_t* __restrict__ words32, uint64_t bits,
-                   uint32_t* __restrict__ mask, uint32_t* __restrict__ tile_counts, uint32_t sw,
+                   uint2* __restrict__ entries, uint32_t* __restrict__ slice_counts, uint32_t sw,
                    DevErr* err) {
   extern __shared__ __align__(16) uint32_t s_words[];  // bitmap prefix [sw]
-  __shared__ uint32_t s_w[kThreads1 / 32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int sub = w / kWarps, ws = w % kWarps;
-  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  const int lane = threadIdx.x & 31;
+  const uint64_t nslices = (n + kWarpRows - 1) / kWarpRows;
+  const uint32_t bits32 = bits < 0xFFFFFFFFull ? (uint32_t)bits : 0xFFFFFFFFu;
+  const uint32_t s_base = (uint32_t)__cvta_generic_to_shared(s_words);
+  const uint32_t lt = lanemask_lt();
   for (uint32_t i = threadIdx.x; i < sw; i += kThreads1) s_words[i] = __ldg(words32 + i);
   __syncthreads();
-  for (uint64_t t0 = (uint64_t)blockIdx.x * kSub; t0 < ntiles; t0 += (uint64_t)gridDim.x * kSub) {
-    const uint64_t tile = t0 + sub;
-    const uint64_t wrow0 = tile * kTile + (uint64_t)ws * kWarpRows;
-    const bool full = wrow0 + kWarpRows <= n;  // warp-uniform
+  const uint64_t warps = (uint64_t)gridDim.x * (kThreads1 / 32);
+  for (uint64_t sl = (uint64_t)blockIdx.x * (kThreads1 / 32) + (threadIdx.x >> 5); sl < nslices;
+       sl += warps) {
+    const uint64_t row0 = sl * kWarpRows;
+    const bool full = row0 + kWarpRows <= n;  // warp-uniform
     uint32_t fk[kItems][4];
+    load_slice<VEC>(fact, n, row0, full, lane, fk);
+    uint32_t sel[kItems];
+    probe_slice(fk, row0, n, full, bits32, sw, s_base, words32, lane, err, sel);
+    uint2* out = entries + sl * kCap;
+    uint32_t run = 0;
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
-      const uint64_t r = wrow0 + (uint64_t)i * 128 + 4 * lane;
-      if (VEC && full) {
-        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(fact + r));
-        fk[i][0] = v.x, fk[i][1] = v.y, fk[i][2] = v.z, fk[i][3] = v.w;
-      } else {
+      uint32_t b[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) fk[i][j] = r + j < n ? __ldcs(fact + r + j) : 1u;
-      }
-    }
-    uint32_t c = 0, mine = 0;
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
+      for (int j = 0; j < 4; ++j) b[j] = __ballot_sync(0xffffffffu, (sel[i] >> j) & 1u);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const uint64_t k = wrow0 + (uint64_t)i * 128 + 4 * lane + j;
-        const uint32_t idx = fk[i][j] - 1u;
-        bool sel = false;
-        if (full || k < n) {
-          if (idx < bits) {
-            const uint32_t wi = idx >> 5;
-            const uint32_t wv = wi < sw ? s_words[wi] : __ldg(words32 + wi);
-            sel = (wv >> (idx & 31)) & 1u;
-          } else {
-            record_violation(err, k, fk[i][j]);
-          }
+        if ((sel[i] >> j) & 1u) {
+          const uint32_t pos = run + item_rank(b, lt, sel[i], j);
+          if (pos < kCap)
+            out[pos] = make_uint2(fk[i][j] - 1u, (uint32_t)(row0 + (uint64_t)i * 128 + 4 * lane + j));
         }
-        const uint32_t b = __ballot_sync(0xffffffffu, sel);
-        c += __popc(b);
-        if (lane == i * 4 + j) mine = b;
       }
+      run += __popc(b[0]) + __popc(b[1]) + __popc(b[2]) + __popc(b[3]);
     }
-    if (tile < ntiles && lane < kItems * 4) mask[(wrow0 >> 5) + lane] = mine;
-    if (lane == 0) s_w[w] = c;
-    __syncthreads();
-    if (threadIdx.x < kSub && t0 + threadIdx.x < ntiles) {
-      uint32_t t = 0;
-      for (int i = 0; i < kWarps; ++i) t += s_w[threadIdx.x * kWarps + i];
-      tile_counts[t0 + threadIdx.x] = t;
-    }
-    __syncthreads();
+    if (lane == 0) slice_counts[sl] = run;
   }
 }
 
-// Pass 2, per tile: (A) decode the mask, load the FKs (128-bit, all rows:
-// at ~10% selectivity nearly every sector holds a selected row) and compact
-// (dimension index, row in tile) into shared memory in row order; (B)
-// process the compacted rows densely -- consecutive threads take
-// consecutive selected rows, so the gathers are independent and the output
-// stores coalesce.  FUSED adds the record gather and the per-category sums.
+// One selected row: offset, and (FUSED) the record gather, the four output
+// columns and the fixed-point category sum.
+template <bool FUSED>
+__device__ __forceinline__ void emit_row(uint64_t p, uint32_t idx, uint32_t row, uint32_t base_off,
+                                         uint32_t* __restrict__ out_off, const Cols& cols,
+                                         bool fixed, int S, unsigned int* s_acc) {
+  out_off[p] = base_off + row;
+  if (FUSED) {
+    const uint4* rp = cols.rec + 2 * (uint64_t)idx;
+    uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
+    asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3), "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
+                 : "l"(rp));
+    const int32_t ct = (int32_t)a0;
+    const float pr = __uint_as_float(a1);
+    cols.out_cat[p] = ct;
+    cols.out_price[p] = pr;
+    cols.out_supp[p] = (unsigned long long)a2 | ((unsigned long long)a3 << 32);
+    cols.out_flag[p] = (uint16_t)b0;
+    const uint32_t ncat = cols.n_categories;
+    if (fixed && (uint32_t)ct < ncat) {
+      const long long v = __double2ll_rn(ldexp((double)pr, S));
+      add96(&s_acc[ct], &s_acc[ncat + ct], &s_acc[2 * ncat + ct], v);
+    }
+  }
+}
+
+// Pass 2: every warp takes slices; a slice's selected rows go to
+// slice_off[slice] + rank.  Slices with <= kCap rows copy pass 1's entries
+// (4 independent rows per lane in flight); denser slices are re-derived from
+// the FK column and the bitmap (global probes).
 template <bool FUSED, bool VEC>
 __global__ void __launch_bounds__(kThreads)
-    k_select_write(const uint32_t* __restrict__ fact, uint64_t n, const uint32_t* __restrict__ mask,
-                   uint32_t base_off, const uint32_t* __restrict__ tile_off,
+    k_select_write(const uint32_t* __restrict__ fact, uint64_t n,
+                   const uint32_t* __restrict__ words32, uint64_t bits,
+                   const uint2* __restrict__ entries, const uint32_t* __restrict__ slice_counts,
+                   const uint32_t* __restrict__ slice_off, uint32_t base_off,
                    const uint32_t* __restrict__ total, uint32_t* __restrict__ out_off, Cols cols,
                    unsigned long long* __restrict__ count_dev) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint32_t* s_idx = reinterpret_cast<uint32_t*>(smem_raw);       // [kTile]
-  uint16_t* s_row = reinterpret_cast<uint16_t*>(s_idx + kTile);  // [kTile]
-  unsigned int* s_acc = reinterpret_cast<unsigned int*>(s_row + kTile);  // [3][ncat] (fixed)
-  __shared__ uint32_t s_w[kWarps];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  extern __shared__ __align__(16) unsigned int s_acc[];  // [3][ncat] (fixed-point sums)
+  const int lane = threadIdx.x & 31;
   if (blockIdx.x == 0 && threadIdx.x == 0) *count_dev = *total;
   const uint32_t ncat = cols.n_categories;
   int S = 0;
   const bool fixed = FUSED && cols.sums && fixed_ok(cols.ctl, ncat, S);
   if (fixed) {
     for (uint32_t i = threadIdx.x; i < 3 * ncat; i += kThreads) s_acc[i] = 0u;
+    __syncthreads();
   }
-  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  const uint64_t nslices = (n + kWarpRows - 1) / kWarpRows;
+  const uint32_t bits32 = bits < 0xFFFFFFFFull ? (uint32_t)bits : 0xFFFFFFFFu;
   const uint32_t lt = lanemask_lt();
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint64_t wrow0 = tile * kTile + (uint64_t)w * kWarpRows;
-    const bool full = wrow0 + kWarpRows <= n;
-    const bool any = wrow0 < n;
-    const uint32_t mw = (any && lane < kItems * 4) ? __ldg(mask + (wrow0 >> 5) + lane) : 0u;
-    uint32_t fk[kItems][4];
+  const uint64_t warps = (uint64_t)gridDim.x * kWarps;
+  for (uint64_t sl = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); sl < nslices;
+       sl += warps) {
+    const uint32_t cnt = __ldg(slice_counts + sl);
+    const uint64_t ob = __ldg(slice_off + sl);
+    if (cnt <= kCap) {
+      const uint2* src = entries + sl * kCap;
+      for (uint32_t j0 = 0; j0 < cnt; j0 += 128) {
+        uint2 e[4];
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-      const uint64_t r = wrow0 + (uint64_t)i * 128 + 4 * lane;
-      if (VEC && full) {
-        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(fact + r));
-        fk[i][0] = v.x, fk[i][1] = v.y, fk[i][2] = v.z, fk[i][3] = v.w;
-      } else {
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t j = j0 + q * 32 + lane;
+          e[q] = j < cnt ? __ldcs(src + j) : make_uint2(0u, 0u);
+        }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) fk[i][j] = r + j < n ? __ldcs(fact + r + j) : 0u;
-      }
-    }
-    uint32_t c = 0;
-#pragma unroll
-    for (int q = 0; q < kItems * 4; ++q) c += __popc(__shfl_sync(0xffffffffu, mw, q));
-    if (lane == 0) s_w[w] = c;
-    __syncthreads();
-    uint32_t lpos = 0, cnt_tile = 0;
-    for (int i = 0; i < kWarps; ++i) {
-      lpos += i < w ? s_w[i] : 0u;
-      cnt_tile += s_w[i];
-    }
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-      uint32_t m[4], before = 0, cnt = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        m[j] = __shfl_sync(0xffffffffu, mw, i * 4 + j);
-        before += __popc(m[j] & lt);
-        cnt += __popc(m[j]);
-      }
-      uint32_t pos = lpos + before;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if ((m[j] >> lane) & 1u) {
-          s_idx[pos] = fk[i][j] - 1u;
-          s_row[pos] = (uint16_t)(w * kWarpRows + i * 128 + 4 * lane + j);
-          ++pos;
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t j = j0 + q * 32 + lane;
+          if (j < cnt) emit_row<FUSED>(ob + j, e[q].x, e[q].y, base_off, out_off, cols, fixed, S,
+                                       s_acc);
         }
       }
-      lpos += cnt;
-    }
-    __syncthreads();
-    // (B) dense pass over the tile's selected rows
-    const uint64_t obase = tile_off[tile];
-    for (uint32_t j0 = 0; j0 < cnt_tile; j0 += kThreads) {
-      const uint32_t j = j0 + threadIdx.x;
-      if (j < cnt_tile) {
-        const uint64_t p = obase + j;
-        out_off[p] = base_off + (uint32_t)(tile * kTile + s_row[j]);
-        if (FUSED) {
-          const uint4* rp = cols.rec + 2 * (uint64_t)s_idx[j];
-          uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
-          asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                       : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3), "=r"(b0), "=r"(b1), "=r"(b2),
-                         "=r"(b3)
-                       : "l"(rp));
-          const int32_t ct = (int32_t)a0;
-          const float pr = __uint_as_float(a1);
-          cols.out_cat[p] = ct;
-          cols.out_price[p] = pr;
-          cols.out_supp[p] = (unsigned long long)a2 | ((unsigned long long)a3 << 32);
-          cols.out_flag[p] = (uint16_t)b0;
-          if (fixed && (uint32_t)ct < ncat) {
-            const long long v = __double2ll_rn(ldexp((double)pr, S));
-            add96(&s_acc[ct], &s_acc[ncat + ct], &s_acc[2 * ncat + ct], v);
-          }
-        }
+    } else {
+      const uint64_t row0 = sl * kWarpRows;
+      const bool full = row0 + kWarpRows <= n;
+      uint32_t fk[kItems][4];
+      load_slice<VEC>(fact, n, row0, full, lane, fk);
+      uint32_t sel[kItems];
+      // domain already checked in pass 1: err = nullptr is never written
+      probe_slice(fk, row0, n, full, bits32, 0u, 0u, words32, lane, nullptr, sel);
+      uint32_t run = 0;
+#pragma unroll
+      for (int i = 0; i < kItems; ++i) {
+        uint32_t b[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = __ballot_sync(0xffffffffu, (sel[i] >> j) & 1u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if ((sel[i] >> j) & 1u)
+            emit_row<FUSED>(ob + run + item_rank(b, lt, sel[i], j), fk[i][j] - 1u,
+                            (uint32_t)(row0 + (uint64_t)i * 128 + 4 * lane + j), base_off,
+                            out_off, cols, fixed, S, s_acc);
+        run += __popc(b[0]) + __popc(b[1]) + __popc(b[2]) + __popc(b[3]);
       }
     }
-    __syncthreads();  // s_idx / s_row / s_w reused by the next tile
   }
   if (fixed) {
-    // s_acc was last touched before the loop's trailing barrier.
+    __syncthreads();
     for (uint32_t c2 = threadIdx.x; c2 < ncat; c2 += kThreads) {
       const unsigned int L = s_acc[c2], M = s_acc[ncat + c2], H = s_acc[2 * ncat + c2];
       if ((L | M | H) == 0u) continue;
@@ -438,19 +487,19 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
     e = cudaMemsetAsync(count_dev, 0, 8, s);
     return e == cudaSuccess ? SKX_OK : cuda_fail(ctx, e, "select memset");
   }
-  const uint64_t ntiles = (n + kTile - 1) / kTile;
-  // scratch: mask words [ntiles * 128] | tile counts | tile offsets | total |
+  const uint64_t nslices = (n + kWarpRows - 1) / kWarpRows;
+  // scratch: entries [nslices][kCap] | slice counts | slice offsets | total |
   //          (fused) SumCtl 256 B | acc96 [ncat][4] | records [d][32 B]
-  const uint64_t base_b = (ntiles * (kTile / 32 + 2) * 4 + 256 + 255) & ~uint64_t(255);
+  const uint64_t ent_b = nslices * kCap * 8;
+  const uint64_t base_b = (ent_b + nslices * 8 + 256 + 255) & ~uint64_t(255);
   const uint64_t acc_b = fused ? (((uint64_t)cols.n_categories * 16 + 255) & ~uint64_t(255)) : 0;
   const uint64_t rec_b = fused ? bits * 32 : 0;
   char* raw = static_cast<char*>(scratch(ctx, 2, base_b + (fused ? 256 : 0) + acc_b + rec_b));
   if (!raw) return set_error(ctx, SKX_CUDA_ERROR, "select: out of device memory");
-  uint32_t* sp = reinterpret_cast<uint32_t*>(raw);
-  uint32_t* mask = sp;
-  uint32_t* counts = sp + ntiles * (kTile / 32);
-  uint32_t* offs = counts + ntiles;
-  uint32_t* total = offs + ntiles;
+  uint2* entries = reinterpret_cast<uint2*>(raw);
+  uint32_t* counts = reinterpret_cast<uint32_t*>(raw + ent_b);
+  uint32_t* offs = counts + nslices;
+  uint32_t* total = offs + nslices;
   if (fused) {
     cols.ctl = reinterpret_cast<SumCtl*>(raw + base_b);
     cols.acc96 = reinterpret_cast<unsigned int*>(raw + base_b + 256);
@@ -465,6 +514,7 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
     }
   }
   const bool vec = reinterpret_cast<uintptr_t>(fact) % 16 == 0;
+  const auto* w32 = reinterpret_cast<const uint32_t*>(words);
   // Pass 1 with the bitmap prefix staged per CTA in shared memory.
   const uint64_t nw32 = (bits + 31) / 32;
   size_t sbytes = (size_t)SKX_SEL_SMEM_KB * 1024;
@@ -473,23 +523,22 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
   const size_t smem1 = (size_t)sw * 4;
   auto k1 = vec ? k_select_count<true> : k_select_count<false>;
   cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
-  const uint64_t iters = (ntiles + kSub - 1) / kSub;
-  const unsigned grid1 = (unsigned)(iters < (uint64_t)ctx->num_sms ? iters : ctx->num_sms);
-  k1<<<grid1, kThreads1, smem1, s>>>(fact, n, reinterpret_cast<const uint32_t*>(words), bits, mask,
-                                     counts, sw, ctx->err);
+  const uint64_t cta1 = (nslices + kThreads1 / 32 - 1) / (kThreads1 / 32);
+  const unsigned grid1 = (unsigned)(cta1 < (uint64_t)ctx->num_sms ? cta1 : ctx->num_sms);
+  k1<<<grid1, kThreads1, smem1, s>>>(fact, n, w32, bits, entries, counts, sw, ctx->err);
   ctx->launches++;
-  int rc = launch_exclusive_scan_u32(ctx, counts, offs, ntiles, total, 3, s);
+  int rc = launch_exclusive_scan_u32(ctx, counts, offs, nslices, total, 3, s);
   if (rc) return rc;
-  const size_t smem = (size_t)kTile * (4 + 2) +
-                      (sums_on && cols.n_categories <= kFixedCategories ? (size_t)cols.n_categories * 12 : 0);
+  const size_t smem = sums_on && cols.n_categories <= kFixedCategories
+                          ? (size_t)cols.n_categories * 12 : 0;
   auto k2 = fused ? (vec ? k_select_write<true, true> : k_select_write<true, false>)
                   : (vec ? k_select_write<false, true> : k_select_write<false, false>);
   cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2, kThreads, smem);
-  const unsigned grid2 = grid_for(ctx, ntiles, 1, per_sm < 1 ? 1 : per_sm);
-  k2<<<grid2, kThreads, smem, s>>>(fact, n, mask, base, offs, total, out, cols,
-                                   reinterpret_cast<unsigned long long*>(count_dev));
+  const unsigned grid2 = grid_for(ctx, (nslices + kWarps - 1) / kWarps, 1, per_sm < 1 ? 1 : per_sm);
+  k2<<<grid2, kThreads, smem, s>>>(fact, n, w32, bits, entries, counts, offs, base, total, out,
+                                   cols, reinterpret_cast<unsigned long long*>(count_dev));
   ctx->launches++;
   if (sums_on) {
     k_sum_finalize<<<(cols.n_categories + 255) / 256, 256, 0, s>>>(cols.acc96, cols.ctl,

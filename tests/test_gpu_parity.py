@@ -248,11 +248,12 @@ def test_select_gather_sum_vs_oracle(sx, oracle):
 
 
 @pytest.mark.parametrize("case", ["neg", "wide", "nan", "zero", "many_cats", "unaligned",
-                                  "ragged"])
+                                  "ragged", "dense", "mixed_density"])
 def test_select_gather_sum_paths(sx, oracle, case):
     """Fixed-point category sums (default) and the on-device fp64 fallback
     (non-finite price, exponent span > 2^30, > 4096 categories), signed
-    prices, unaligned and ragged FK columns."""
+    prices, unaligned and ragged FK columns, and selections dense enough that
+    slices overflow pass 1's compacted entries (re-derived in pass 2)."""
     d = 1 << 14
     n = (1 << 20) + (4093 if case == "ragged" else 0)
     rng = np.random.default_rng(11)
@@ -271,7 +272,7 @@ def test_select_gather_sum_paths(sx, oracle, case):
     flag = rng.integers(0, 2**16, size=d, dtype=np.uint16)
     fact = sx.generate_zipf(cu(sx.zipf_cdf(d, 1.0)), n + 1, 7)
     fact = fact[1:] if case == "unaligned" else fact[:n]
-    thr = 700 if case == "many_cats" else 100
+    thr = {"many_cats": 700, "dense": 1000, "mixed_density": 250}.get(case, 100)
     bm = sx.build_bitmap_lt(cu(cat), thr)
     got = sx.select_gather_sum(fact, bm, cu(cat), cu(price), cu(supp), cu(flag), ncat, base=5)
     exp = oracle.select_gather_sum(np_(fact), np_(bm.words), cat, price, supp, flag, ncat, base=5)
