@@ -170,9 +170,10 @@ __device__ __forceinline__ void load_slice(const uint32_t* __restrict__ fact, ui
 }
 
 // Selection bits of one slice: sel[i] bit j = row 128i + 4*lane + j selected.
-// Records the first out-of-domain row of the slice.
+// Records the first out-of-domain row of the slice (when err != nullptr).
+template <bool FULL>
 __device__ __forceinline__ void probe_slice(const uint32_t (&fk)[kItems][4], uint64_t row0,
-                                            uint64_t n, bool full, uint32_t bits32, uint32_t sw,
+                                            uint64_t n, uint32_t bits32, uint32_t sw,
                                             uint32_t s_base, const uint32_t* words32, int lane,
                                             DevErr* err, uint32_t (&sel)[kItems]) {
   bool anybad = false;
@@ -182,12 +183,11 @@ __device__ __forceinline__ void probe_slice(const uint32_t (&fk)[kItems][4], uin
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const uint32_t idx = fk[i][j] - 1u;
-      const bool live = full || row0 + (uint64_t)i * 128 + 4 * lane + j < n;
-      const bool bad = live && idx >= bits32;
-      const uint32_t wi = (live && !bad) ? idx >> 5 : 0u;
-      const uint32_t wv = probe_word(wi, sw, s_base, words32);
-      if (live && !bad && ((wv >> (idx & 31)) & 1u)) sel[i] |= 1u << j;
-      anybad |= bad;
+      const bool live = FULL || row0 + (uint64_t)i * 128 + 4 * lane + j < n;
+      const bool ok = live && idx < bits32;
+      const uint32_t wv = probe_word(ok ? idx >> 5 : 0u, sw, s_base, words32);
+      sel[i] |= (ok ? (wv >> (idx & 31)) & 1u : 0u) << j;
+      anybad |= live && !ok;
     }
   }
   if (err != nullptr && __any_sync(0xffffffffu, anybad)) {
@@ -196,18 +196,18 @@ __device__ __forceinline__ void probe_slice(const uint32_t (&fk)[kItems][4], uin
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const uint64_t k = row0 + (uint64_t)i * 128 + 4 * lane + j;
-        if ((full || k < n) && fk[i][j] - 1u >= bits32) record_violation(err, k, fk[i][j]);
+        if ((FULL || k < n) && fk[i][j] - 1u >= bits32) record_violation(err, k, fk[i][j]);
       }
   }
 }
 
-// Row-order rank of this lane's j-th row within item i, given the four
-// ballots of the item: rows before it are lanes < lane (any j) and this
-// lane's rows j' < j.
-__device__ __forceinline__ uint32_t item_rank(const uint32_t (&b)[4], uint32_t lt, uint32_t mysel,
-                                              int j) {
-  return __popc(b[0] & lt) + __popc(b[1] & lt) + __popc(b[2] & lt) + __popc(b[3] & lt) +
-         __popc(mysel & ((1u << j) - 1u));
+// Compact one 128-row item: rows before this lane's j-th row are the
+// selected rows of lanes < lane (any j) and this lane's rows j' < j.
+__device__ __forceinline__ uint32_t item_base(const uint32_t (&b)[4], uint32_t lt) {
+  return __popc(b[0] & lt) + __popc(b[1] & lt) + __popc(b[2] & lt) + __popc(b[3] & lt);
+}
+__device__ __forceinline__ uint32_t item_count(const uint32_t (&b)[4]) {
+  return __popc(b[0]) + __popc(b[1]) + __popc(b[2]) + __popc(b[3]);
 }
 
 // Pass 1: probe every row once; each warp compacts its slice's selected rows
@@ -235,47 +235,61 @@ __global__ void __launch_bounds__(kThreads1, 1)
     uint32_t fk[kItems][4];
     load_slice<VEC>(fact, n, row0, full, lane, fk);
     uint32_t sel[kItems];
-    probe_slice(fk, row0, n, full, bits32, sw, s_base, words32, lane, err, sel);
+    if (full)
+      probe_slice<true>(fk, row0, n, bits32, sw, s_base, words32, lane, err, sel);
+    else
+      probe_slice<false>(fk, row0, n, bits32, sw, s_base, words32, lane, err, sel);
     uint2* out = entries + sl * kCap;
+    const uint32_t row_l = (uint32_t)row0 + 4u * lane;  // n < 2^32
     uint32_t run = 0;
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
       uint32_t b[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) b[j] = __ballot_sync(0xffffffffu, (sel[i] >> j) & 1u);
+      if (sel[i]) {
+        uint32_t pos = run + item_base(b, lt);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if ((sel[i] >> j) & 1u) {
-          const uint32_t pos = run + item_rank(b, lt, sel[i], j);
-          if (pos < kCap)
-            out[pos] = make_uint2(fk[i][j] - 1u, (uint32_t)(row0 + (uint64_t)i * 128 + 4 * lane + j));
+        for (int j = 0; j < 4; ++j) {
+          if ((sel[i] >> j) & 1u) {
+            if (pos < kCap) out[pos] = make_uint2(fk[i][j] - 1u, row_l + i * 128 + j);
+            ++pos;
+          }
         }
       }
-      run += __popc(b[0]) + __popc(b[1]) + __popc(b[2]) + __popc(b[3]);
+      run += item_count(b);
     }
     if (lane == 0) slice_counts[sl] = run;
   }
 }
 
-// One selected row: offset, and (FUSED) the record gather, the four output
-// columns and the fixed-point category sum.
+struct Rec8 {
+  uint32_t a0, a1, a2, a3, b0;
+};
+
+__device__ __forceinline__ Rec8 load_rec(const uint4* rec, uint32_t idx) {
+  Rec8 r;
+  uint32_t b1, b2, b3;
+  asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(r.a0), "=r"(r.a1), "=r"(r.a2), "=r"(r.a3), "=r"(r.b0), "=r"(b1), "=r"(b2), "=r"(b3)
+      : "l"(rec + 2 * (uint64_t)idx));
+  return r;
+}
+
+// One selected row: offset, and (FUSED) the four output columns and the
+// fixed-point category sum from its record.
 template <bool FUSED>
-__device__ __forceinline__ void emit_row(uint64_t p, uint32_t idx, uint32_t row, uint32_t base_off,
-                                         uint32_t* __restrict__ out_off, const Cols& cols,
-                                         bool fixed, int S, unsigned int* s_acc) {
+__device__ __forceinline__ void emit_row(uint64_t p, uint32_t row, const Rec8& r,
+                                         uint32_t base_off, uint32_t* __restrict__ out_off,
+                                         const Cols& cols, bool fixed, int S, unsigned int* s_acc) {
   out_off[p] = base_off + row;
   if (FUSED) {
-    const uint4* rp = cols.rec + 2 * (uint64_t)idx;
-    uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
-    asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3), "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
-                 : "l"(rp));
-    const int32_t ct = (int32_t)a0;
-    const float pr = __uint_as_float(a1);
+    const int32_t ct = (int32_t)r.a0;
+    const float pr = __uint_as_float(r.a1);
     cols.out_cat[p] = ct;
     cols.out_price[p] = pr;
-    cols.out_supp[p] = (unsigned long long)a2 | ((unsigned long long)a3 << 32);
-    cols.out_flag[p] = (uint16_t)b0;
+    cols.out_supp[p] = (unsigned long long)r.a2 | ((unsigned long long)r.a3 << 32);
+    cols.out_flag[p] = (uint16_t)r.b0;
     const uint32_t ncat = cols.n_categories;
     if (fixed && (uint32_t)ct < ncat) {
       const long long v = __double2ll_rn(ldexp((double)pr, S));
@@ -301,7 +315,11 @@ __global__ void __launch_bounds__(kThreads)
   if (blockIdx.x == 0 && threadIdx.x == 0) *count_dev = *total;
   const uint32_t ncat = cols.n_categories;
   int S = 0;
+#ifdef SKX_SEL_DIAG_NOSUM
+  const bool fixed = false;  // diagnostic build: no category sums
+#else
   const bool fixed = FUSED && cols.sums && fixed_ok(cols.ctl, ncat, S);
+#endif
   if (fixed) {
     for (uint32_t i = threadIdx.x; i < 3 * ncat; i += kThreads) s_acc[i] = 0u;
     __syncthreads();
@@ -316,19 +334,18 @@ __global__ void __launch_bounds__(kThreads)
     const uint64_t ob = __ldg(slice_off + sl);
     if (cnt <= kCap) {
       const uint2* src = entries + sl * kCap;
-      for (uint32_t j0 = 0; j0 < cnt; j0 += 128) {
-        uint2 e[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t j = j0 + q * 32 + lane;
-          e[q] = j < cnt ? __ldcs(src + j) : make_uint2(0u, 0u);
+      for (uint32_t j0 = 0; j0 < cnt; j0 += 64) {
+        // two entries per lane: both record loads in flight before any store
+        const uint32_t ja = j0 + lane, jb = j0 + 32 + lane;
+        const uint2 ea = ja < cnt ? __ldcs(src + ja) : make_uint2(0u, 0u);
+        const uint2 eb = jb < cnt ? __ldcs(src + jb) : make_uint2(0u, 0u);
+        Rec8 ra{}, rb{};
+        if (FUSED) {
+          if (ja < cnt) ra = load_rec(cols.rec, ea.x);
+          if (jb < cnt) rb = load_rec(cols.rec, eb.x);
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t j = j0 + q * 32 + lane;
-          if (j < cnt) emit_row<FUSED>(ob + j, e[q].x, e[q].y, base_off, out_off, cols, fixed, S,
-                                       s_acc);
-        }
+        if (ja < cnt) emit_row<FUSED>(ob + ja, ea.y, ra, base_off, out_off, cols, fixed, S, s_acc);
+        if (jb < cnt) emit_row<FUSED>(ob + jb, eb.y, rb, base_off, out_off, cols, fixed, S, s_acc);
       }
     } else {
       const uint64_t row0 = sl * kWarpRows;
@@ -336,21 +353,30 @@ __global__ void __launch_bounds__(kThreads)
       uint32_t fk[kItems][4];
       load_slice<VEC>(fact, n, row0, full, lane, fk);
       uint32_t sel[kItems];
-      // domain already checked in pass 1: err = nullptr is never written
-      probe_slice(fk, row0, n, full, bits32, 0u, 0u, words32, lane, nullptr, sel);
+      // domain already checked in pass 1 (err = nullptr)
+      if (full)
+        probe_slice<true>(fk, row0, n, bits32, 0u, 0u, words32, lane, nullptr, sel);
+      else
+        probe_slice<false>(fk, row0, n, bits32, 0u, 0u, words32, lane, nullptr, sel);
+      const uint32_t row_l = (uint32_t)row0 + 4u * lane;
       uint32_t run = 0;
 #pragma unroll
       for (int i = 0; i < kItems; ++i) {
         uint32_t b[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) b[j] = __ballot_sync(0xffffffffu, (sel[i] >> j) & 1u);
+        uint32_t pos = run + item_base(b, lt);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if ((sel[i] >> j) & 1u)
-            emit_row<FUSED>(ob + run + item_rank(b, lt, sel[i], j), fk[i][j] - 1u,
-                            (uint32_t)(row0 + (uint64_t)i * 128 + 4 * lane + j), base_off,
-                            out_off, cols, fixed, S, s_acc);
-        run += __popc(b[0]) + __popc(b[1]) + __popc(b[2]) + __popc(b[3]);
+        for (int j = 0; j < 4; ++j) {
+          if ((sel[i] >> j) & 1u) {
+            Rec8 r{};
+            if (FUSED) r = load_rec(cols.rec, fk[i][j] - 1u);
+            emit_row<FUSED>(ob + pos, row_l + i * 128 + j, r, base_off, out_off, cols, fixed, S,
+                            s_acc);
+            ++pos;
+          }
+        }
+        run += item_count(b);
       }
     }
   }
@@ -521,10 +547,10 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
   if (sbytes > ctx->smem_optin - 1024) sbytes = ctx->smem_optin - 1024;
   const uint32_t sw = (uint32_t)(nw32 < sbytes / 4 ? nw32 : sbytes / 4);
   const size_t smem1 = (size_t)sw * 4;
-  auto k1 = vec ? k_select_count<true> : k_select_count<false>;
-  cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
   const uint64_t cta1 = (nslices + kThreads1 / 32 - 1) / (kThreads1 / 32);
   const unsigned grid1 = (unsigned)(cta1 < (uint64_t)ctx->num_sms ? cta1 : ctx->num_sms);
+  auto k1 = vec ? k_select_count<true> : k_select_count<false>;
+  cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
   k1<<<grid1, kThreads1, smem1, s>>>(fact, n, w32, bits, entries, counts, sw, ctx->err);
   ctx->launches++;
   int rc = launch_exclusive_scan_u32(ctx, counts, offs, nslices, total, 3, s);
