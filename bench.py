@@ -427,6 +427,7 @@ def run_ours(args):
                    "roofline": {"bound": "hbm", "achieved": gb_bytes / (statistics.mean(per_g) * 1e-3) / 1e9,
                                 "peak": peak, "unit": "GB/s",
                                 "frac": gb_bytes / (statistics.mean(per_g) * 1e-3) / 1e9 / peak,
+                                "traffic": ncu_traffic("groupby_c3"),
                                 "alg_bytes_per_step": gb_bytes}}
         del gdat, counts, sums
         torch.cuda.empty_cache()

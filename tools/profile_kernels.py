@@ -1,7 +1,7 @@
 """Run each hot kernel once inside a cudaProfilerStart/Stop window so that
 `ncu --profile-from-start off` captures exactly those launches.
 
-  python tools/profile_kernels.py [--ops gather_freq,gather_rand,groupby,histogram]
+  python tools/profile_kernels.py [--ops gather_freq,gather_rand,groupby,histogram,select]
 """
 import argparse
 import os
@@ -14,7 +14,7 @@ from paper_1910_10063_b200 import dataset as dsm  # noqa: E402
 from paper_1910_10063_b200 import skewdx as sx  # noqa: E402
 
 p = argparse.ArgumentParser()
-p.add_argument("--ops", default="gather_freq,gather_rand,groupby,histogram")
+p.add_argument("--ops", default="gather_freq,gather_rand,groupby,histogram,select")
 p.add_argument("--z", type=float, default=1.0)
 p.add_argument("--rows", type=int, default=1 << 30)
 p.add_argument("--domain", type=int, default=1 << 27)
@@ -37,6 +37,20 @@ if "groupby" in ops:
         sx.aggregate_count_sum(gb.fact_freq, gb.qty, 1 << 24)
 if "histogram" in ops:
     sx.histogram_u32(g.fact_rand, a.domain)
+sel = None
+if "select" in ops:  # C5: 2^31 rows, D=2^25, reordered layout, category < 100
+    d5, n5 = 1 << 25, 1 << 31
+    f5 = dsm.make_rand_fact(d5, n5, 1.0, 42, dsm.shard_of(n5))
+    idx5 = sx.build_index(sx.FrequencyProfile(sx.histogram_u32(f5, d5), n5))
+    f5 = sx.recode_fact(f5, idx5)
+    cat = sx.permute_dimension(dsm.fill_column(1, torch.int32, d5, 11, 0, 1000), idx5)
+    price = sx.permute_dimension(dsm.fill_column(2, torch.float32, d5, 12, 3.0, 1.0), idx5)
+    supp = sx.permute_dimension(dsm.fill_column(0, torch.int64, d5, 13), idx5)
+    flag = sx.permute_dimension(dsm.fill_column(0, torch.int16, d5, 14), idx5)
+    bm = sx.build_bitmap_lt(cat, 100)
+    del idx5
+    sel = (f5, bm, cat, price, supp, flag)
+    sx.select_gather_sum(*sel, 1000)
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
 for o in ops:
@@ -48,6 +62,8 @@ for o in ops:
         sx.aggregate_count_sum(gb.fact_freq, gb.qty, 1 << 24, sync=False)
     elif o == "histogram":
         sx.histogram_u32(g.fact_rand, a.domain, sync=False)
+    elif o == "select":
+        sx.select_gather_sum(*sel, 1000)
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
 ctx.sync()
