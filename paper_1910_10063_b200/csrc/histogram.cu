@@ -12,13 +12,17 @@
 //     sees first -- for skewed data the hot ones -- claiming slots with CAS;
 //  3. a key that finds no slot within kProbe probes is cold: for small
 //     domains (counters L2-resident) it is a global red.add; for large ones
-//     (counters >> L2) it is appended to the bucket of its key range
-//     (bucket.cuh) and folded in shared memory by a second kernel, so no
-//     cold update read-modify-writes an HBM line;
+//     (counters >> L2) the CTA collects the cold (key, count) pairs of each
+//     4096-row tile in shared memory, partitions them by key range (64
+//     ranges) and appends each range's run to that range's global bucket
+//     with one cursor atomic; a second kernel applies each bucket while its
+//     counter slice is L2-resident -- so no cold update read-modify-writes an
+//     HBM line (on B200 every L2 miss moves a 128-byte line,
+//     profiles/r1_experiments.md §7);
 //  4. each CTA flushes its table once.
 // The FK column is streamed once with 128-bit evict_first loads; the domain
 // check is fused (first bad row via atomicMin, reported at skx_sync).
-#include "bucket.cuh"
+#include "skx_internal.cuh"
 
 namespace skx {
 namespace {
@@ -28,9 +32,9 @@ constexpr int kTableBits = 13;  // 8192 slots x 8 B = 64 KB per CTA
 constexpr int kTable = 1 << kTableBits;
 constexpr int kProbe = 4;
 constexpr int kUnroll = 2;        // uint4 per thread per iteration
-constexpr int kBucketShift = 15;  // 32768 keys per bucket: 128 KB of u32 fold counters
-constexpr uint32_t kBucketRange = 1u << kBucketShift;
-constexpr int kFoldThreads = 1024;
+constexpr int kTileRows = kThreads * kUnroll * 4;  // rows per CTA iteration
+constexpr int kNB = 64;           // key-range buckets (staged cold path)
+constexpr int kLocalBits = 26;    // entry = (count << 26) | (idx - bucket base)
 
 __device__ __forceinline__ uint32_t slot_hash(uint32_t id) {
   return (id * 0x9E3779B1u) >> (32 - kTableBits);
@@ -49,15 +53,25 @@ __device__ __forceinline__ void global_add<unsigned long long>(unsigned long lon
 }
 
 struct Buckets {
-  unsigned int* cursors;  // [nb]
-  uint32_t* buf;          // [nb][cap]: (count << 16) | (id-1 within bucket)
+  unsigned int* cursors;  // [kNB]
+  uint32_t* buf;          // [kNB][cap]: (count << 26) | (idx - (b << shift))
   uint64_t cap;
+  uint32_t shift;         // bucket = idx >> shift
+};
+
+// Shared-memory state of the bucketed (BK) path: the tile's cold pairs and
+// its per-range counts / global bases.
+struct TileCold {
+  unsigned long long* pairs;  // [kTileRows]: (count << 32) | idx
+  unsigned int* n;            // number of pairs
+  unsigned int* cnt;          // [kNB]
+  unsigned int* base;         // [kNB]
 };
 
 // Warp-collective: every lane calls it (invalid lanes with valid = false).
 template <typename CT, bool BK>
 __device__ __forceinline__ void count_one(uint32_t id, bool valid, uint32_t* keys, uint32_t* cnts,
-                                          CT* counts, const Buckets& bk) {
+                                          CT* counts, const TileCold& tc) {
   const uint32_t key = valid ? id : 0u;
   const uint32_t peers = __match_any_sync(0xffffffffu, key);
   const uint32_t lane = threadIdx.x & 31;
@@ -83,25 +97,68 @@ __device__ __forceinline__ void count_one(uint32_t id, bool valid, uint32_t* key
     }
     if (cold && !BK) global_add<CT>(counts, key - 1, c);
   }
-  if (BK && __any_sync(0xffffffffu, cold)) {
-    const uint32_t idx = key - 1u;
-    if (!bucket_append<uint32_t>(idx >> kBucketShift, cold, (c << 16) | (idx & (kBucketRange - 1)),
-                                 bk.cursors, bk.buf, bk.cap))
-      global_add<CT>(counts, idx, c);  // bucket full: fall back to a direct update
+  if (BK) {  // warp-aggregated append to the tile's cold list
+    const uint32_t m = __ballot_sync(0xffffffffu, cold);
+    if (m) {
+      const int lane = threadIdx.x & 31;
+      const int first = __ffs(m) - 1;
+      unsigned int at = 0;
+      if (lane == first) at = atomicAdd(tc.n, (unsigned int)__popc(m));
+      at = __shfl_sync(0xffffffffu, at, first);
+      if (cold)
+        tc.pairs[at + __popc(m & lanemask_lt())] = ((unsigned long long)c << 32) | (key - 1u);
+    }
   }
+}
+
+// BK: partition the tile's cold pairs by key range and append each range's
+// run to its global bucket (one cursor atomic per range per tile).  Called
+// by the whole CTA between barriers.
+template <typename CT>
+__device__ __forceinline__ void flush_tile(const TileCold& tc, const Buckets& bk, CT* counts) {
+  __syncthreads();
+  const unsigned int m = *tc.n;
+  for (unsigned int i = threadIdx.x; i < m; i += kThreads)
+    atomicAdd(&tc.cnt[(uint32_t)tc.pairs[i] >> bk.shift], 1u);
+  __syncthreads();
+  if (threadIdx.x < kNB) {
+    const unsigned int c = tc.cnt[threadIdx.x];
+    tc.base[threadIdx.x] = c ? atomicAdd(&bk.cursors[threadIdx.x], c) : 0u;
+    tc.cnt[threadIdx.x] = 0u;
+  }
+  __syncthreads();
+  for (unsigned int i = threadIdx.x; i < m; i += kThreads) {
+    const unsigned long long p = tc.pairs[i];
+    const uint32_t idx = (uint32_t)p, c = (uint32_t)(p >> 32);
+    const uint32_t b = idx >> bk.shift;
+    const uint64_t pos = (uint64_t)tc.base[b] + atomicAdd(&tc.cnt[b], 1u);
+    if (pos < bk.cap)
+      bk.buf[(uint64_t)b * bk.cap + pos] = (c << kLocalBits) | (idx - (b << bk.shift));
+    else
+      global_add<CT>(counts, idx, c);  // bucket full: direct reduction
+  }
+  __syncthreads();
+  if (threadIdx.x < kNB) tc.cnt[threadIdx.x] = 0u;
+  if (threadIdx.x == 0) *tc.n = 0u;
+  __syncthreads();  // resets visible before the next tile's appends
 }
 
 template <typename CT, bool BK>
 __global__ void __launch_bounds__(kThreads)
     k_histogram(const uint32_t* __restrict__ fact, uint64_t head, uint64_t nvec, uint64_t n,
                 uint32_t d, CT* __restrict__ counts, Buckets bk, DevErr* err) {
-  extern __shared__ uint32_t smem_tab[];
+  extern __shared__ __align__(16) uint32_t smem_tab[];
   uint32_t* keys = smem_tab;
   uint32_t* cnts = smem_tab + kTable;
+  // BK: [pairs kTileRows x u64][n][cnt kNB][base kNB] after the table
+  TileCold tc{reinterpret_cast<unsigned long long*>(smem_tab + 2 * kTable),
+              smem_tab + 2 * kTable + 2 * kTileRows, smem_tab + 2 * kTable + 2 * kTileRows + 1,
+              smem_tab + 2 * kTable + 2 * kTileRows + 1 + kNB};
   for (int i = threadIdx.x; i < kTable; i += kThreads) {
     keys[i] = 0u;
     cnts[i] = 0u;
   }
+  if (BK && threadIdx.x <= kNB) tc.n[threadIdx.x] = 0u;  // n and cnt[]
   __syncthreads();
   const uint64_t pol = policy_evict_first();
   const uint4* fv = reinterpret_cast<const uint4*>(fact + head);
@@ -126,9 +183,10 @@ __global__ void __launch_bounds__(kThreads)
       for (int j = 0; j < 4; ++j) {
         const bool ok = (ids[j] - 1u) < d;
         if (live && !ok) record_violation(err, head + vi * 4 + j, ids[j]);
-        count_one<CT, BK>(ids[j], live && ok, keys, cnts, counts, bk);
+        count_one<CT, BK>(ids[j], live && ok, keys, cnts, counts, tc);
       }
     }
+    if (BK) flush_tile<CT>(tc, bk, counts);
   }
   // Scalar head [0, head) and tail [head + 4*nvec, n): block 0, warp-uniform trips.
   if (blockIdx.x == 0) {
@@ -142,9 +200,10 @@ __global__ void __launch_bounds__(kThreads)
       const uint32_t id = live ? fact[k] : 0u;
       const bool ok = (id - 1u) < d;
       if (live && !ok) record_violation(err, k, id);
-      count_one<CT, BK>(id, live && ok, keys, cnts, counts, bk);
+      count_one<CT, BK>(id, live && ok, keys, cnts, counts, tc);
     }
   }
+  if (BK) flush_tile<CT>(tc, bk, counts);  // block-uniform: also blocks != 0
   __syncthreads();
   for (int i = threadIdx.x; i < kTable; i += kThreads) {
     const uint32_t k = keys[i];
@@ -152,28 +211,21 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// Second kernel: fold each key-range bucket in shared memory, then update its
-// (exclusively owned) counters with plain coalesced read-modify-writes.
+// Second kernel: apply the buckets in key-range order; all CTAs sweep bucket
+// b together, so its counter slice (2^shift counters) stays L2-resident and
+// the reductions never read-modify-write HBM lines.
 template <typename CT>
-__global__ void __launch_bounds__(kFoldThreads, 1)
-    k_hist_fold(Buckets bk, uint32_t nb, uint32_t d, CT* __restrict__ counts) {
-  extern __shared__ uint32_t sc[];  // [kBucketRange]
-  for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
-    for (uint32_t j = threadIdx.x; j < kBucketRange; j += kFoldThreads) sc[j] = 0u;
-    __syncthreads();
+__global__ void __launch_bounds__(256)
+    k_hist_fold(Buckets bk, CT* __restrict__ counts) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint32_t b = 0; b < kNB; ++b) {
     const uint64_t m = bk.cursors[b] < bk.cap ? bk.cursors[b] : bk.cap;
     const uint32_t* src = bk.buf + (uint64_t)b * bk.cap;
-    for (uint64_t i = threadIdx.x; i < m; i += kFoldThreads) {
+    const uint32_t g0 = b << bk.shift;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
       const uint32_t v = __ldcs(src + i);
-      atomicAdd(&sc[v & 0xFFFFu], v >> 16);
+      global_add<CT>(counts, g0 + (v & ((1u << kLocalBits) - 1u)), v >> kLocalBits);
     }
-    __syncthreads();
-    const uint64_t g0 = (uint64_t)b << kBucketShift;
-    for (uint32_t j = threadIdx.x; j < kBucketRange; j += kFoldThreads) {
-      const uint32_t c = sc[j];
-      if (c && g0 + j < d) counts[g0 + j] += (CT)c;
-    }
-    __syncthreads();
   }
 }
 
@@ -188,24 +240,39 @@ int histogram_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64_t n
   // reductions (C4 histogram 6.96 -> 9.11 ms, C2 index 17.4 -> 25.5 ms)
   // because the bucket cursors become the contended addresses.  Kept,
   // parity-tested, for the CTA-staged variant planned next.
+  // Stage the cold updates by key range when the counters overflow half of L2
+  // -- opt-in (skx_set_histogram_mode(1)): the staging removes the HBM
+  // read-modify-writes (C2 index: 40 -> 7 GB of DRAM traffic in the counting
+  // kernel) but its per-tile partition work makes the kernel instruction-bound
+  // and the L2-resident fold is reduction-rate bound, so the sum is slower
+  // than direct reductions as measured (C4 6.86 -> 10.0 ms, C2 index
+  // 17.6 -> 20.9 ms; profiles/r1_experiments.md).
   const bool bucketed = ctx->hist_bucketed && (uint64_t)d * sizeof(CT) > ctx->l2_bytes / 2 &&
                         n >= (uint64_t(1) << 20);
-  Buckets bk{nullptr, nullptr, 0};
-  uint32_t nb = 0;
+  Buckets bk{nullptr, nullptr, 0, 0};
   if (bucketed) {
-    nb = (uint32_t)(((uint64_t)d + kBucketRange - 1) >> kBucketShift);
-    bk.cap = n / nb + 4096;
-    char* sp = static_cast<char*>(scratch(ctx, 0, (uint64_t)nb * bk.cap * 4 + (uint64_t)nb * 4 + 256));
+    uint32_t shift = 0;
+    while (((uint64_t)d + (uint64_t(1) << shift) - 1) >> shift > (uint64_t)kNB) ++shift;
+    bk.shift = shift;
+    // the fair share of all rows (overflow -> direct reductions); a multiple
+    // of 4 so full 8-entry flushes can use 16-byte stores
+    bk.cap = (n / kNB + 65536 + 3) & ~uint64_t(3);
+    if (bk.cap > 0xFFFFFFFCull) bk.cap = 0xFFFFFFFCull;
+    char* sp = static_cast<char*>(scratch(ctx, 0, (uint64_t)kNB * bk.cap * 4 + 512));
     if (!sp) return set_error(ctx, SKX_CUDA_ERROR, "histogram: out of device memory for buckets");
     bk.cursors = reinterpret_cast<unsigned int*>(sp);
-    bk.buf = reinterpret_cast<uint32_t*>(sp + (((uint64_t)nb * 4 + 255) & ~uint64_t(255)));
-    cudaError_t e = cudaMemsetAsync(bk.cursors, 0, (size_t)nb * 4, s);
+    bk.buf = reinterpret_cast<uint32_t*>(sp + 512);
+    cudaError_t e = cudaMemsetAsync(bk.cursors, 0, kNB * 4, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "histogram memset");
-    cudaFuncSetAttribute(k_histogram<CT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_histogram<CT, true><<<grid, kThreads, smem, s>>>(fact, head, nvec, n, d, counts, bk, ctx->err);
-    const size_t fsmem = (size_t)kBucketRange * 4;
-    cudaFuncSetAttribute(k_hist_fold<CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
-    k_hist_fold<CT><<<grid_for(ctx, nb, 1, 1), kFoldThreads, fsmem, s>>>(bk, nb, d, counts);
+    const size_t bsmem = smem + (size_t)kTileRows * 8 + (1 + 2 * kNB) * 4;
+    cudaFuncSetAttribute(k_histogram<CT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)bsmem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_histogram<CT, true>, kThreads, bsmem);
+    const unsigned bgrid = grid_for(ctx, nvec ? nvec : 1, kThreads * kUnroll, per_sm < 1 ? 1 : per_sm);
+    k_histogram<CT, true><<<bgrid, kThreads, bsmem, s>>>(fact, head, nvec, n, d, counts, bk,
+                                                         ctx->err);
+    k_hist_fold<CT><<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(bk, counts);
     ctx->launches += 2;
   } else {
     cudaFuncSetAttribute(k_histogram<CT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

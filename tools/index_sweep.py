@@ -16,8 +16,11 @@ p.add_argument("--z", type=float, default=1.25)
 p.add_argument("--rows", type=int, default=1 << 30)
 p.add_argument("--domain", type=int, default=1 << 26)
 p.add_argument("--reps", type=int, default=3)
+p.add_argument("--hist-mode", type=int, default=-1, help="skx_set_histogram_mode (-1: default)")
 a = p.parse_args()
 ctx = sx.context(0)
+if a.hist_mode >= 0:
+    ctx.check(ctx.lib.skx_set_histogram_mode(ctx.handle, a.hist_mode))
 d, n = a.domain, a.rows
 fact = dsm.make_rand_fact(d, n, a.z, 42, dsm.shard_of(n))
 dim_i = dsm.fill_column(0, torch.int32, d, 1)
@@ -50,4 +53,4 @@ alg = n * 12 + d * 28
 out["alg_bytes"] = alg
 out["frac_total"] = round(alg / (out["total"] * 1e-3) / 6545.3e9, 4)
 out["rows_per_s"] = n / (out["total"] * 1e-3)
-print(json.dumps({"z": a.z, "domain": d, "rows": n, **out}))
+print(json.dumps({"z": a.z, "domain": d, "rows": n, "hist_mode": a.hist_mode, **out}))

@@ -71,6 +71,17 @@ __device__ __forceinline__ uint64_t ld_cv(const uint64_t* p) {
   asm volatile("ld.global.cv.u64 %0, [%1];" : "=l"(v) : "l"(p));
   return v;
 }
+__device__ __forceinline__ uint64_t ld_cas(const uint64_t* p) {
+  uint64_t v;
+  const uint64_t x = 0x5a5a5a5a5a5a5a5aull;  // cas(p, x, x): never changes memory
+  asm volatile("atom.global.cas.b64 %0, [%1], %2, %2;" : "=l"(v) : "l"(p), "l"(x) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_orz(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("atom.global.or.b64 %0, [%1], 0;" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ uint64_t ld_lu(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.global.lu.u64 %0, [%1];" : "=l"(v) : "l"(p));
@@ -206,6 +217,9 @@ k_l2(const uint32_t* __restrict__ fk, uint64_t n, const uint64_t* __restrict__ d
       if (H == 15) v[u] = hot ? 0ull : ld_cg(p);
       if (H == 16) v[u] = hot ? 0ull : ld_na(p);
       if (H == 17) v[u] = hot ? 0ull : ld_ca(p);
+      if (H == 40) v[u] = hot ? ld_plain(p) : ld_cas(p);
+      if (H == 41) v[u] = hot ? ld_plain(p) : ld_orz(p);
+      if (H == 42) v[u] = hot ? 0ull : ld_cas(p);
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
@@ -213,6 +227,51 @@ k_l2(const uint32_t* __restrict__ fk, uint64_t n, const uint64_t* __restrict__ d
       if (row < n) __stcs(reinterpret_cast<unsigned long long*>(out + row), v[u]);
     }
   }
+}
+
+// H=30: plain dimension loads; outputs staged per warp in shared memory and
+// written with 256-byte TMA bulk stores (cp.async.bulk.global.shared::cta).
+__global__ void __launch_bounds__(kT, 2)
+k_tma_store(const uint32_t* __restrict__ fk, uint64_t n, const uint64_t* __restrict__ dim,
+            uint64_t* __restrict__ out) {
+  __shared__ __align__(128) uint64_t stage[kT / 32][kU][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t span = (uint64_t)gridDim.x * kT * kU;
+  for (uint64_t base = (uint64_t)blockIdx.x * kT * kU; base < n; base += span) {
+    uint32_t r[kU];
+    uint64_t v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      uint64_t row = base + (uint64_t)u * kT + threadIdx.x;
+      r[u] = row < n ? __ldcs(fk + row) - 1u : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) v[u] = ld_plain(dim + r[u]);
+    // previous bulk stores must have finished reading the staging buffer
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < kU; ++u) stage[w][u][lane] = v[u];
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      const bool full = base + (uint64_t)kU * kT <= n;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint64_t row0 = base + (uint64_t)u * kT + (uint64_t)w * 32;
+        if (full) {
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 256;" ::"l"(out + row0),
+                       "r"((uint32_t)__cvta_generic_to_shared(&stage[w][u][0]))
+                       : "memory");
+        } else {
+          for (int l = 0; l < 32; ++l)
+            if (row0 + l < n) out[row0 + l] = stage[w][u][l];
+        }
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 template <int H>
@@ -233,6 +292,7 @@ static int launch(int grid, uint64_t win_bytes, float hit_ratio, const uint32_t*
     cfg.attrs = at;
     cfg.numAttrs = 1;
   }
+  if (H == 30) return (int)cudaLaunchKernelEx(&cfg, k_tma_store, fk, n, dim, out);
   if (H >= 18) {
     cfg.dynamicSmemBytes = (size_t)kT * kU * 16;
     cudaFuncSetAttribute(k_async<H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -268,6 +328,10 @@ extern "C" int probe_l2(int h, int grid, uint64_t win_bytes, float hit_ratio, ui
     case 18: return launch<18>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
     case 19: return launch<19>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
     case 20: return launch<20>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
+    case 30: return launch<30>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
+    case 40: return launch<40>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
+    case 41: return launch<41>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
+    case 42: return launch<42>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
   }
   return -1;
 }

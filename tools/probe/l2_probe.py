@@ -72,6 +72,14 @@ if MODE == "tma":
     for K in (256 * 1024, 1 * MB, 4 * MB, 16 * MB):
         for h in (0, 18, 19, 20, 10):
             cfgs.append((h, K, 0, 0, 1.0, 592))
+if MODE == "atom":
+    for K in (1 * MB, 4 * MB, 16 * MB):
+        for h in (0, 40, 41, 10, 42):
+            cfgs.append((h, K, 0, 0, 1.0, 592))
+if MODE == "tmastore":
+    for grid in (296, 444, 592):
+        cfgs.append((0, 0, 0, 0, 1.0, grid))
+        cfgs.append((30, 0, 0, 0, 1.0, grid))
 gran = int(os.environ.get("PROBE_GRAN", "0"))
 if gran:
     assert lib.probe_set_granularity(gran) == 0
