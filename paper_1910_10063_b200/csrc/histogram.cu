@@ -5,11 +5,11 @@
 //
 // B200 design.  Before the reorder the hot
 // keys are scattered ids (a Zipf(1.25) key alone is ~22% of all rows), so:
-//  1. lanes of a warp holding equal keys merge with __match_any_sync (one
-//     update per distinct key per warp instruction);
-//  2. the leader adds the group size to a per-CTA shared-memory
-//     open-addressing table (key -> count) that captures the keys the CTA
-//     sees first -- for skewed data the hot ones -- claiming slots with CAS;
+//  1. every lane adds 1 to a per-CTA shared-memory open-addressing table
+//     (key -> count) that captures the keys the CTA sees first -- for skewed
+//     data the hot ones -- claiming slots with CAS; same-key lanes of a warp
+//     are merged by the shared-memory atomic unit itself (a __match_any_sync
+//     pre-aggregation was measured 2.4x slower at C4);
 //  3. a key that finds no slot within kProbe probes is cold: for small
 //     domains (counters L2-resident) it is a global red.add; for large ones
 //     (counters >> L2) the CTA collects the cold (key, count) pairs of each
@@ -73,10 +73,11 @@ template <typename CT, bool BK>
 __device__ __forceinline__ void count_one(uint32_t id, bool valid, uint32_t* keys, uint32_t* cnts,
                                           CT* counts, const TileCold& tc) {
   const uint32_t key = valid ? id : 0u;
-  const uint32_t peers = __match_any_sync(0xffffffffu, key);
-  const uint32_t lane = threadIdx.x & 31;
-  const bool leader = key != 0u && lane == (uint32_t)(__ffs(peers) - 1);
-  const uint32_t c = __popc(peers);
+  // Every lane updates on its own: same-address 32-bit shared adds from one
+  // warp merge in hardware, so warp pre-aggregation with __match_any_sync
+  // only adds latency (C4 histogram 6.86 -> 2.88 ms without it).
+  const bool leader = key != 0u;
+  const uint32_t c = 1u;
   bool cold = false;
   if (leader) {
     uint32_t h = slot_hash(key);
