@@ -206,6 +206,7 @@ __global__ void __launch_bounds__(kTileThreads)
       const uint64_t p = base + w * (kItems * 32) + i * 32 + lane;
       const bool valid = p < nnz;
       const uint32_t dg = valid ? (uint32_t)((keys[p] >> shift) & 0xFF) : 256u;
+      // (per-lane shared atomics instead: measured slower, C4 sort 1.18 -> 1.21 ms)
       const uint32_t peers = __match_any_sync(0xffffffffu, dg);
       if (valid && lane == __ffs(peers) - 1) wcnt[w][dg] += __popc(peers);
     }
@@ -247,6 +248,8 @@ __global__ void __launch_bounds__(kTileThreads)
     const uint64_t p = base + w * (kItems * 32) + i * 32 + lane;
     const bool valid = p < nnz;
     const uint32_t dg = valid ? (uint32_t)((key[i] >> shift) & 0xFF) : 256u;
+    // (8 ballots, one per digit bit, instead of __match_any_sync: measured
+    // slower on B200, C4 sort 1.18 -> 1.50 ms)
     const uint32_t peers = __match_any_sync(0xffffffffu, dg);
     const uint32_t cur = valid ? wcnt[w][dg] : 0u;
     rank[i] = cur + __popc(peers & lt);
