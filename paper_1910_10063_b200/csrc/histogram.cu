@@ -27,8 +27,17 @@
 namespace skx {
 namespace {
 
-constexpr int kThreads = 512;
-constexpr int kTableBits = 13;  // 8192 slots x 8 B = 64 KB per CTA
+#ifndef SKX_HIST_THREADS
+#define SKX_HIST_THREADS 512
+#endif
+#ifndef SKX_HIST_TBITS
+#define SKX_HIST_TBITS 13
+#endif
+#ifndef SKX_HIST_CTAS
+#define SKX_HIST_CTAS 3
+#endif
+constexpr int kThreads = SKX_HIST_THREADS;
+constexpr int kTableBits = SKX_HIST_TBITS;  // default 8192 slots x 8 B = 64 KB per CTA
 constexpr int kTable = 1 << kTableBits;
 constexpr int kProbe = 4;
 constexpr int kUnroll = 2;        // uint4 per thread per iteration
@@ -233,7 +242,7 @@ __global__ void __launch_bounds__(256)
 template <typename CT>
 int histogram_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64_t nvec, uint64_t n,
                    uint32_t d, CT* counts, cudaStream_t s) {
-  const unsigned grid = grid_for(ctx, nvec ? nvec : 1, kThreads * kUnroll, 3);
+  const unsigned grid = grid_for(ctx, nvec ? nvec : 1, kThreads * kUnroll, SKX_HIST_CTAS);
   const size_t smem = size_t(2) * kTable * sizeof(uint32_t);
   // Bucket the cold updates only when the counters overflow half of L2 --
   // and only when enabled: measured on B200 (profiles/r1_experiments.md) the
