@@ -118,14 +118,28 @@ struct Tail {
   uint32_t wshift;              // bucket = (idx - hot) >> wshift
 };
 
+#ifndef SKX_AGG_BIN_BYTES
+#define SKX_AGG_BIN_BYTES 8
+#endif
+constexpr int kBinBytes = SKX_AGG_BIN_BYTES;  // 8: {count, sum lo}; 12: + sum hi
+
+// Hot row: 32-bit shared count and sum-lo adds; the bits above 32 (the
+// measure's high word plus the lo word's carry, decided from the returned
+// old value) go straight to the key's global sum when they occur (8-byte
+// bins) or to a third shared word (12-byte bins).
 __device__ __forceinline__ void hot_add(const HotBins& b, uint32_t idx, unsigned long long m,
-                                        bool with_sum) {
+                                        bool with_sum, unsigned long long* gpairs) {
   atomicAdd(&b.cnt[idx], 1u);
   if (with_sum) {
     const uint32_t ml = (uint32_t)m;
     const uint32_t old = atomicAdd(&b.lo[idx], ml);
     const uint32_t hi_add = (uint32_t)(m >> 32) + ((uint32_t)(old + ml) < old ? 1u : 0u);
-    if (hi_add) atomicAdd(&b.hi[idx], hi_add);
+    if (hi_add) {
+      if (kBinBytes == 8)
+        atomicAdd(&gpairs[2 * (uint64_t)idx + 1], (unsigned long long)hi_add << 32);
+      else
+        atomicAdd(&b.hi[idx], hi_add);
+    }
   }
 }
 
@@ -147,7 +161,7 @@ __device__ __forceinline__ void agg_row(uint32_t idx, unsigned long long m, uint
                                         uint32_t limit, const HotBins& b, const Tail& t,
                                         PackTally& pt) {
   if (idx < hot) {
-    hot_add(b, idx, m, MW != 0);
+    hot_add(b, idx, m, MW != 0, t.pairs);
   } else if (idx < limit) {
     if (!MW) {
       atomicAdd(&t.pairs[idx], 1ull);
@@ -174,12 +188,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (gate && agg_ok(gate)) return;
   extern __shared__ uint32_t smem_agg[];
   PackTally pt;
-  HotBins b{smem_agg, smem_agg + hot, smem_agg + 2 * (size_t)hot};  // lo/hi only if MW
+  HotBins b{smem_agg, smem_agg + hot, smem_agg + 2 * (size_t)hot};  // lo (hi) only if MW
   for (uint32_t i = threadIdx.x; i < hot; i += kThreads) {
     b.cnt[i] = 0u;
     if (MW) {
       b.lo[i] = 0u;
-      b.hi[i] = 0u;
+      if (kBinBytes == 12) b.hi[i] = 0u;
     }
   }
   __syncthreads();
@@ -253,7 +267,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (c) {
       if (MW) {
         atomicAdd(&t.pairs[2 * (uint64_t)i], c);
-        atomicAdd(&t.pairs[2 * (uint64_t)i + 1], ((unsigned long long)b.hi[i] << 32) | b.lo[i]);
+        atomicAdd(&t.pairs[2 * (uint64_t)i + 1],
+                  ((unsigned long long)(kBinBytes == 12 ? b.hi[i] : 0u) << 32) | b.lo[i]);
       } else {
         atomicAdd(&t.pairs[i], c);
       }
@@ -278,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (uint32_t i = threadIdx.x; i < hot; i += kThreads) {
     b.cnt[i] = 0u;
     b.lo[i] = 0u;
-    b.hi[i] = 0u;
+    if (kBinBytes == 12) b.hi[i] = 0u;
   }
   const uint64_t pol = policy_evict_first();
   const uint4* fv = reinterpret_cast<const uint4*>(fact + head);
@@ -306,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (idx >= d) {
         record_violation(err, head + vi * 4 + j, ids[j]);
       } else if (idx < hot) {
-        hot_add(b, idx, m[j], true);
+        hot_add(b, idx, m[j], true, t.pairs);
       } else {
         bk[j] = (idx - hot) >> t.wshift;
         slot[j] = atomicAdd(&s_cnt[bk[j]], 1u);
@@ -350,7 +365,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const unsigned long long c = b.cnt[i];
     if (c) {
       atomicAdd(&t.pairs[2 * (uint64_t)i], c);
-      atomicAdd(&t.pairs[2 * (uint64_t)i + 1], ((unsigned long long)b.hi[i] << 32) | b.lo[i]);
+      atomicAdd(&t.pairs[2 * (uint64_t)i + 1],
+                ((unsigned long long)(kBinBytes == 12 ? b.hi[i] : 0u) << 32) | b.lo[i]);
     }
   }
 }
@@ -432,7 +448,7 @@ __global__ void __launch_bounds__(256)
 }
 
 uint32_t hot_keys(const skx_ctx* ctx, int mw, uint32_t hot_req, uint32_t limit) {
-  const size_t per_key = mw ? 12 : 4;
+  const size_t per_key = mw ? kBinBytes : 4;
   const size_t budget = ctx->smem_optin > 2048 ? ctx->smem_optin - 2048 : 0;
   uint32_t hot = (uint32_t)(budget / per_key);
   if (hot_req && hot_req < hot) hot = hot_req;
@@ -456,7 +472,7 @@ int aggregate_impl(skx_ctx* ctx, const uint32_t* fact, const void* measure, uint
   if (n / grid + 4 * (uint64_t)kThreads >= (uint64_t(1) << 32))
     return set_error(ctx, SKX_INVALID_ARGUMENT, "aggregate: too many rows per call");
   const uint32_t hot = hot_keys(ctx, MW, hot_req, limit);
-  const size_t smem = (size_t)hot * (MW ? 12 : 4);
+  const size_t smem = (size_t)hot * (MW ? kBinBytes : 4);
   // Stage the cold tail when its pairs overflow half of L2 (MW != 0 only).
   const uint64_t tail_keys = limit > hot ? limit - hot : 0;
   if (MW && !PACK && !gate && limit == d && ctx->agg_mode == 1 &&

@@ -8,6 +8,6 @@ for v in "$@"; do
   if [ "$v" = orig ]; then cp /tmp/ab_orig.so paper_1910_10063_b200/libskx.so
   else cp "tools/variants/libskx_$v.so" paper_1910_10063_b200/libskx.so; fi
   echo "== $v"
-  timeout 300 bash -c "$cmd" 2>&1 | tail -2
+  timeout 300 bash -c "$cmd" 2>&1 | tail -${AB_TAIL:-2}
 done
 cp /tmp/ab_orig.so paper_1910_10063_b200/libskx.so
