@@ -82,6 +82,16 @@ __device__ __forceinline__ uint64_t ld_orz(const uint64_t* p) {
   asm volatile("atom.global.or.b64 %0, [%1], 0;" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint64_t ld_p64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.global.nc.L2::64B.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_p128(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.global.nc.L2::128B.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ uint64_t ld_lu(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.global.lu.u64 %0, [%1];" : "=l"(v) : "l"(p));
@@ -218,6 +228,10 @@ k_l2(const uint32_t* __restrict__ fk, uint64_t n, const uint64_t* __restrict__ d
       if (H == 16) v[u] = hot ? 0ull : ld_na(p);
       if (H == 17) v[u] = hot ? 0ull : ld_ca(p);
       if (H == 40) v[u] = hot ? ld_plain(p) : ld_cas(p);
+      if (H == 50) v[u] = hot ? ld_plain(p) : ld_p64(p);
+      if (H == 51) v[u] = ld_p64(p);
+      if (H == 52) v[u] = hot ? 0ull : ld_p64(p);
+      if (H == 53) v[u] = hot ? 0ull : ld_p128(p);
       if (H == 41) v[u] = hot ? ld_plain(p) : ld_orz(p);
       if (H == 42) v[u] = hot ? 0ull : ld_cas(p);
     }
@@ -293,7 +307,7 @@ static int launch(int grid, uint64_t win_bytes, float hit_ratio, const uint32_t*
     cfg.numAttrs = 1;
   }
   if (H == 30) return (int)cudaLaunchKernelEx(&cfg, k_tma_store, fk, n, dim, out);
-  if (H >= 18) {
+  if (H >= 18 && H <= 20) {
     cfg.dynamicSmemBytes = (size_t)kT * kU * 16;
     cudaFuncSetAttribute(k_async<H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)cfg.dynamicSmemBytes);
@@ -330,6 +344,10 @@ extern "C" int probe_l2(int h, int grid, uint64_t win_bytes, float hit_ratio, ui
     case 20: return launch<20>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
     case 30: return launch<30>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
     case 40: return launch<40>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
+    case 50: return launch<50>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
+    case 51: return launch<51>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
+    case 52: return launch<52>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
+    case 53: return launch<53>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
     case 41: return launch<41>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
     case 42: return launch<42>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
   }
