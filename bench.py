@@ -179,6 +179,98 @@ def cpu_gather_baseline(fact_np, dim_np, steps=3):
                 "reference_note": f"oracle/_ref unavailable: {e}"}
 
 
+def _cpu_extra(fn):
+    """CPU reference timings beside the C3/C4/C5 lines: never fatal."""
+    try:
+        return fn()
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": f"{type(e).__name__}: {e}"}
+
+
+def cpu_groupby_reference(fact_np, qty_np, d):
+    """C3 on the host: the reference's parallel_aggregate (hybrid, h=8192, all
+    threads; COUNT only -- parallel.cpp:131-216) on a 2^26-row sample and its
+    single-thread aggregate_sum (operators.cpp:107-118, the reference has no
+    parallel SUM) on a 2^24-row sample, both of the recoded C3 FK column."""
+    import ctypes as C
+
+    import numpy as np
+    from oracle.oracle import Reference
+    ref = Reference()
+    threads = os.cpu_count() or 1
+    f = np.ascontiguousarray(fact_np[:1 << 26])
+    ns = ref.L.ref_time_parallel_aggregate(f.ctypes.data_as(C.c_void_p), len(f), d, threads, 2,
+                                           8192, 3)
+    f2 = np.ascontiguousarray(fact_np[:1 << 24])
+    q2 = np.ascontiguousarray(qty_np[:1 << 24].astype(np.uint32))  # 1..100 fits u32
+    ns2 = ref.L.ref_time_aggregate_sum(f2.ctypes.data_as(C.c_void_p), q2.ctypes.data_as(C.c_void_p),
+                                       len(f2), d, 1)
+    return {"parallel_aggregate_count_rows_per_s": len(f) / (ns * 1e-9), "threads": threads,
+            "aggregate_sum_1thread_rows_per_s": len(f2) / (ns2 * 1e-9), "kind": "reference",
+            "sample": f"{len(f)} / {len(f2)} rows of the recoded C3 FK column (D={d})",
+            "heavy_hitters": cpu_heavy_hitters_reference(f, d)}
+
+
+def cpu_heavy_hitters_reference(fact_np, d, k=8192):
+    """Q3a on the host: the reference's heavy_hitter_count (operators.cpp:184-203,
+    single thread) on a 2^26-row sample of the recoded C3 column."""
+    import ctypes as C
+
+    import numpy as np
+    from oracle.oracle import Reference
+    ref = Reference()
+    f = np.ascontiguousarray(fact_np)
+    ids = np.empty(k, np.uint32)
+    cnt = np.empty(k, np.uint64)
+    ln = C.c_uint64(0)
+    cl = C.c_int(0)
+    ts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        ref.L.ref_heavy_hitter_count(f.ctypes.data_as(C.c_void_p), len(f), d, k,
+                                     ids.ctypes.data_as(C.c_void_p), cnt.ctypes.data_as(C.c_void_p),
+                                     C.byref(ln), C.byref(cl))
+        ts.append(time.perf_counter() - t0)
+    return {"heavy_hitter_count_1thread_rows_per_s": len(f) / statistics.median(ts[1:]),
+            "kind": "reference", "sample": f"{len(f)} rows, k={k}, D={d}"}
+
+
+def cpu_rebuild_reference(fact_np, d):
+    """C4 on the host: the reference's rebuild (count_frequencies + build_index,
+    single thread -- the reference has no parallel index build) at the
+    CPU-runnable scale of BASELINE configs[0] (D=2^22, 2^24 rows)."""
+    import ctypes as C
+
+    import numpy as np
+    from oracle.oracle import Reference
+    ref = Reference()
+    f = np.ascontiguousarray(fact_np)
+    ns = ref.L.ref_time_rebuild(f.ctypes.data_as(C.c_void_p), len(f), d, 1)
+    return {"rebuild_1thread_ms": ns * 1e-6, "rows_per_s": len(f) / (ns * 1e-9), "kind": "reference",
+            "sample": f"{len(f)} Zipf(1.25) rows over D={d} (configs[0] scale)"}
+
+
+def cpu_select_reference(fact_np, words_np, bits):
+    """C5 selection on the host: the reference's parallel_select
+    (parallel.cpp:102-129, all threads) with the same permuted bitmap on a
+    2^26-row sample of the recoded FK column."""
+    import ctypes as C
+
+    import numpy as np
+    from oracle.oracle import Reference
+    ref = Reference()
+    threads = os.cpu_count() or 1
+    f = np.ascontiguousarray(fact_np)
+    w = np.ascontiguousarray(words_np)
+    sel = C.c_uint64(0)
+    ns = ref.L.ref_time_parallel_select(f.ctypes.data_as(C.c_void_p), len(f),
+                                        w.ctypes.data_as(C.c_void_p), bits, threads, 3,
+                                        C.byref(sel))
+    return {"parallel_select_rows_per_s": len(f) / (ns * 1e-9), "threads": threads,
+            "selected": int(sel.value), "kind": "reference",
+            "sample": f"{len(f)} rows of the recoded C5 FK column, permuted bitmap over D={bits}"}
+
+
 def run_reference_arm(args):
     """--impl reference: the reference's CPU gather on a bounded sample of the
     same workload, all host threads, K timed steps after W warm-ups."""
@@ -429,6 +521,28 @@ def run_ours(args):
                                 "frac": gb_bytes / (statistics.mean(per_g) * 1e-3) / 1e9 / peak,
                                 "traffic": ncu_traffic("groupby_c3"),
                                 "alg_bytes_per_step": gb_bytes}}
+        # Q3a heavy hitters: counts of the k = 8192 hottest ids of
+        # the recoded C3 column -- the device part of heavy_hitter_count
+        # (operators.cpp:184-203); the top-k ordering of k pairs is host work.
+        hh = torch.empty(8192, dtype=torch.uint64, device="cuda")
+
+        def step_hh():
+            ctx.call("skx_heavy_hitter_count", C_ptr(gdat.fact_freq), rows_local, D_C3, 8192,
+                     C_ptr(hh), ctx.stream(), sync=False)
+            if dist_on:
+                dist.reduce(hh.view(torch.int64), dst=0)
+        th, per_h, _ = timed_launches(step_hh, args.steps, args.warmup, stream, dist_on)
+        ctx.sync()
+        th = max_over_ranks(th, dist_on)
+        hb = rows_local * 4 + 8192 * 8
+        groupby["heavy_hitters_k8192"] = {
+            "value": rows_local * world * args.steps / (th * 1e-3), "unit": "rows/s",
+            "ms_per_step": th / args.steps,
+            "roofline_frac": hb / (statistics.mean(per_h) * 1e-3) / 1e9 / peak}
+        del hh
+        if rank == 0 and world == 1 and not args.no_cpu:
+            groupby["cpu_reference"] = _cpu_extra(lambda: cpu_groupby_reference(
+                gdat.fact_freq[:1 << 26].cpu().numpy(), gdat.qty[:1 << 24].cpu().numpy(), D_C3))
         del gdat, counts, sums
         torch.cuda.empty_cache()
         extras.update(other_configs(args, ctx, stream, dist_on, rank, world, peak))
@@ -447,6 +561,7 @@ def run_ours(args):
                        "gather_policy": args.policy},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
+                         "frac_vs_nominal_8000": achieved / 8000.0,
                          "traffic": ncu_traffic("gather_c2"),
                          "alg_bytes_per_launch": alg_bytes,
                          "avg_launch_ms": statistics.mean(per)},
@@ -470,6 +585,7 @@ def other_configs(args, ctx, stream, dist_on, rank, world, peak):
     warm-ups, K launches between barriers, CUDA events, max over ranks):
     C1 small gather (both layouts), C4 index build at scale, C5 select +
     4-column gather + per-category fp64 SUM."""
+    import numpy as np
     import torch
 
     from paper_1910_10063_b200 import dataset as ds_mod
@@ -524,6 +640,11 @@ def other_configs(args, ctx, stream, dist_on, rank, world, peak):
                                      "float32 dims; warm"}
     del fact, dim_i, dim_f, counts, ff
     torch.cuda.empty_cache()
+    if rank == 0 and world == 1 and not args.no_cpu:
+        small = ds_mod.make_rand_fact(1 << 22, 1 << 24, 1.25, SEED + 9, ds_mod.shard_of(1 << 24))
+        out["index_build_c4"]["cpu_reference"] = _cpu_extra(
+            lambda: cpu_rebuild_reference(small.cpu().numpy(), 1 << 22))
+        del small
 
     # C5: 2^31 rows (per GPU), D=2^25, category < 100, 4-column gather + fp64 SUM(price).
     d5, n5 = 1 << 25, 1 << 31
@@ -564,6 +685,10 @@ def other_configs(args, ctx, stream, dist_on, rank, world, peak):
                         "ms_per_step": t5 / k, "selected": sel, "selectivity": sel / n5,
                         "roofline_frac": alg5 / (statistics.mean(per5) * 1e-3) / 1e9 / peak,
                         "alg_bytes_per_step": alg5}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        out["select_c5"]["cpu_reference"] = _cpu_extra(lambda: cpu_select_reference(
+            fact_f[:1 << 26].cpu().numpy(), bm.words.view(torch.int64).cpu().numpy().view(np.uint64),
+            d5))
     del fact_f, cat, prc, sup, flg, bm, bufs, sums, cnt, idx
     torch.cuda.empty_cache()
     return out

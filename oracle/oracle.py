@@ -314,6 +314,10 @@ class Reference:
         L.ref_time_parallel_materialize.argtypes = [vp, u64, vp, u64, C.c_uint, ci]
         L.ref_time_gather_kernel.restype = dbl
         L.ref_time_gather_kernel.argtypes = [vp, u64, vp, vp, C.c_uint, ci]
+        L.ref_time_parallel_select.restype = dbl
+        L.ref_time_parallel_select.argtypes = [vp, u64, vp, u64, C.c_uint, ci, vp]
+        L.ref_time_aggregate_sum.restype = dbl
+        L.ref_time_aggregate_sum.argtypes = [vp, vp, u64, u32, ci]
         L.ref_time_parallel_aggregate.restype = dbl
         L.ref_time_parallel_aggregate.argtypes = [vp, u64, u32, C.c_uint, ci, u32, ci]
         L.ref_time_rebuild.restype = dbl

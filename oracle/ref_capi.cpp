@@ -334,6 +334,41 @@ double ref_time_rebuild(const std::uint32_t* fact, std::uint64_t n, std::uint32_
   return median(t);
 }
 
+// parallel_select (parallel.cpp:102-129) with the reference's own output
+// vectors; median ns over reps after one warm-up.
+double ref_time_parallel_select(const std::uint32_t* fact, std::uint64_t n,
+                                const std::uint64_t* words, std::uint64_t bits, unsigned threads,
+                                int reps, std::uint64_t* selected) {
+  const Column f = to_col(fact, n);
+  const Bitmap bm = to_bitmap(words, bits);
+  ParallelPlan plan;
+  plan.threads = threads;
+  std::vector<double> t;
+  for (int r = 0; r <= reps; ++r) {
+    const double t0 = now_ns();
+    const auto out = parallel_select(f, bm, plan);
+    const double t1 = now_ns();
+    if (selected) *selected = out.size();
+    if (r > 0) t.push_back(t1 - t0);
+  }
+  return median(t);
+}
+
+// aggregate_sum (operators.cpp:107-118, single thread: the reference has no
+// parallel SUM); median ns over reps after one warm-up.
+double ref_time_aggregate_sum(const std::uint32_t* fact, const std::uint32_t* measure,
+                              std::uint64_t n, std::uint32_t d, int reps) {
+  const Column f = to_col(fact, n), m = to_col(measure, n);
+  std::vector<double> t;
+  for (int r = 0; r <= reps; ++r) {
+    const double t0 = now_ns();
+    const auto out = aggregate_sum(f, m, d);
+    const double t1 = now_ns();
+    if (r > 0) t.push_back(t1 - t0);
+  }
+  return median(t);
+}
+
 const char* ref_active_kernels_name() { return kernels::active_kernels().name; }
 
 }  // extern "C"
