@@ -199,16 +199,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   const uint64_t pol = policy_evict_first();
   const uint4* fv = reinterpret_cast<const uint4*>(fact + head);
-  // kAggUnroll vectors of 4 rows per thread per iteration: all loads first
+  constexpr int U = MW ? kAggUnroll : 2 * kAggUnroll;
+  // U vectors of 4 rows per thread per iteration (COUNT-only: twice as many,
+  // it streams 4 B/row): all loads first
   // (more bytes in flight per SM), then the updates.
-  const uint64_t stride = (uint64_t)gridDim.x * kThreads * kAggUnroll;
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads * U;
   // Block-uniform trip count: the warp collectives below need every lane.
-  for (uint64_t vb0 = (uint64_t)blockIdx.x * kThreads * kAggUnroll; vb0 < nvec; vb0 += stride) {
+  for (uint64_t vb0 = (uint64_t)blockIdx.x * kThreads * U; vb0 < nvec; vb0 += stride) {
     const uint64_t vb = vb0 + threadIdx.x;
-    uint4 f[kAggUnroll];
-    unsigned long long m[kAggUnroll][4];
+    uint4 f[U];
+    unsigned long long m[U][4];
 #pragma unroll
-    for (int u = 0; u < kAggUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       const uint64_t vi = vb + (uint64_t)u * kThreads;
       if (vi < nvec) {
         f[u] = ld_cs_v4(fv + vi);
@@ -216,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
 #pragma unroll
-    for (int u = 0; u < kAggUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       const uint64_t vi = vb + (uint64_t)u * kThreads;
       const bool live = vi < nvec;  // warp-collective below: no early exit
       const uint32_t ids[4] = {f[u].x, f[u].y, f[u].z, f[u].w};
