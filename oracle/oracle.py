@@ -106,6 +106,10 @@ class Oracle:
         L.orc_rolling_checksum_u32.argtypes = [vp, u64]
         L.orc_unordered_checksum_u64.restype = u64
         L.orc_unordered_checksum_u64.argtypes = [vp, u64]
+        L.orc_line_frequencies.argtypes = [vp, u32, C.c_int, u64, u32, vp]
+        L.orc_estimate_hit_rate.argtypes = [vp, u64, u64, vp]
+        L.orc_simulate_lru.argtypes = [vp, u64, u64, vp, vp, vp]
+        L.orc_trace_from_column.argtypes = [vp, u64, u32, vp, vp, vp]
 
     # -- generator ------------------------------------------------------------
     def splitmix64(self, x: int) -> int:
@@ -282,6 +286,38 @@ class Oracle:
         v = _u64(v)
         return self.L.orc_unordered_checksum_u64(_p(v), len(v))
 
+    # -- cache model (cachemodel.cpp) ---------------------------------------------
+    def line_frequencies(self, value_freqs, layout, line_bytes, element_bytes, seed):
+        vf = np.ascontiguousarray(value_freqs, dtype=np.float64)
+        per = line_bytes // element_bytes
+        out = np.empty((len(vf) + per - 1) // per, np.float64)
+        if self.L.orc_line_frequencies(_p(vf), len(vf), 0 if layout == "freq" else 1, seed, per,
+                                       _p(out)):
+            raise OracleError(1)
+        return out
+
+    def estimate_hit_rate(self, line_freqs, cache_lines):
+        lf = np.ascontiguousarray(line_freqs, dtype=np.float64)
+        r = C.c_double(0.0)
+        if self.L.orc_estimate_hit_rate(_p(lf), len(lf), cache_lines, C.byref(r)):
+            raise OracleError(1)
+        return r.value
+
+    def simulate_lru(self, trace, cache_lines):
+        t = _u32(trace)
+        a, h, dd = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        if self.L.orc_simulate_lru(_p(t), len(t), cache_lines, C.byref(a), C.byref(h), C.byref(dd)):
+            raise OracleError(1)
+        return a.value, h.value, dd.value
+
+    def trace_from_column(self, fact, line_bytes, element_bytes):
+        fact = _u32(fact)
+        out = np.empty(len(fact), np.uint32)
+        e = _Err()
+        e.check(self.L.orc_trace_from_column(_p(fact), len(fact), line_bytes // element_bytes,
+                                             _p(out), *e.args()))
+        return out
+
 
 class Reference:
     """The unmodified reference library (oracle/_ref/libskewdx_ref.so)."""
@@ -314,6 +350,10 @@ class Reference:
         L.ref_time_parallel_materialize.argtypes = [vp, u64, vp, u64, C.c_uint, ci]
         L.ref_time_gather_kernel.restype = dbl
         L.ref_time_gather_kernel.argtypes = [vp, u64, vp, vp, C.c_uint, ci]
+        L.ref_line_frequencies.argtypes = [vp, u32, ci, u64, u32, u32, vp]
+        L.ref_estimate_hit_rate.argtypes = [vp, u64, u64, vp]
+        L.ref_simulate_lru.argtypes = [vp, u64, u64, vp]
+        L.ref_trace_from_column.argtypes = [vp, u64, u32, u32, vp, vp, vp]
         L.ref_time_parallel_select.restype = dbl
         L.ref_time_parallel_select.argtypes = [vp, u64, vp, u64, C.c_uint, ci, vp]
         L.ref_time_aggregate_sum.restype = dbl
@@ -460,6 +500,37 @@ class Reference:
         if st:
             raise OracleError(st)
         return ids[: ln.value], cnt[: ln.value], bool(cl.value)
+
+    def line_frequencies(self, value_freqs, layout, line_bytes, element_bytes, seed):
+        vf = np.ascontiguousarray(value_freqs, dtype=np.float64)
+        per = line_bytes // element_bytes
+        out = np.empty((len(vf) + per - 1) // per, np.float64)
+        if self.L.ref_line_frequencies(_p(vf), len(vf), 1 if layout == "freq" else 0, seed,
+                                       line_bytes, element_bytes, _p(out)):
+            raise OracleError(1)
+        return out
+
+    def estimate_hit_rate(self, line_freqs, cache_lines):
+        lf = np.ascontiguousarray(line_freqs, dtype=np.float64)
+        r = C.c_double(0.0)
+        if self.L.ref_estimate_hit_rate(_p(lf), len(lf), cache_lines, C.byref(r)):
+            raise OracleError(1)
+        return r.value
+
+    def simulate_lru(self, trace, cache_lines):
+        t = _u32(trace)
+        st = np.zeros(3, np.uint64)
+        if self.L.ref_simulate_lru(_p(t), len(t), cache_lines, _p(st)):
+            raise OracleError(1)
+        return int(st[0]), int(st[1]), int(st[2])
+
+    def trace_from_column(self, fact, line_bytes, element_bytes):
+        fact = _u32(fact)
+        out = np.empty(len(fact), np.uint32)
+        e = _Err()
+        e.check(self.L.ref_trace_from_column(_p(fact), len(fact), line_bytes, element_bytes,
+                                             _p(out), *e.args()))
+        return out
 
     def active_kernels_name(self):
         return self.L.ref_active_kernels_name().decode()

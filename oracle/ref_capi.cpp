@@ -20,6 +20,7 @@
 #include <thread>
 #include <vector>
 
+#include "skewdx/cachemodel.hpp"
 #include "skewdx/column.hpp"
 #include "skewdx/error.hpp"
 #include "skewdx/kernels.hpp"
@@ -367,6 +368,50 @@ double ref_time_aggregate_sum(const std::uint32_t* fact, const std::uint32_t* me
     if (r > 0) t.push_back(t1 - t0);
   }
   return median(t);
+}
+
+// ---- cache model (cachemodel.hpp) ---------------------------------------
+int ref_line_frequencies(const double* vf, std::uint32_t d, int layout_freq, std::uint64_t seed,
+                         std::uint32_t line_bytes, std::uint32_t element_bytes, double* out) {
+  return guarded({nullptr, nullptr}, [&] {
+    CacheGeometry g;
+    g.lines = 1;
+    g.line_bytes = line_bytes;
+    g.element_bytes = element_bytes;
+    const auto f = line_frequencies(std::span<const double>(vf, d),
+                                    layout_freq ? Layout::freq : Layout::rand, g, seed);
+    std::memcpy(out, f.data(), f.size() * sizeof(double));
+  });
+}
+
+int ref_estimate_hit_rate(const double* lf, std::uint64_t nlines, std::uint64_t cache_lines,
+                          double* result) {
+  return guarded({nullptr, nullptr}, [&] {
+    *result = estimate_hit_rate(std::span<const double>(lf, nlines), cache_lines);
+  });
+}
+
+int ref_simulate_lru(const std::uint32_t* trace, std::uint64_t n, std::uint64_t cache_lines,
+                     std::uint64_t* stats) {
+  return guarded({nullptr, nullptr}, [&] {
+    const auto st = simulate_lru(std::span<const std::uint32_t>(trace, n), cache_lines);
+    stats[0] = st.accesses;
+    stats[1] = st.hits;
+    stats[2] = st.distinct_lines;
+  });
+}
+
+int ref_trace_from_column(const std::uint32_t* fact, std::uint64_t n, std::uint32_t line_bytes,
+                          std::uint32_t element_bytes, std::uint32_t* out, std::uint64_t* err_row,
+                          std::uint32_t* err_value) {
+  return guarded({err_row, err_value}, [&] {
+    CacheGeometry g;
+    g.lines = 1;
+    g.line_bytes = line_bytes;
+    g.element_bytes = element_bytes;
+    const auto t = trace_from_column(to_col(fact, n), g);
+    std::memcpy(out, t.data(), t.size() * 4);
+  });
 }
 
 const char* ref_active_kernels_name() { return kernels::active_kernels().name; }

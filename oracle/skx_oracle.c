@@ -487,3 +487,176 @@ void orc_generate_zipf_counter_mt(const double* cdf, uint32_t d, const uint32_t*
   free(jobs);
   free(tids);
 }
+
+/* ---- cache model: proj/src/cachemodel.cpp ------------- */
+
+/* line_frequencies (cachemodel.cpp:22-45): per-line sums of per-rank value
+ * frequencies; freq layout = ranks in place, rand layout = ranks scattered by
+ * random_bijection(d, seed).  Lines accumulate in ascending rank order. */
+int orc_line_frequencies(const double* vf, uint32_t d, int layout, uint64_t seed,
+                         uint32_t per_line, double* out) {
+  if (d == 0 || per_line == 0) return ORC_INVALID;
+  const uint64_t lines = ((uint64_t)d + per_line - 1) / per_line;
+  memset(out, 0, lines * sizeof(double));
+  if (layout == 0) {
+    for (uint32_t r = 0; r < d; ++r) out[r / per_line] += vf[r];
+  } else {
+    uint32_t* map = (uint32_t*)malloc(sizeof(uint32_t) * d);
+    if (!map) return ORC_INVALID;
+    orc_random_bijection(d, seed, map);
+    for (uint32_t r = 0; r < d; ++r) out[(map[r] - 1) / per_line] += vf[r];
+    free(map);
+  }
+  return ORC_OK;
+}
+
+static int cmp_desc(const void* a, const void* b) {
+  const double x = *(const double*)a, y = *(const double*)b;
+  return x < y ? 1 : (x > y ? -1 : 0);
+}
+
+/* Expected distinct lines in k trials that end with a reference to the line
+ * of frequency f (cachemodel.cpp:57-72): lines expected more than once
+ * (n_j = k f_j / (1 - f) > 1, i.e. f_j > (1 - f) / k) contribute one. */
+static double orc_expected_distinct(double k, double f, const double* sorted, uint64_t n,
+                                    const double* prefix) {
+  const double cutoff = (1.0 - f) / k;
+  uint64_t lo = 0, hi = n;  /* first index with sorted[i] <= cutoff */
+  while (lo < hi) {
+    const uint64_t mid = lo + (hi - lo) / 2;
+    if (sorted[mid] > cutoff) lo = mid + 1; else hi = mid;
+  }
+  uint64_t m = lo;
+  double mass = prefix[m];
+  if (f > cutoff) {
+    mass -= f;
+    m -= 1;
+  }
+  return k - (k * mass / (1.0 - f) - (double)m);
+}
+
+/* estimate_hit_rate (cachemodel.cpp:76-123): per line, the smallest horizon K
+ * >= S (doubling, then bisection, capped at 2^40) at which the expected
+ * distinct lines reach the capacity S; hit probability 1 - (1 - f)^K. */
+int orc_estimate_hit_rate(const double* lf, uint64_t nlines, uint64_t cache_lines,
+                          double* result) {
+  if (cache_lines == 0) return ORC_INVALID;
+  double* sorted = (double*)malloc(sizeof(double) * (nlines ? nlines : 1));
+  double* prefix = (double*)malloc(sizeof(double) * (nlines + 1));
+  if (!sorted || !prefix) return ORC_INVALID;
+  memcpy(sorted, lf, nlines * sizeof(double));
+  qsort(sorted, nlines, sizeof(double), cmp_desc);
+  uint64_t n = nlines;
+  while (n > 0 && sorted[n - 1] <= 0.0) --n;
+  if (n <= cache_lines) {
+    *result = 1.0;
+    free(sorted);
+    free(prefix);
+    return ORC_OK;
+  }
+  prefix[0] = 0.0;
+  for (uint64_t i = 0; i < n; ++i) prefix[i + 1] = prefix[i] + sorted[i];
+  const double target = (double)cache_lines;
+  const uint64_t cap = (uint64_t)1 << 40;
+  double total = 0.0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const double f = sorted[i];
+    if (f >= 1.0 - 1e-12) {
+      total += f;
+      continue;
+    }
+    uint64_t hi = cache_lines;
+    double dd = orc_expected_distinct((double)hi, f, sorted, n, prefix);
+    while (dd < target && hi < cap) {
+      hi *= 2;
+      dd = orc_expected_distinct((double)hi, f, sorted, n, prefix);
+    }
+    uint64_t k = hi;
+    if (dd >= target && hi > cache_lines) {
+      uint64_t lo = hi / 2 + 1;
+      while (lo < hi) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if (orc_expected_distinct((double)mid, f, sorted, n, prefix) >= target) hi = mid;
+        else lo = mid + 1;
+      }
+      k = lo;
+    }
+    total += f * -expm1((double)k * log1p(-f));
+  }
+  *result = total < 1.0 ? total : 1.0;
+  free(sorted);
+  free(prefix);
+  return ORC_OK;
+}
+
+/* simulate_lru (cachemodel.cpp:125-173): exact fully associative LRU over a
+ * trace of dense line ids (doubly linked recency list). */
+int orc_simulate_lru(const uint32_t* trace, uint64_t n, uint64_t cache_lines,
+                     uint64_t* accesses, uint64_t* hits, uint64_t* distinct) {
+  if (cache_lines == 0) return ORC_INVALID;
+  *accesses = n;
+  *hits = 0;
+  *distinct = 0;
+  if (n == 0) return ORC_OK;
+  uint32_t mx = 0;
+  for (uint64_t i = 0; i < n; ++i) mx = trace[i] > mx ? trace[i] : mx;
+  const uint64_t u = (uint64_t)mx + 1;
+  const uint32_t nil = 0xFFFFFFFFu;
+  uint32_t* prv = (uint32_t*)malloc(u * 4);
+  uint32_t* nxt = (uint32_t*)malloc(u * 4);
+  uint8_t* res = (uint8_t*)calloc(u, 1);
+  uint8_t* seen = (uint8_t*)calloc(u, 1);
+  if (!prv || !nxt || !res || !seen) return ORC_INVALID;
+  uint32_t head = nil, tail = nil;
+  uint64_t size = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint32_t x = trace[i];
+    if (!seen[x]) {
+      seen[x] = 1;
+      ++*distinct;
+    }
+    if (res[x]) {
+      ++*hits;
+      if (x == head) continue;
+      /* unlink */
+      if (prv[x] != nil) nxt[prv[x]] = nxt[x]; else head = nxt[x];
+      if (nxt[x] != nil) prv[nxt[x]] = prv[x]; else tail = prv[x];
+    } else {
+      res[x] = 1;
+      ++size;
+    }
+    /* push front */
+    prv[x] = nil;
+    nxt[x] = head;
+    if (head != nil) prv[head] = x; else tail = x;
+    head = x;
+    if (size > cache_lines) {
+      const uint32_t v = tail;
+      tail = prv[v];
+      if (tail != nil) nxt[tail] = nil; else head = nil;
+      res[v] = 0;
+      --size;
+    }
+  }
+  free(prv);
+  free(nxt);
+  free(res);
+  free(seen);
+  return ORC_OK;
+}
+
+/* trace_from_column (cachemodel.cpp:175-186): line = (id - 1) / per_line;
+ * id 0 is a DomainViolation at its row. */
+int orc_trace_from_column(const uint32_t* fact, uint64_t n, uint32_t per_line, uint32_t* out,
+                          uint64_t* err_row, uint32_t* err_value) {
+  if (per_line == 0) return ORC_INVALID;
+  for (uint64_t k = 0; k < n; ++k) {
+    if (fact[k] == 0) {
+      if (err_row) *err_row = k;
+      if (err_value) *err_value = 0;
+      return ORC_DOMAIN;
+    }
+    out[k] = (fact[k] - 1) / per_line;
+  }
+  return ORC_OK;
+}
