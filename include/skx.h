@@ -199,6 +199,32 @@ int skx_generate_zipf(skx_ctx* ctx, const double* cdf, uint32_t d, const uint32_
 int skx_fill_column(skx_ctx* ctx, int kind, int width, uint64_t seed, uint64_t n, double p0,
                     double p1, void* out, void* stream);
 
+/* ---- cache model (cachemodel.hpp) ------------------------ *
+ * line_frequencies (cachemodel.cpp:22-45): out[l] = sum of value_freqs[r]
+ * over the ranks r whose element lands in line l, accumulated in ascending
+ * rank order (bit-identical to the reference).  rank_to_id NULL = freq layout
+ * (rank r is element r); else element rank_to_id[r]-1 (the rand layout's
+ * random_bijection, skx_random_bijection_host).  per_line = line_bytes /
+ * element_bytes (1..64 with a bijection).  Device pointers, d doubles in,
+ * ceil(d / per_line) doubles out. */
+int skx_line_frequencies(skx_ctx* ctx, const double* value_freqs, uint32_t d,
+                         const uint32_t* rank_to_id, uint32_t per_line, double* out,
+                         void* stream);
+/* estimate_hit_rate (cachemodel.cpp:76-123): analytical LRU hit rate of an
+ * access stream with independent per-line frequencies, for a cache of
+ * cache_lines lines; *result (device double) written on `stream`.  Matches
+ * the reference to rounding (parallel prefix sums). */
+int skx_estimate_hit_rate(skx_ctx* ctx, const double* line_freqs, uint64_t nlines,
+                          uint64_t cache_lines, double* result, void* stream);
+/* trace_from_column (cachemodel.cpp:175-186): out[k] = (fact[k]-1)/per_line;
+ * an id 0 is a DomainViolation (deferred to skx_sync, domain 0xFFFFFFFE). */
+int skx_trace_from_column(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint32_t per_line,
+                          uint32_t* out, void* stream);
+/* simulate_lru (cachemodel.cpp:125-173), host: exact LRU over a host trace;
+ * stats[0..3) = {accesses, hits, distinct lines}. */
+int skx_simulate_lru_host(const uint32_t* trace, uint64_t n, uint64_t cache_lines,
+                          uint64_t* stats);
+
 /* ---- host-buffer entry points (what a reference caller hands over) ------- *
  * materialize() with host vectors: value_width 2, 4 or 8.  fact/dim/out are
  * HOST pointers (pinned or pageable).  Synchronous. */

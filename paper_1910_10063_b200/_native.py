@@ -54,6 +54,10 @@ SIGNATURES = {
     "skx_heavy_hitter_count": (_int, [_vp, _vp, _u64, _u32, _u32, _vp, _vp]),
     "skx_zipf_cdf_host": (_int, [_u32, _dbl, _vp]),
     "skx_random_bijection_host": (_int, [_u32, _u64, _vp]),
+    "skx_line_frequencies": (_int, [_vp, _vp, _u32, _vp, _u32, _vp, _vp]),
+    "skx_estimate_hit_rate": (_int, [_vp, _vp, _u64, _u64, _vp, _vp]),
+    "skx_trace_from_column": (_int, [_vp, _vp, _u64, _u32, _vp, _vp]),
+    "skx_simulate_lru_host": (_int, [_vp, _u64, _u64, _vp]),
     "skx_generate_zipf": (_int, [_vp, _vp, _u32, _vp, _u64, _u64, _u64, _vp, _vp]),
     "skx_materialize_host": (_int, [_vp, _int, _vp, _u64, _vp, _u64, _vp]),
     "skx_aggregate_host": (_int, [_vp, _vp, _vp, _int, _u64, _u32, _u32, _vp, _vp]),

@@ -220,6 +220,54 @@ int skx_sync(skx_ctx* ctx, void* stream) {
 
 // ---- generator host side (column.cpp:44-71) --------------------------------
 
+// simulate_lru (cachemodel.cpp:125-173): exact fully associative LRU over a
+// trace of dense line ids -- a sequential recency list, host-side analysis
+// code as in the reference.  stats = {accesses, hits, distinct lines}.
+int skx_simulate_lru_host(const uint32_t* trace, uint64_t n, uint64_t cache_lines,
+                          uint64_t* stats) {
+  if (cache_lines == 0 || !stats || (n && !trace)) return SKX_INVALID_ARGUMENT;
+  stats[0] = n;
+  stats[1] = 0;
+  stats[2] = 0;
+  if (n == 0) return SKX_OK;
+  uint32_t mx = 0;
+  for (uint64_t i = 0; i < n; ++i) mx = trace[i] > mx ? trace[i] : mx;
+  const size_t u = (size_t)mx + 1;
+  constexpr uint32_t nil = 0xFFFFFFFFu;
+  std::vector<uint32_t> prv(u, nil), nxt(u, nil);
+  std::vector<uint8_t> resident(u, 0), seen(u, 0);
+  uint32_t head = nil, tail = nil;
+  uint64_t size = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint32_t x = trace[i];
+    if (!seen[x]) {
+      seen[x] = 1;
+      ++stats[2];
+    }
+    if (resident[x]) {
+      ++stats[1];
+      if (x == head) continue;
+      if (prv[x] != nil) nxt[prv[x]] = nxt[x]; else head = nxt[x];
+      if (nxt[x] != nil) prv[nxt[x]] = prv[x]; else tail = prv[x];
+    } else {
+      resident[x] = 1;
+      ++size;
+    }
+    prv[x] = nil;
+    nxt[x] = head;
+    if (head != nil) prv[head] = x; else tail = x;
+    head = x;
+    if (size > cache_lines) {
+      const uint32_t v = tail;
+      tail = prv[v];
+      if (tail != nil) nxt[tail] = nil; else head = nil;
+      resident[v] = 0;
+      --size;
+    }
+  }
+  return SKX_OK;
+}
+
 int skx_zipf_cdf_host(uint32_t d, double z, double* cdf) {
   if (d == 0 || d > SKX_MAX_DOMAIN_CARDINALITY || !(z >= 0.0) || !cdf) return SKX_INVALID_ARGUMENT;
   // zipf_frequencies: Kahan-summed normaliser, column.cpp:44-60.

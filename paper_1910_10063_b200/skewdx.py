@@ -495,7 +495,111 @@ def select_gather_sum(fact, bitmap: Bitmap, cat, price, supp, flag, n_categories
     return o_off[:c], o_cat[:c], o_pr[:c], o_su[:c], o_fl[:c], sums
 
 
+# ---------------------------------------------------------------------------
+# Cache model (cachemodel.hpp)
+# ---------------------------------------------------------------------------
+class Layout(enum.IntEnum):
+    """column.hpp Layout: rand = ranks scattered by random_bijection, freq = in place."""
+    rand = 0
+    freq = 1
+
+
+@dataclass
+class CacheGeometry:
+    """cachemodel.hpp:14-22."""
+    lines: int = 1
+    line_bytes: int = 64
+    element_bytes: int = 4
+
+    def elements_per_line(self) -> int:
+        return self.line_bytes // self.element_bytes
+
+    def validate(self):
+        if self.lines == 0:
+            raise InvalidArgument("cache geometry: line count must be at least 1")
+        if self.element_bytes == 0 or self.line_bytes == 0 or self.line_bytes % self.element_bytes:
+            raise InvalidArgument("cache geometry: line bytes must be a multiple of element bytes")
+
+
+@dataclass
+class LruStats:
+    """cachemodel.hpp:46-66."""
+    accesses: int = 0
+    hits: int = 0
+    distinct_lines: int = 0
+
+    def hit_rate(self) -> float:
+        return 0.0 if self.accesses == 0 else self.hits / self.accesses
+
+    def steady_hit_rate(self, cache_lines: int) -> float:
+        fill = min(self.distinct_lines, cache_lines)
+        denom = self.accesses - fill
+        return 0.0 if denom == 0 else self.hits / denom
+
+
+def line_frequencies(value_freqs: torch.Tensor, layout: Layout, geometry: CacheGeometry,
+                     seed: int, *, ctx=None, sync=True) -> torch.Tensor:
+    """cachemodel.cpp:22-45 on the device: per-line access frequencies of a
+    float64 per-rank frequency vector (bit-identical to the reference)."""
+    geometry.validate()
+    if not value_freqs.is_cuda or value_freqs.dtype != torch.float64:
+        raise InvalidArgument("value_freqs must be a float64 CUDA tensor")
+    d = value_freqs.numel()
+    if d == 0:
+        raise InvalidArgument("line_frequencies: empty frequency vector")
+    ctx = _ctx_for(value_freqs, ctx)
+    per = geometry.elements_per_line()
+    out = torch.empty((d + per - 1) // per, dtype=torch.float64, device=value_freqs.device)
+    r2i = None
+    if Layout(layout) == Layout.rand:
+        r2i = torch.from_numpy(random_bijection(d, seed)).to(value_freqs.device)
+    ctx.call("skx_line_frequencies", _ptr(value_freqs.contiguous()), d, _ptr(r2i), per, _ptr(out),
+             ctx.stream(), sync=sync)
+    return out
+
+
+def estimate_hit_rate(line_freqs: torch.Tensor, cache_lines: int, *, ctx=None) -> float:
+    """cachemodel.cpp:76-123 on the device (the reference to rounding)."""
+    if cache_lines == 0:
+        raise InvalidArgument("estimate_hit_rate: cache must have at least 1 line")
+    if not line_freqs.is_cuda or line_freqs.dtype != torch.float64:
+        raise InvalidArgument("line_freqs must be a float64 CUDA tensor")
+    ctx = _ctx_for(line_freqs, ctx)
+    res = torch.empty(1, dtype=torch.float64, device=line_freqs.device)
+    ctx.call("skx_estimate_hit_rate", _ptr(line_freqs.contiguous()), line_freqs.numel(),
+             int(cache_lines), _ptr(res), ctx.stream(), sync=True)
+    return float(res.item())
+
+
+def trace_from_column(fact: torch.Tensor, geometry: CacheGeometry, *, ctx=None,
+                      sync=True) -> torch.Tensor:
+    """cachemodel.cpp:175-186 on the device: 0-based line ids of a 1-based FK column."""
+    geometry.validate()
+    fact = _col(fact)
+    ctx = _ctx_for(fact, ctx)
+    out = torch.empty(fact.numel(), dtype=torch.uint32, device=fact.device)
+    ctx.call("skx_trace_from_column", _ptr(fact), fact.numel(), geometry.elements_per_line(),
+             _ptr(out), ctx.stream(), sync=sync)
+    return out
+
+
+def simulate_lru(trace, cache_lines: int) -> LruStats:
+    """cachemodel.cpp:125-173: exact sequential LRU over a trace (host)."""
+    if cache_lines == 0:
+        raise InvalidArgument("simulate_lru: cache must have at least 1 line")
+    t = trace.cpu().numpy() if isinstance(trace, torch.Tensor) else np.asarray(trace)
+    t = np.ascontiguousarray(t, dtype=np.uint32)
+    st = np.zeros(3, np.uint64)
+    lib = _native.load()
+    if lib.skx_simulate_lru_host(t.ctypes.data_as(C.c_void_p), len(t), int(cache_lines),
+                                 st.ctypes.data_as(C.c_void_p)) != 0:
+        raise InvalidArgument("simulate_lru: invalid arguments")
+    return LruStats(int(st[0]), int(st[1]), int(st[2]))
+
+
 __all__ = [
+    "Layout", "CacheGeometry", "LruStats", "line_frequencies", "estimate_hit_rate",
+    "trace_from_column", "simulate_lru",
     "Context", "context", "FrequencyProfile", "PermutationIndex", "count_frequencies",
     "histogram_u32", "build_index", "rebuild", "recode_fact", "permute_dimension", "Bitmap",
     "build_bitmap_lt", "permute_bitmap", "materialize", "select", "aggregate_count",

@@ -129,3 +129,16 @@ def test_cache_model_matches_reference_live(oracle, reference):
                 assert oracle.estimate_hit_rate(a, s) == reference.estimate_hit_rate(b, s)
         tr = rng.integers(0, 500, size=5000).astype(np.uint32)
         assert oracle.simulate_lru(tr, 37) == reference.simulate_lru(tr, 37)
+
+
+def test_libskx_simulate_lru_host_matches_reference_fixtures():
+    """The product library's host LRU simulator (no GPU needed) against the
+    reference's outputs."""
+    from paper_1910_10063_b200 import skewdx as sx
+    z, meta = _golden()
+    for i, m in enumerate(meta):
+        for s, exp in zip(m["caches"], m["lru"]):
+            st = sx.simulate_lru(z[f"c{i}_trace"], s)
+            assert [st.accesses, st.hits, st.distinct_lines] == exp, (i, s)
+    assert sx.simulate_lru([1, 1, 1, 1], 1).hit_rate() == 0.75
+    assert sx.simulate_lru([], 4).hit_rate() == 0.0

@@ -406,3 +406,42 @@ def test_aggregate_packed_tail_fallback(sx, oracle, case):
         c, s = sx.aggregate_count_sum(cu(fact), cu(m32), d, hot_threshold=hot)
         ce, se = oracle.aggregate_count_sum(fact, m32, d)
         assert np.array_equal(np_(c), ce) and np.array_equal(np_(s), se)
+
+
+def test_cache_model_vs_reference_fixtures(sx):
+    """Cache model on the device (csrc/cachemodel.cu) against the reference's
+    outputs: line_frequencies and trace_from_column bit-exact,
+    estimate_hit_rate to rounding (parallel prefix sums)."""
+    import json
+    import os
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "ref_cachemodel.npz"))
+    meta = json.loads(bytes(z["meta"]).decode())
+    for i, m in enumerate(meta):
+        geom = sx.CacheGeometry(1, m["line_bytes"], m["element_bytes"])
+        layout = sx.Layout.freq if m["layout"] == "freq" else sx.Layout.rand
+        lf = sx.line_frequencies(cu(z[f"c{i}_value_freqs"]), layout, geom, m["seed"])
+        assert np.array_equal(np_(lf), z[f"c{i}_line_freqs"]), i
+        for s, exp in zip(m["caches"], m["estimate"]):
+            got = sx.estimate_hit_rate(lf, s)
+            assert got == pytest.approx(exp, rel=1e-9, abs=1e-15), (i, s)
+        tr = sx.trace_from_column(cu(z[f"c{i}_fact"]), geom)
+        assert np.array_equal(np_(tr), z[f"c{i}_trace"]), i
+    from paper_1910_10063_b200 import DomainViolation
+    with pytest.raises(DomainViolation) as e:  # cachemodel.cpp:180: id 0 at row 1
+        sx.trace_from_column(cu(np.array([3, 0, 1], np.uint32)), sx.CacheGeometry(1, 64, 4))
+    assert e.value.row() == 1 and e.value.value() == 0
+
+
+@pytest.mark.parametrize("layout", ["freq", "rand"])
+def test_cache_model_at_scale_vs_oracle(sx, oracle, layout):
+    """2^22 keys, Zipf(1.0), B200 L2-like geometry: the device model equals
+    the oracle (bit-exact lines, estimate to rounding)."""
+    d = 1 << 22
+    vf = oracle.zipf_frequencies(d, 1.0)
+    lf_o = oracle.line_frequencies(vf, layout, 128, 8, 42)
+    geom = sx.CacheGeometry(1, 128, 8)
+    lf = sx.line_frequencies(cu(vf), sx.Layout[layout], geom, 42)
+    assert np.array_equal(np_(lf), lf_o)
+    for s in (1 << 10, 1 << 14, 1 << 17):
+        assert sx.estimate_hit_rate(lf, s) == pytest.approx(oracle.estimate_hit_rate(lf_o, s),
+                                                            rel=1e-9)
