@@ -205,7 +205,7 @@ int skx_fill_column(skx_ctx* ctx, int kind, int width, uint64_t seed, uint64_t n
  * rank order (bit-identical to the reference).  rank_to_id NULL = freq layout
  * (rank r is element r); else element rank_to_id[r]-1 (the rand layout's
  * random_bijection, skx_random_bijection_host).  per_line = line_bytes /
- * element_bytes (1..64 with a bijection).  Device pointers, d doubles in,
+ * element_bytes (1..256 with a bijection).  Device pointers, d doubles in,
  * ceil(d / per_line) doubles out. */
 int skx_line_frequencies(skx_ctx* ctx, const double* value_freqs, uint32_t d,
                          const uint32_t* rank_to_id, uint32_t per_line, double* out,

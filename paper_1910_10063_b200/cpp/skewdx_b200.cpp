@@ -27,6 +27,7 @@
 #include "skewdx/operators.hpp"
 #include "skewdx/parallel.hpp"
 #include "skewdx/permindex.hpp"
+#include "skewdx/cachemodel.hpp"
 #include "skx.h"
 
 namespace skewdx {
@@ -571,6 +572,66 @@ std::uint64_t memory_footprint(const ParallelPlan& plan, std::uint64_t domain_ca
       return domain_cardinality * 8 + std::uint64_t{plan.threads} * plan.hot_threshold * 8;
   }
   return 0;
+}
+
+// ---- cache model (cachemodel.hpp) -------------------------------------------
+void validate(const CacheGeometry& geometry) {
+  if (geometry.lines == 0) throw InvalidArgument("cache geometry: line count must be at least 1");
+  if (geometry.element_bytes == 0 || geometry.line_bytes == 0 ||
+      geometry.line_bytes % geometry.element_bytes != 0)
+    throw InvalidArgument("cache geometry: line bytes must be a multiple of element bytes");
+}
+
+std::vector<double> line_frequencies(std::span<const double> value_freqs, Layout layout,
+                                     const CacheGeometry& geometry, std::uint64_t seed) {
+  validate(geometry);
+  if (value_freqs.empty()) throw InvalidArgument("line_frequencies: empty frequency vector");
+  const auto d = static_cast<std::uint32_t>(value_freqs.size());
+  const std::uint32_t per = geometry.elements_per_line();
+  std::vector<double> out((value_freqs.size() + per - 1) / per);
+  DevBuf vf(std::vector<double>(value_freqs.begin(), value_freqs.end())), o(out.size() * 8);
+  if (layout == Layout::freq) {
+    run(skx_line_frequencies(ctx(), vf.as<double>(), d, nullptr, per, o.as<double>(), nullptr));
+  } else {
+    DevBuf map(random_bijection(d, seed));
+    run(skx_line_frequencies(ctx(), vf.as<double>(), d, map.as<std::uint32_t>(), per,
+                             o.as<double>(), nullptr));
+  }
+  o.to(out);
+  return out;
+}
+
+double estimate_hit_rate(std::span<const double> line_freqs, std::uint64_t cache_lines) {
+  if (cache_lines == 0) throw InvalidArgument("estimate_hit_rate: cache must have at least 1 line");
+  if (line_freqs.empty()) return 1.0;
+  DevBuf lf(std::vector<double>(line_freqs.begin(), line_freqs.end())), r(8);
+  run(skx_estimate_hit_rate(ctx(), lf.as<double>(), line_freqs.size(), cache_lines, r.as<double>(),
+                            nullptr));
+  std::vector<double> v(1);
+  r.to(v);
+  return v[0];
+}
+
+LruStats simulate_lru(std::span<const std::uint32_t> trace, std::uint64_t cache_lines) {
+  if (cache_lines == 0) throw InvalidArgument("simulate_lru: cache must have at least 1 line");
+  std::uint64_t st[3] = {0, 0, 0};
+  check(skx_simulate_lru_host(trace.data(), trace.size(), cache_lines, st));
+  LruStats s;
+  s.accesses = st[0];
+  s.hits = st[1];
+  s.distinct_lines = st[2];
+  return s;
+}
+
+std::vector<std::uint32_t> trace_from_column(const Column& fact, const CacheGeometry& geometry) {
+  validate(geometry);
+  std::vector<std::uint32_t> out(fact.size());
+  if (fact.empty()) return out;
+  DevBuf f(fact), o(fact.size() * 4);
+  run(skx_trace_from_column(ctx(), f.as<std::uint32_t>(), fact.size(), geometry.elements_per_line(),
+                            o.as<std::uint32_t>(), nullptr));
+  o.to(out);
+  return out;
 }
 
 }  // namespace skewdx

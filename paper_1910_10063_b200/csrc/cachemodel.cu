@@ -28,7 +28,7 @@
 namespace skx {
 namespace {
 
-constexpr uint32_t kMaxPerLine = 64;  // rand layout: members sorted in registers
+constexpr uint32_t kMaxPerLine = 256;  // rand layout: members sorted per thread
 
 __global__ void k_line_freq_consecutive(const double* __restrict__ vf, uint32_t d, uint32_t per,
                                         uint64_t lines, double* __restrict__ out) {
@@ -174,7 +174,7 @@ int skx_line_frequencies(skx_ctx* ctx, const double* value_freqs, uint32_t d,
   if (!ctx) return SKX_INVALID_ARGUMENT;
   if (d == 0) return set_error(ctx, SKX_INVALID_ARGUMENT, "line_frequencies: empty frequency vector");
   if (per_line == 0 || (rank_to_id && per_line > kMaxPerLine))
-    return set_error(ctx, SKX_INVALID_ARGUMENT, "line_frequencies: 1..64 elements per line");
+    return set_error(ctx, SKX_INVALID_ARGUMENT, "line_frequencies: 1..256 elements per line");
   cudaStream_t s = as_stream(stream);
   const uint64_t lines = ((uint64_t)d + per_line - 1) / per_line;
   if (!rank_to_id) {
