@@ -96,6 +96,18 @@ struct AggCheck {
 constexpr unsigned long long kPackOne = 1ull << 40;
 constexpr unsigned long long kPackMax = 1ull << 16;  // packed measures are < 2^16
 constexpr unsigned long long kPackMask = kPackOne - 1;
+// Far tail (ids >= Tail::far, the rarest keys): 4-byte packed accumulators,
+// count in bits 21..31, sum in bits 0..20 -- half the footprint again, so the
+// accumulators of a 2^24-key domain fit the half of L2 the streams leave
+// (C3 s=1.0 5.85 -> 3.8 ms).  The same exact-totals check covers them; the
+// boundary (2^18 for 2^30 rows, scaled with the row count) keeps a Zipf key's
+// expected count there in the low hundreds for s in [0.5, 1.5].
+constexpr int kFarSumBits = 21;
+constexpr unsigned int kFarOne = 1u << kFarSumBits;
+constexpr unsigned int kFarMask = kFarOne - 1u;
+#ifndef SKX_AGG_FAR
+#define SKX_AGG_FAR 1
+#endif
 
 __device__ __forceinline__ bool agg_ok(const AggCheck* c) {
   return c->big == 0 && c->dec_rows == c->tail_rows && c->dec_sum == c->tail_sum;
@@ -106,8 +118,10 @@ __device__ __forceinline__ bool agg_ok(const AggCheck* c) {
 // tail row).
 struct Tail {
   unsigned long long* pairs;
-  unsigned long long* acc;  // packed mode: [d] (count << 40 | sum)
+  unsigned long long* acc;  // packed mode: [far] (count << 40 | sum) for ids < far
   AggCheck* chk;            // packed mode
+  unsigned int* acc32;      // packed mode: [d - far] (count << 22 | sum) for ids >= far
+  uint32_t far;             // packed mode: first id of the far tail (d = none)
   // Staged tail (STG): rows of cold keys are appended per key-range bucket
   // and folded by k_agg_fold while the bucket's pairs are L2-resident.
   unsigned long long* cursors;  // [nb]
@@ -167,7 +181,10 @@ __device__ __forceinline__ void agg_row(uint32_t idx, unsigned long long m, uint
       atomicAdd(&t.pairs[idx], 1ull);
     } else if (PACK) {
       if (m < kPackMax) {
-        atomicAdd(&t.acc[idx], kPackOne | m);
+        if (idx < t.far)
+          atomicAdd(&t.acc[idx], kPackOne | m);
+        else
+          atomicAdd(&t.acc32[idx - t.far], kFarOne | (unsigned int)m);
         ++pt.rows;
         pt.sum += m;
       } else {
@@ -408,7 +425,8 @@ __global__ void k_deinterleave(const unsigned long long* __restrict__ pairs, uin
 // accumulators (ids >= hot), plus the decoded totals for the exactness check.
 __global__ void __launch_bounds__(256)
     k_agg_decode(const unsigned long long* __restrict__ hotpairs,
-                 const unsigned long long* __restrict__ acc, uint32_t hot, uint32_t d,
+                 const unsigned long long* __restrict__ acc,
+                 const unsigned int* __restrict__ acc32, uint32_t far, uint32_t hot, uint32_t d,
                  unsigned long long* __restrict__ counts, unsigned long long* __restrict__ sums,
                  AggCheck* chk) {
   unsigned long long lr = 0, ls = 0;
@@ -419,10 +437,16 @@ __global__ void __launch_bounds__(256)
       const ulonglong2 p = reinterpret_cast<const ulonglong2*>(hotpairs)[i];
       c = p.x;
       sm = p.y;
-    } else {
+    } else if (i < far) {
       const unsigned long long x = __ldcs(acc + i);
       c = x >> 40;
       sm = x & kPackMask;
+      lr += c;
+      ls += sm;
+    } else {
+      const unsigned int x = __ldcs(acc32 + (i - far));
+      c = x >> kFarSumBits;
+      sm = x & kFarMask;
       lr += c;
       ls += sm;
     }
@@ -526,16 +550,28 @@ int launch_aggregate(skx_ctx* ctx, const uint32_t* fact, const void* measure, in
     if (sums && e == cudaSuccess) e = cudaMemsetAsync(sums, 0, (size_t)d * 8, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "aggregate memset");
     if (n == 0) return SKX_OK;
-    Tail t{reinterpret_cast<unsigned long long*>(counts), nullptr, nullptr, nullptr, nullptr,
-           nullptr, 0, 0, 0};
+    Tail t{reinterpret_cast<unsigned long long*>(counts), nullptr, nullptr, nullptr, 0, nullptr,
+           nullptr, nullptr, 0, 0, 0};
     return aggregate_impl<0, false>(ctx, fact, nullptr, n, d, d, hot_req, t, s);
   }
   const bool pack = ctx->agg_mode == 0 && n > 0;
   const uint32_t hot = hot_keys(ctx, mw, hot_req, d);
-  // Slot-1 layout: [AggCheck 256 B][hot pairs hot x 16 B][acc d x 8 B][pairs d x 16 B]
+  // Far tail for domains whose 8-byte accumulators would not fit half of L2.
+  uint32_t far = d;
+#ifndef SKX_AGG_FAR_BITS
+#define SKX_AGG_FAR_BITS 18
+#endif
+  if (SKX_AGG_FAR && d > (1u << 22)) {
+    uint64_t first = uint64_t(1) << SKX_AGG_FAR_BITS;  // for <= 2^30 rows
+    for (uint64_t r = uint64_t(1) << 30; r < n && first < (uint64_t(1) << 22); r <<= 1) first <<= 1;
+    far = hot > first ? hot : (uint32_t)first;
+  }
+  // Slot-1 layout: [AggCheck 256 B][hot pairs hot x 16 B][acc far x 8 B]
+  //                [acc32 (d - far) x 4 B][pairs d x 16 B]
   auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
-  const size_t chk_b = 256, hp_b = up((size_t)hot * 16), acc_b = up((size_t)d * 8);
-  const size_t pairs_off = pack ? chk_b + hp_b + acc_b : 0;
+  const size_t chk_b = 256, hp_b = up((size_t)hot * 16), acc_b = up((size_t)far * 8);
+  const size_t acc32_b = up((size_t)(d - far) * 4);
+  const size_t pairs_off = pack ? chk_b + hp_b + acc_b + acc32_b : 0;
   char* base = static_cast<char*>(scratch(ctx, 1, pairs_off + (size_t)d * 16 + 16));
   if (!base) return set_error(ctx, SKX_CUDA_ERROR, "aggregate: out of device memory");
   unsigned long long* pairs = reinterpret_cast<unsigned long long*>(base + pairs_off);
@@ -545,19 +581,20 @@ int launch_aggregate(skx_ctx* ctx, const uint32_t* fact, const void* measure, in
     AggCheck* chk = reinterpret_cast<AggCheck*>(base);
     unsigned long long* hotpairs = reinterpret_cast<unsigned long long*>(base + chk_b);
     unsigned long long* acc = reinterpret_cast<unsigned long long*>(base + chk_b + hp_b);
+    unsigned int* acc32 = reinterpret_cast<unsigned int*>(base + chk_b + hp_b + acc_b);
     cudaError_t e = cudaMemsetAsync(base, 0, pairs_off, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "aggregate memset");
-    Tail tp{hotpairs, acc, chk, nullptr, nullptr, nullptr, 0, 0, 0};
+    Tail tp{hotpairs, acc, chk, acc32, far, nullptr, nullptr, nullptr, 0, 0, 0};
     int rc = mw == 8 ? aggregate_impl<8, true>(ctx, fact, measure, n, d, d, hot_req, tp, s)
                      : aggregate_impl<4, true>(ctx, fact, measure, n, d, d, hot_req, tp, s);
     if (rc) return rc;
-    k_agg_decode<<<grid_for(ctx, d, 256, 8), 256, 0, s>>>(hotpairs, acc, hot, d, counts64,
-                                                         sums64, chk);
+    k_agg_decode<<<grid_for(ctx, d, 256, 8), 256, 0, s>>>(hotpairs, acc, acc32, far, hot, d,
+                                                         counts64, sums64, chk);
     // Exact fallback, queued now and skipped on the device when the check passed.
     k_agg_zero_if_failed<<<grid_for(ctx, d, 256, 8), 256, 0, s>>>(
         reinterpret_cast<ulonglong2*>(pairs), d, chk);
     ctx->launches += 2;
-    Tail t{pairs, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, 0};
+    Tail t{pairs, nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr, 0, 0, 0};
     rc = mw == 8 ? aggregate_impl<8, false>(ctx, fact, measure, n, d, d, hot_req, t, s, chk)
                  : aggregate_impl<4, false>(ctx, fact, measure, n, d, d, hot_req, t, s, chk);
     if (rc) return rc;
@@ -568,7 +605,7 @@ int launch_aggregate(skx_ctx* ctx, const uint32_t* fact, const void* measure, in
   }
   cudaError_t e = cudaMemsetAsync(pairs, 0, (size_t)d * 16, s);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "aggregate memset");
-  Tail t{pairs, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, 0};
+  Tail t{pairs, nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr, 0, 0, 0};
   int rc = SKX_OK;
   if (n > 0) {
     rc = mw == 8 ? aggregate_impl<8, false>(ctx, fact, measure, n, d, d, hot_req, t, s)
@@ -607,8 +644,8 @@ int skx_heavy_hitter_count(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint3
     if (e != cudaSuccess) return skx::cuda_fail(ctx, e, "heavy_hitter memset");
   }
   if (n == 0) return SKX_OK;
-  skx::Tail t{reinterpret_cast<unsigned long long*>(counts), nullptr, nullptr, nullptr, nullptr,
-              nullptr, 0, 0, 0};
+  skx::Tail t{reinterpret_cast<unsigned long long*>(counts), nullptr, nullptr, nullptr, 0,
+              nullptr, nullptr, nullptr, 0, 0, 0};
   return skx::aggregate_impl<0, false>(ctx, fact, nullptr, n, d, cutoff, cutoff, t, s);
 }
 

@@ -371,14 +371,26 @@ def test_aggregate_large_domain_modes(sx, oracle, mode, z):
     assert np.array_equal(np_(c), ce) and np.array_equal(np_(s), se)
 
 
-@pytest.mark.parametrize("case", ["big_measure", "count_wrap", "sum_carry", "mixed"])
+@pytest.mark.parametrize("case", ["big_measure", "count_wrap", "sum_carry", "mixed",
+                                  "far_count_wrap", "far_sum_carry", "far_ok"])
 def test_aggregate_packed_tail_fallback(sx, oracle, case):
     """The packed tail (count << 40 | sum) must detect every overflow on the
     device and redo the call exactly: measures >= 2^16, a cold key with
     >= 2^24 rows (count field wraps), a cold key whose sum reaches 2^40."""
     d, hot = 1000, 16
     rng = np.random.default_rng(5)
-    if case == "big_measure":
+    if case.startswith("far"):
+        # domains > 2^22 keep ids >= 2^18 in 4-byte accumulators (count 11 bits, sum 21 bits)
+        d = (1 << 22) + 4099
+        n = 200_003
+        fact = rng.integers(1, d + 1, size=n, dtype=np.uint32)
+        meas = rng.integers(1, 101, size=n, dtype=np.int64)
+        if case == "far_count_wrap":
+            fact[:5000] = 3_000_000  # 5000 rows > 2047 on one far key
+        elif case == "far_sum_carry":
+            fact[:100] = 3_000_001
+            meas[:100] = 60000  # sum 6e6 >= 2^21 on one far key
+    elif case == "big_measure":
         n = 100_003
         fact = rng.integers(1, d + 1, size=n, dtype=np.uint32)
         meas = rng.integers(0, 2**63, size=n, dtype=np.int64)
