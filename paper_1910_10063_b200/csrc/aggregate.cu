@@ -120,8 +120,9 @@ struct Tail {
   unsigned long long* pairs;
   unsigned long long* acc;  // packed mode: [far] (count << 40 | sum) for ids < far
   AggCheck* chk;            // packed mode
-  unsigned int* acc32;      // packed mode: [d - far] (count << 22 | sum) for ids >= far
+  unsigned int* acc32;      // packed mode: [d - far] (count << 21 | sum) for ids >= far
   uint32_t far;             // packed mode: first id of the far tail (d = none)
+  unsigned int* cnt32;      // COUNT only, < 2^32 rows: u32 counts (half the footprint)
   // Staged tail (STG): rows of cold keys are appended per key-range bucket
   // and folded by k_agg_fold while the bucket's pairs are L2-resident.
   unsigned long long* cursors;  // [nb]
@@ -178,7 +179,10 @@ __device__ __forceinline__ void agg_row(uint32_t idx, unsigned long long m, uint
     hot_add(b, idx, m, MW != 0, t.pairs);
   } else if (idx < limit) {
     if (!MW) {
-      atomicAdd(&t.pairs[idx], 1ull);
+      if (t.cnt32)
+        atomicAdd(&t.cnt32[idx], 1u);
+      else
+        atomicAdd(&t.pairs[idx], 1ull);
     } else if (PACK) {
       if (m < kPackMax) {
         if (idx < t.far)
@@ -289,7 +293,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         atomicAdd(&t.pairs[2 * (uint64_t)i + 1],
                   ((unsigned long long)(kBinBytes == 12 ? b.hi[i] : 0u) << 32) | b.lo[i]);
       } else {
-        atomicAdd(&t.pairs[i], c);
+        if (t.cnt32)
+          atomicAdd(&t.cnt32[i], (unsigned int)c);
+        else
+          atomicAdd(&t.pairs[i], c);
       }
     }
   }
@@ -473,6 +480,14 @@ __global__ void __launch_bounds__(256)
     pairs[i] = make_ulonglong2(0ull, 0ull);
 }
 
+__global__ void __launch_bounds__(256)
+    k_widen_u32(const unsigned int* __restrict__ c32, uint32_t d,
+                unsigned long long* __restrict__ counts) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d; i += stride)
+    __stcs(counts + i, (unsigned long long)__ldcs(c32 + i));
+}
+
 uint32_t hot_keys(const skx_ctx* ctx, int mw, uint32_t hot_req, uint32_t limit) {
   const size_t per_key = mw ? kBinBytes : 4;
   const size_t budget = ctx->smem_optin > 2048 ? ctx->smem_optin - 2048 : 0;
@@ -550,8 +565,23 @@ int launch_aggregate(skx_ctx* ctx, const uint32_t* fact, const void* measure, in
     if (sums && e == cudaSuccess) e = cudaMemsetAsync(sums, 0, (size_t)d * 8, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "aggregate memset");
     if (n == 0) return SKX_OK;
+    if (n < 0xFFFFFFFFull && d >= (1u << 20)) {
+      // u32 counts are exact below 2^32 rows and halve the tail's footprint
+      unsigned int* c32 = static_cast<unsigned int*>(scratch(ctx, 1, (size_t)d * 4));
+      if (!c32) return set_error(ctx, SKX_CUDA_ERROR, "aggregate: out of device memory");
+      e = cudaMemsetAsync(c32, 0, (size_t)d * 4, s);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "aggregate memset");
+      Tail t{nullptr, nullptr, nullptr, nullptr, 0, c32, nullptr, nullptr, nullptr, 0, 0, 0};
+      const int rc = aggregate_impl<0, false>(ctx, fact, nullptr, n, d, d, hot_req, t, s);
+      if (rc) return rc;
+      k_widen_u32<<<grid_for(ctx, d, 256, 8), 256, 0, s>>>(c32, d,
+                                                          reinterpret_cast<unsigned long long*>(counts));
+      ctx->launches++;
+      SKX_CHECK_LAUNCH(ctx, "aggregate widen");
+      return SKX_OK;
+    }
     Tail t{reinterpret_cast<unsigned long long*>(counts), nullptr, nullptr, nullptr, 0, nullptr,
-           nullptr, nullptr, 0, 0, 0};
+           nullptr, nullptr, nullptr, 0, 0, 0};
     return aggregate_impl<0, false>(ctx, fact, nullptr, n, d, d, hot_req, t, s);
   }
   const bool pack = ctx->agg_mode == 0 && n > 0;
@@ -584,7 +614,7 @@ int launch_aggregate(skx_ctx* ctx, const uint32_t* fact, const void* measure, in
     unsigned int* acc32 = reinterpret_cast<unsigned int*>(base + chk_b + hp_b + acc_b);
     cudaError_t e = cudaMemsetAsync(base, 0, pairs_off, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "aggregate memset");
-    Tail tp{hotpairs, acc, chk, acc32, far, nullptr, nullptr, nullptr, 0, 0, 0};
+    Tail tp{hotpairs, acc, chk, acc32, far, nullptr, nullptr, nullptr, nullptr, 0, 0, 0};
     int rc = mw == 8 ? aggregate_impl<8, true>(ctx, fact, measure, n, d, d, hot_req, tp, s)
                      : aggregate_impl<4, true>(ctx, fact, measure, n, d, d, hot_req, tp, s);
     if (rc) return rc;
@@ -594,7 +624,7 @@ int launch_aggregate(skx_ctx* ctx, const uint32_t* fact, const void* measure, in
     k_agg_zero_if_failed<<<grid_for(ctx, d, 256, 8), 256, 0, s>>>(
         reinterpret_cast<ulonglong2*>(pairs), d, chk);
     ctx->launches += 2;
-    Tail t{pairs, nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr, 0, 0, 0};
+    Tail t{pairs, nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr, nullptr, 0, 0, 0};
     rc = mw == 8 ? aggregate_impl<8, false>(ctx, fact, measure, n, d, d, hot_req, t, s, chk)
                  : aggregate_impl<4, false>(ctx, fact, measure, n, d, d, hot_req, t, s, chk);
     if (rc) return rc;
@@ -605,7 +635,7 @@ int launch_aggregate(skx_ctx* ctx, const uint32_t* fact, const void* measure, in
   }
   cudaError_t e = cudaMemsetAsync(pairs, 0, (size_t)d * 16, s);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "aggregate memset");
-  Tail t{pairs, nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr, 0, 0, 0};
+  Tail t{pairs, nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr, nullptr, 0, 0, 0};
   int rc = SKX_OK;
   if (n > 0) {
     rc = mw == 8 ? aggregate_impl<8, false>(ctx, fact, measure, n, d, d, hot_req, t, s)
@@ -645,7 +675,7 @@ int skx_heavy_hitter_count(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint3
   }
   if (n == 0) return SKX_OK;
   skx::Tail t{reinterpret_cast<unsigned long long*>(counts), nullptr, nullptr, nullptr, 0,
-              nullptr, nullptr, nullptr, 0, 0, 0};
+              nullptr, nullptr, nullptr, nullptr, 0, 0, 0};
   return skx::aggregate_impl<0, false>(ctx, fact, nullptr, n, d, cutoff, cutoff, t, s);
 }
 

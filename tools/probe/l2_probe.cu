@@ -229,6 +229,7 @@ k_l2(const uint32_t* __restrict__ fk, uint64_t n, const uint64_t* __restrict__ d
       if (H == 17) v[u] = hot ? 0ull : ld_ca(p);
       if (H == 40) v[u] = hot ? ld_plain(p) : ld_cas(p);
       if (H == 50) v[u] = hot ? ld_plain(p) : ld_p64(p);
+      if (H >= 60 && H <= 62) v[u] = ld_plain(p);
       if (H == 51) v[u] = ld_p64(p);
       if (H == 52) v[u] = hot ? 0ull : ld_p64(p);
       if (H == 53) v[u] = hot ? 0ull : ld_p128(p);
@@ -238,7 +239,14 @@ k_l2(const uint32_t* __restrict__ fk, uint64_t n, const uint64_t* __restrict__ d
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       uint64_t row = base + (uint64_t)u * kT + threadIdx.x;
-      if (row < n) __stcs(reinterpret_cast<unsigned long long*>(out + row), v[u]);
+      if (row < n) {
+        unsigned long long* q = reinterpret_cast<unsigned long long*>(out + row);
+        if (H == 60) asm volatile("st.global.wt.u64 [%0], %1;" ::"l"(q), "l"(v[u]) : "memory");
+        else if (H == 61) asm volatile("st.global.L1::no_allocate.L2::cache_hint.u64 [%0], %1, %2;"
+                                       ::"l"(q), "l"(v[u]), "l"(pf) : "memory");
+        else if (H == 62) *q = v[u];
+        else __stcs(q, v[u]);
+      }
     }
   }
 }
@@ -345,6 +353,9 @@ extern "C" int probe_l2(int h, int grid, uint64_t win_bytes, float hit_ratio, ui
     case 30: return launch<30>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
     case 40: return launch<40>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
     case 50: return launch<50>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
+    case 60: return launch<60>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
+    case 61: return launch<61>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
+    case 62: return launch<62>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
     case 51: return launch<51>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
     case 52: return launch<52>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);
     case 53: return launch<53>(grid, win_bytes, hit_ratio, fk, n, dim, out, K, s);

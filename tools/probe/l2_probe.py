@@ -72,6 +72,9 @@ if MODE == "tma":
     for K in (256 * 1024, 1 * MB, 4 * MB, 16 * MB):
         for h in (0, 18, 19, 20, 10):
             cfgs.append((h, K, 0, 0, 1.0, 592))
+if MODE == "st":
+    for h in (0, 60, 61, 62):
+        cfgs.append((h, 0, 0, 0, 1.0, 592))
 if MODE == "pf":
     for K in (1 * MB, 16 * MB):
         for h in (0, 50, 51, 10, 52, 53):
