@@ -11,17 +11,32 @@ __device__ __forceinline__ uint64_t mix(uint64_t x) {
   return x ^ (x >> 31);
 }
 
+template <int M>
+__device__ __forceinline__ uint64_t ld(const uint64_t* p) {
+  uint64_t v;
+  if (M == 0) v = __ldg(p);
+  if (M == 1) asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  if (M == 2) asm volatile("ld.global.relaxed.gpu.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  if (M == 3) asm volatile("ld.global.cv.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+
+template <int M>
 __global__ void __launch_bounds__(256) k_pure(const uint64_t* __restrict__ dim, uint64_t D,
                                               int iters, uint64_t seed, uint64_t* out) {
   const uint64_t t = (uint64_t)blockIdx.x * 256 + threadIdx.x;
   uint64_t acc = 0;
 #pragma unroll 8
-  for (int i = 0; i < iters; ++i) acc ^= __ldg(dim + mix(seed ^ (t * 1000003ull + i)) % D);
+  for (int i = 0; i < iters; ++i) acc ^= ld<M>(dim + mix(seed ^ (t * 1000003ull + i)) % D);
   out[t] = acc;
 }
 
 extern "C" int probe_pure(const uint64_t* dim, uint64_t D, int iters, uint64_t seed,
-                          uint64_t* out, int grid, void* stream) {
-  k_pure<<<grid, 256, 0, (cudaStream_t)stream>>>(dim, D, iters, seed, out);
+                          uint64_t* out, int grid, void* stream, int mode) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (mode == 0) k_pure<0><<<grid, 256, 0, s>>>(dim, D, iters, seed, out);
+  if (mode == 1) k_pure<1><<<grid, 256, 0, s>>>(dim, D, iters, seed, out);
+  if (mode == 2) k_pure<2><<<grid, 256, 0, s>>>(dim, D, iters, seed, out);
+  if (mode == 3) k_pure<3><<<grid, 256, 0, s>>>(dim, D, iters, seed, out);
   return (int)cudaGetLastError();
 }

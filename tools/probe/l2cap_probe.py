@@ -16,7 +16,8 @@ if not os.path.exists(so):
                            os.path.join(HERE, "l2cap_probe.cu"), "-o", so])
 lib = C.CDLL(so)
 lib.probe_pure.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_uint64, C.c_void_p, C.c_int,
-                           C.c_void_p]
+                           C.c_void_p, C.c_int]
+MODE = int(os.environ.get("PROBE_LD", 0))
 grid = int(os.environ.get("PROBE_GRID", 148 * 8))
 iters = int(os.environ.get("PROBE_ITERS", 256))
 out = torch.empty(grid * 256, dtype=torch.int64, device="cuda")
@@ -26,14 +27,14 @@ big = torch.randint(0, 2**62, (max(sizes) << 17,), dtype=torch.int64, device="cu
 for mb in sizes:
     D = mb << 17  # MB of int64
     for _ in range(3):
-        lib.probe_pure(big.data_ptr(), D, iters, 1, out.data_ptr(), grid, s)
+        lib.probe_pure(big.data_ptr(), D, iters, 1, out.data_ptr(), grid, s, MODE)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for r in range(5):
-        lib.probe_pure(big.data_ptr(), D, iters, 7 + r, out.data_ptr(), grid, s)
+        lib.probe_pure(big.data_ptr(), D, iters, 7 + r, out.data_ptr(), grid, s, MODE)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 5
     reads = grid * 256 * iters
-    print(json.dumps({"MB": mb, "ms": round(ms, 4), "Greads_per_s": round(reads / ms / 1e6, 1)}),
+    print(json.dumps({"ld": MODE, "MB": mb, "ms": round(ms, 4), "Greads_per_s": round(reads / ms / 1e6, 1)}),
           flush=True)
