@@ -162,9 +162,11 @@ int skx_build_bitmap_lt_i32(skx_ctx* ctx, const int32_t* dim, uint64_t d, int32_
                             uint64_t* out_words, void* stream);
 /* BASELINE config 5, fused: select rows whose bit is set, gather the four
  * dimension columns (i32 category, f32 price, u64 supplier, u16 flag) for
- * the selected rows in ascending row order, and SUM(price) per category in
- * fp64 (sums[n_categories], overwritten; categories outside
- * [0, n_categories) are not summed).  Offsets get `base` added. */
+ * the selected rows in ascending row order, and SUM(price) per category
+ * (sums[n_categories] as fp64, overwritten; categories outside
+ * [0, n_categories) are not summed): exact 96-bit fixed point when the
+ * prices are finite, span <= 2^30 in exponent and n_categories <= 4096,
+ * else an fp64 reduction (decided on the device).  Offsets get `base` added. */
 int skx_select_gather_sum(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uint64_t* words,
                           uint32_t d, const int32_t* cat, const float* price,
                           const uint64_t* supp, const uint16_t* flag, uint32_t base,
