@@ -22,7 +22,7 @@
  *    reported by the next skx_sync() on that context -- the first offending
  *    row, exactly as DomainViolation::row() reports it (error.hpp:20-33).
  *    Enqueue one operator and skx_sync() to attribute an error to it; the
- *    C++ drop-in (cpp/include/skewdx/*.hpp over libskewdx_b200.so) does exactly that and rethrows the
+ *    C++ drop-in (the cpp/include/skewdx headers over libskewdx_b200.so) does that and rethrows the
  *    reference's exception types.
  *  - A context belongs to one device and one host thread; operators issued on
  *    one context must be ordered on one stream (the context owns scratch).
