@@ -350,6 +350,17 @@ def timed_launches(fn, steps, warmup, stream, dist_on, ctx=None):
     return ev[0].elapsed_time(ev[steps]), per, launches
 
 
+def reduce_to_root(t):
+    """NCCL reduce to rank 0 (the BASELINE combine step).  The gloo backend,
+    used only for the single-GPU multi-rank dry run (SKX_BENCH_DIST_BACKEND),
+    all-reduces instead."""
+    import torch.distributed as dist
+    if dist.get_backend() == "nccl":
+        dist.reduce(t, dst=0)
+    else:
+        dist.all_reduce(t)
+
+
 def max_over_ranks(x, dist_on):
     import torch
     import torch.distributed as dist
@@ -371,10 +382,19 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SKX_BENCH_ONE_GPU=1 + SKX_BENCH_DIST_BACKEND=gloo: every rank on cuda:0, host-side
+    # collectives -- a logic dry run of the multi-rank path on a one-GPU box (no kernel
+    # waits on another rank's kernel).  Timings from it are not scaling numbers.
+    if os.environ.get("SKX_BENCH_ONE_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dist_on = world > 1
     if dist_on:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("SKX_BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     ctx = sx.context(local)
     ctx.set_gather_policy(args.policy)
     peak, peak_kind = load_peaks()
@@ -507,8 +527,8 @@ def run_ours(args):
             ctx.call("skx_aggregate", C_ptr(gdat.fact_freq), C_ptr(gdat.qty), 8, rows_local, D_C3, 0,
                      C_ptr(counts), C_ptr(sums), ctx.stream(), sync=False)
             if dist_on:  # per-GPU partials combined with NCCL reduce (BASELINE config 3)
-                dist.reduce(counts.view(torch.int64), dst=0)
-                dist.reduce(sums.view(torch.int64), dst=0)
+                reduce_to_root(counts.view(torch.int64))
+                reduce_to_root(sums.view(torch.int64))
         tg, per_g, _ = timed_launches(step_gb, args.steps, args.warmup, stream, dist_on)
         ctx.sync()
         tg = max_over_ranks(tg, dist_on)
@@ -530,7 +550,7 @@ def run_ours(args):
             ctx.call("skx_heavy_hitter_count", C_ptr(gdat.fact_freq), rows_local, D_C3, 8192,
                      C_ptr(hh), ctx.stream(), sync=False)
             if dist_on:
-                dist.reduce(hh.view(torch.int64), dst=0)
+                reduce_to_root(hh.view(torch.int64))
         th, per_h, _ = timed_launches(step_hh, args.steps, args.warmup, stream, dist_on)
         ctx.sync()
         th = max_over_ranks(th, dist_on)
@@ -673,7 +693,7 @@ def other_configs(args, ctx, stream, dist_on, rank, world, peak):
                  C_ptr(prc), C_ptr(sup), C_ptr(flg), 0, 1000, *[C_ptr(b) for b in bufs],
                  C_ptr(sums), C_ptr(cnt), ctx.stream(), sync=False)
         if dist_on:  # per-category fp64 partials reduced to rank 0
-            torch.distributed.reduce(sums, dst=0)
+            reduce_to_root(sums)
     t5, per5, _ = timed_launches(c5_step, k, args.warmup, stream, dist_on)
     ctx.sync()
     t5 = max_over_ranks(t5, dist_on)
