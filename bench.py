@@ -583,6 +583,9 @@ def run_ours(args):
                          "frac": achieved / peak, "peak_kind": peak_kind,
                          "frac_vs_nominal_8000": achieved / 8000.0,
                          "traffic": ncu_traffic("gather_c2"),
+                         # DRAM bytes actually moved per launch (ncu) over the live launch time:
+                         # how close the kernel runs to the HBM peak with its real traffic
+                         "traffic_GBps": (ncu_traffic("gather_c2") or 0) / statistics.mean(per) / 1e6,
                          "alg_bytes_per_launch": alg_bytes,
                          "avg_launch_ms": statistics.mean(per)},
             "cpu_baseline": cpu,

@@ -19,10 +19,11 @@ K = {"t": "gpu__time_duration.sum", "rd": "dram__bytes_read.sum", "wr": "dram__b
      "warps": "sm__warps_active.avg.pct_of_peak_sustained_active",
      "issue": "smsp__issue_active.avg.pct_of_peak_sustained_active",
      "regs": "launch__registers_per_thread", "grid": "launch__grid_size",
-     "block": "launch__block_size"}
-print("| # | kernel | grid x block | regs | time ms | DRAM rd GB | DRAM wr GB | L2 hit % | L1 hit % "
-      "| warps active % | issue active % | top stall |")
-print("|---|---|---|---|---|---|---|---|---|---|---|---|")
+     "block": "launch__block_size", "sec": "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+     "req": "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum"}
+print("| # | kernel | grid x block | regs | time ms | DRAM rd GB | DRAM wr GB | DRAM GB/s | L2 hit % "
+      "| L1 hit % | ld sectors/req | warps active % | issue active % | top stall |")
+print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
 for i, r in enumerate(rows[2:]):
     d = dict(zip(hdr, r))
 
@@ -37,6 +38,10 @@ for i, r in enumerate(rows[2:]):
     tot = sum(st.values()) or 1
     top = max(st, key=st.get) if st else ""
     name = d["Kernel Name"].split("(")[0].replace("void ", "").split("::")[-1]
+    t, rd, wr = f("t", 6), f("rd", 6), f("wr", 6)
+    bw = round((rd + wr) / (t * 1e-3), 0) if t and rd != "" and wr != "" else ""
+    sec, req = f("sec", 0), f("req", 0)
+    spr = round(sec / req, 2) if sec and req else ""
     print(f"| {i} | {name} | {d.get(K['grid'])} x {d.get(K['block'])} | {d.get(K['regs'])} | "
-          f"{f('t', 3)} | {f('rd')} | {f('wr')} | {f('l2', 1)} | {f('l1', 1)} | {f('warps', 1)} | "
-          f"{f('issue', 1)} | {top} {round(100 * st.get(top, 0) / tot)}% |")
+          f"{f('t', 3)} | {f('rd')} | {f('wr')} | {bw} | {f('l2', 1)} | {f('l1', 1)} | {spr} | "
+          f"{f('warps', 1)} | {f('issue', 1)} | {top} {round(100 * st.get(top, 0) / tot)}% |")
