@@ -476,6 +476,27 @@ def run_ours(args):
             "note": ("per-GPU u32 histogram, NCCL all-reduce (N>1), sort-by-count of D=%d, "
                      "recode of the local shard, permute of the int64 dim; warm, best of 3, "
                      "CUDA events" % d)}
+        # Cache model (csrc/cachemodel.cu) on the empirical profile: predicted
+        # dimension line misses of this gather vs the ncu-measured DRAM traffic.
+        def model():
+            vf = hist_counts.view(torch.int32).long()[idx2.offsets.view(torch.int32).long() - 1]
+            vf = vf.double() / float(n_total)  # rank order
+            geom = sx.CacheGeometry(1, 128, 8)
+            eff = 64 << 20  # random-read capacity of the L2 (profiles/r1_experiments.md §10)
+            res = {"geometry": "128 B lines of int64, L2 random-read capacity 64 MiB"}
+            for name, lay in (("freq", sx.Layout.freq), ("rand", sx.Layout.rand)):
+                lf = sx.line_frequencies(vf, lay, geom, SEED)
+                h = sx.estimate_hit_rate(lf, eff // 128)
+                res[name] = {"pred_l2_hit": h, "pred_line_misses": (1.0 - h) * rows_local}
+            tr = ncu_traffic("gather_c2")
+            if tr:
+                res["freq"]["ncu_line_misses"] = (tr - rows_local * 12) / 128.0
+            trr = ncu_traffic("gather_c2_rand")
+            if trr:
+                res["rand"]["ncu_line_misses"] = (trr - rows_local * 12) / 128.0
+            return res
+        if rank == 0:
+            extras["cache_model"] = _cpu_extra(model)
         del hist_counts, fact_tmp, idx2
 
     # e2e through the C-ABI host-buffer entry (pinned host fact+dim in, out back)
