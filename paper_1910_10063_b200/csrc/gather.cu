@@ -30,6 +30,9 @@ namespace {
 constexpr int kThreads = 256;      // plain variant: several CTAs per SM
 constexpr int kThreadsHot = 1024;  // hot-prefix variant: one CTA per SM owns the smem copy
 constexpr int kUnroll = 8;         // uint4 FK vectors per thread per iteration (32 rows)
+#ifndef SKX_GATHER_SMALL_CTAS
+#define SKX_GATHER_SMALL_CTAS 2    // CTAs per SM for small columns
+#endif
 
 // Policy bits (skx_set_gather_policy).
 constexpr int kPolHints = 1;   // evict_first streams, evict_last dimension
@@ -283,7 +286,8 @@ cudaError_t launch_vec(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64
                          // small columns: exactly the 2 resident CTAs/SM (no tail wave);
                          // large ones: 8/SM so the scheduler balances SM speed differences
                          : grid_for(ctx, nvec, kThreads * kUnroll,
-                                    nvec / (kThreads * kUnroll) < 16u * 2u * ctx->num_sms ? 2 : 8));
+                                    nvec / (kThreads * kUnroll) < 16u * 2u * ctx->num_sms
+                                        ? SKX_GATHER_SMALL_CTAS : 8));
   cfg.dynamicSmemBytes = HOT ? (size_t)hot * sizeof(V) : 0;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
