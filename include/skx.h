@@ -262,9 +262,13 @@ int skx_set_l2_fetch_granularity(skx_ctx* ctx, int bytes);
 int skx_set_gather_tiers(skx_ctx* ctx, uint64_t smem_bytes, uint64_t l1_bytes,
                          double l2_fraction);
 /* Histogram cold-key handling for domains whose counters exceed half of L2:
- * 0 = direct global reductions (default, faster as measured), 1 = key-range
- * buckets folded in shared memory (csrc/bucket.cuh). */
-int skx_set_histogram_mode(skx_ctx* ctx, int bucketed);
+ * 0 = default: beyond 3x L2, packed 16-bit counters (two keys per word)
+ *     checked on the device against the exact cold-row count, with a gated
+ *     direct recount on a wrap (only when the call starts from zeroed
+ *     counts); otherwise direct reductions,
+ * 1 = cold keys staged per key-range bucket and applied while L2-resident,
+ * 2 = direct 32/64-bit reductions. */
+int skx_set_histogram_mode(skx_ctx* ctx, int mode);
 /* Group-by (measure_width 4/8) cold-tail strategy:
  * 0 = packed (default): one 64-bit reduction of (1 << 40 | m) per cold row
  *     into an 8 B/key accumulator, decoded and validated on the device

@@ -149,9 +149,9 @@ int skx_set_gather_tiers(skx_ctx* ctx, uint64_t smem_bytes, uint64_t l1_bytes, d
   return SKX_OK;
 }
 
-int skx_set_histogram_mode(skx_ctx* ctx, int bucketed) {
-  if (!ctx || bucketed < 0 || bucketed > 1) return SKX_INVALID_ARGUMENT;
-  ctx->hist_bucketed = bucketed != 0;
+int skx_set_histogram_mode(skx_ctx* ctx, int mode) {
+  if (!ctx || mode < 0 || mode > 2) return SKX_INVALID_ARGUMENT;
+  ctx->hist_mode = mode;
   return SKX_OK;
 }
 

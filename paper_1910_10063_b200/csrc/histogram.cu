@@ -68,6 +68,18 @@ struct Buckets {
   uint32_t shift;         // bucket = idx >> shift
 };
 
+// Packed 16-bit cold counters (C16): two keys per 32-bit word, half the
+// footprint of u32 counters so more of the cold keys' lines stay in L2.  A
+// wrap of a half is caught on the device: the merged halves fall short of the
+// exact number of cold rows (each half <= its true count, equality iff it
+// did not wrap); gated kernels then redo the call with direct counters.
+struct HistCheck {
+  unsigned long long cold_rows;  // rows counted into the 16-bit halves (exact)
+  unsigned long long merged;     // sum of the merged halves
+};
+
+__device__ __forceinline__ bool hist_ok(const HistCheck* c) { return c->cold_rows == c->merged; }
+
 // Shared-memory state of the bucketed (BK) path: the tile's cold pairs and
 // its per-range counts / global bases.
 struct TileCold {
@@ -78,9 +90,10 @@ struct TileCold {
 };
 
 // Warp-collective: every lane calls it (invalid lanes with valid = false).
-template <typename CT, bool BK>
+template <typename CT, bool BK, bool C16>
 __device__ __forceinline__ void count_one(uint32_t id, bool valid, uint32_t* keys, uint32_t* cnts,
-                                          CT* counts, const TileCold& tc) {
+                                          CT* counts, const TileCold& tc, unsigned int* c16,
+                                          unsigned long long& cold_rows) {
   const uint32_t key = valid ? id : 0u;
   // Every lane updates on its own: same-address 32-bit shared adds from one
   // warp merge in hardware, so warp pre-aggregation with __match_any_sync
@@ -105,7 +118,15 @@ __device__ __forceinline__ void count_one(uint32_t id, bool valid, uint32_t* key
       }
       h = (h + 1) & (kTable - 1);
     }
-    if (cold && !BK) global_add<CT>(counts, key - 1, c);
+    if (cold && !BK) {
+      if (C16) {
+        const uint32_t idx = key - 1u;
+        atomicAdd(&c16[idx >> 1], 1u << ((idx & 1u) * 16));
+        ++cold_rows;
+      } else {
+        global_add<CT>(counts, key - 1, c);
+      }
+    }
   }
   if (BK) {  // warp-aggregated append to the tile's cold list
     const uint32_t m = __ballot_sync(0xffffffffu, cold);
@@ -153,10 +174,13 @@ __device__ __forceinline__ void flush_tile(const TileCold& tc, const Buckets& bk
   __syncthreads();  // resets visible before the next tile's appends
 }
 
-template <typename CT, bool BK>
+template <typename CT, bool BK, bool C16>
 __global__ void __launch_bounds__(kThreads)
     k_histogram(const uint32_t* __restrict__ fact, uint64_t head, uint64_t nvec, uint64_t n,
-                uint32_t d, CT* __restrict__ counts, Buckets bk, DevErr* err) {
+                uint32_t d, CT* __restrict__ counts, Buckets bk, DevErr* err,
+                unsigned int* __restrict__ c16, HistCheck* chk, const HistCheck* gate) {
+  if (gate && hist_ok(gate)) return;  // C16 fallback: nothing to redo
+  unsigned long long cold_rows = 0;
   extern __shared__ __align__(16) uint32_t smem_tab[];
   uint32_t* keys = smem_tab;
   uint32_t* cnts = smem_tab + kTable;
@@ -193,7 +217,7 @@ __global__ void __launch_bounds__(kThreads)
       for (int j = 0; j < 4; ++j) {
         const bool ok = (ids[j] - 1u) < d;
         if (live && !ok) record_violation(err, head + vi * 4 + j, ids[j]);
-        count_one<CT, BK>(ids[j], live && ok, keys, cnts, counts, tc);
+        count_one<CT, BK, C16>(ids[j], live && ok, keys, cnts, counts, tc, c16, cold_rows);
       }
     }
     if (BK) flush_tile<CT>(tc, bk, counts);
@@ -210,10 +234,15 @@ __global__ void __launch_bounds__(kThreads)
       const uint32_t id = live ? fact[k] : 0u;
       const bool ok = (id - 1u) < d;
       if (live && !ok) record_violation(err, k, id);
-      count_one<CT, BK>(id, live && ok, keys, cnts, counts, tc);
+      count_one<CT, BK, C16>(id, live && ok, keys, cnts, counts, tc, c16, cold_rows);
     }
   }
   if (BK) flush_tile<CT>(tc, bk, counts);  // block-uniform: also blocks != 0
+  if (C16) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cold_rows += __shfl_down_sync(0xffffffffu, cold_rows, o);
+    if ((threadIdx.x & 31) == 0 && cold_rows) atomicAdd(&chk->cold_rows, cold_rows);
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < kTable; i += kThreads) {
     const uint32_t k = keys[i];
@@ -239,17 +268,40 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// C16: counts[i] += half i of the packed words; sums the halves for the check.
+template <typename CT>
+__global__ void __launch_bounds__(256)
+    k_hist_merge16(const unsigned int* __restrict__ c16, uint32_t d, CT* __restrict__ counts,
+                   HistCheck* chk) {
+  unsigned long long tot = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < ((uint64_t)d + 1) / 2;
+       w += stride) {
+    const unsigned int x = __ldcs(c16 + w);
+    const uint32_t lo = x & 0xFFFFu, hi = x >> 16;
+    if (lo) counts[2 * w] += (CT)lo;
+    if (hi && 2 * w + 1 < d) counts[2 * w + 1] += (CT)hi;
+    tot += lo + hi;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tot += __shfl_down_sync(0xffffffffu, tot, o);
+  if ((threadIdx.x & 31) == 0 && tot) atomicAdd(&chk->merged, tot);
+}
+
+template <typename CT>
+__global__ void __launch_bounds__(256)
+    k_hist_zero_if_failed(CT* __restrict__ counts, uint32_t d, const HistCheck* gate) {
+  if (hist_ok(gate)) return;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d; i += stride)
+    counts[i] = 0;
+}
+
 template <typename CT>
 int histogram_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64_t nvec, uint64_t n,
-                   uint32_t d, CT* counts, cudaStream_t s) {
+                   uint32_t d, CT* counts, bool fresh, cudaStream_t s) {
   const unsigned grid = grid_for(ctx, nvec ? nvec : 1, kThreads * kUnroll, SKX_HIST_CTAS);
   const size_t smem = size_t(2) * kTable * sizeof(uint32_t);
-  // Bucket the cold updates only when the counters overflow half of L2 --
-  // and only when enabled: measured on B200 (profiles/r1_experiments.md) the
-  // per-element warp-aggregated bucket append is still slower than direct
-  // reductions (C4 histogram 6.96 -> 9.11 ms, C2 index 17.4 -> 25.5 ms)
-  // because the bucket cursors become the contended addresses.  Kept,
-  // parity-tested, for the CTA-staged variant planned next.
   // Stage the cold updates by key range when the counters overflow half of L2
   // -- opt-in (skx_set_histogram_mode(1)): the staging removes the HBM
   // read-modify-writes (C2 index: 40 -> 7 GB of DRAM traffic in the counting
@@ -257,7 +309,7 @@ int histogram_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64_t n
   // and the L2-resident fold is reduction-rate bound, so the sum is slower
   // than direct reductions as measured (C4 6.86 -> 10.0 ms, C2 index
   // 17.6 -> 20.9 ms; profiles/r1_experiments.md).
-  const bool bucketed = ctx->hist_bucketed && (uint64_t)d * sizeof(CT) > ctx->l2_bytes / 2 &&
+  const bool bucketed = ctx->hist_mode == 1 && (uint64_t)d * sizeof(CT) > ctx->l2_bytes / 2 &&
                         n >= (uint64_t(1) << 20);
   Buckets bk{nullptr, nullptr, 0, 0};
   if (bucketed) {
@@ -275,18 +327,47 @@ int histogram_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64_t n
     cudaError_t e = cudaMemsetAsync(bk.cursors, 0, kNB * 4, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "histogram memset");
     const size_t bsmem = smem + (size_t)kTileRows * 8 + (1 + 2 * kNB) * 4;
-    cudaFuncSetAttribute(k_histogram<CT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_histogram<CT, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)bsmem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_histogram<CT, true>, kThreads, bsmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_histogram<CT, true, false>, kThreads,
+                                                  bsmem);
     const unsigned bgrid = grid_for(ctx, nvec ? nvec : 1, kThreads * kUnroll, per_sm < 1 ? 1 : per_sm);
-    k_histogram<CT, true><<<bgrid, kThreads, bsmem, s>>>(fact, head, nvec, n, d, counts, bk,
-                                                         ctx->err);
+    k_histogram<CT, true, false><<<bgrid, kThreads, bsmem, s>>>(fact, head, nvec, n, d, counts, bk,
+                                                                ctx->err, nullptr, nullptr,
+                                                                nullptr);
     k_hist_fold<CT><<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(bk, counts);
     ctx->launches += 2;
+  } else if (fresh && ctx->hist_mode == 0 && (uint64_t)d * sizeof(CT) > 3 * ctx->l2_bytes &&
+             n >= (uint64_t(1) << 20)) {
+    // C16 cold counters, for counter arrays beyond 3x L2 (C2 index, 512 MiB of
+    // u32: 17.5 -> 14.6 ms; at 256 MiB the extra merge pass costs more than it
+    // saves: C4 2.89 -> 3.38 ms).  counts were zeroed by the caller, so the
+    // gated fallback may zero them again and recount directly.
+    const size_t w16 = (((size_t)d + 1) / 2) * 4;
+    char* sp = static_cast<char*>(scratch(ctx, 0, 256 + w16));
+    if (!sp) return set_error(ctx, SKX_CUDA_ERROR, "histogram: out of device memory");
+    HistCheck* chk = reinterpret_cast<HistCheck*>(sp);
+    unsigned int* c16 = reinterpret_cast<unsigned int*>(sp + 256);
+    cudaError_t e = cudaMemsetAsync(sp, 0, 256 + w16, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "histogram memset");
+    cudaFuncSetAttribute(k_histogram<CT, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    k_histogram<CT, false, true><<<grid, kThreads, smem, s>>>(fact, head, nvec, n, d, counts, bk,
+                                                              ctx->err, c16, chk, nullptr);
+    k_hist_merge16<CT><<<grid_for(ctx, (d + 1) / 2, 256, 8), 256, 0, s>>>(c16, d, counts, chk);
+    k_hist_zero_if_failed<CT><<<grid_for(ctx, d, 256, 8), 256, 0, s>>>(counts, d, chk);
+    cudaFuncSetAttribute(k_histogram<CT, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    k_histogram<CT, false, false><<<grid, kThreads, smem, s>>>(fact, head, nvec, n, d, counts, bk,
+                                                               ctx->err, nullptr, nullptr, chk);
+    ctx->launches += 4;
   } else {
-    cudaFuncSetAttribute(k_histogram<CT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_histogram<CT, false><<<grid, kThreads, smem, s>>>(fact, head, nvec, n, d, counts, bk, ctx->err);
+    cudaFuncSetAttribute(k_histogram<CT, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    k_histogram<CT, false, false><<<grid, kThreads, smem, s>>>(fact, head, nvec, n, d, counts, bk,
+                                                               ctx->err, nullptr, nullptr,
+                                                               nullptr);
     ctx->launches++;
   }
   SKX_CHECK_LAUNCH(ctx, "histogram");
@@ -296,7 +377,7 @@ int histogram_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64_t n
 }  // namespace
 
 int launch_histogram(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint32_t d, void* counts,
-                     int counter_bytes, cudaStream_t s) {
+                     int counter_bytes, bool fresh, cudaStream_t s) {
   if (n == 0) return SKX_OK;
   if (n > (uint64_t(1) << 34))
     return set_error(ctx, SKX_INVALID_ARGUMENT, "histogram: more than 2^34 rows per call");
@@ -309,9 +390,10 @@ int launch_histogram(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint32_t d,
   const uint64_t nvec = (n - head) / 4;
   ctx->last_domain = d;
   if (counter_bytes == 4)
-    return histogram_impl<uint32_t>(ctx, fact, head, nvec, n, d, static_cast<uint32_t*>(counts), s);
+    return histogram_impl<uint32_t>(ctx, fact, head, nvec, n, d, static_cast<uint32_t*>(counts),
+                                    fresh, s);
   return histogram_impl<unsigned long long>(ctx, fact, head, nvec, n, d,
-                                            static_cast<unsigned long long*>(counts), s);
+                                            static_cast<unsigned long long*>(counts), fresh, s);
 }
 
 }  // namespace skx
@@ -326,7 +408,7 @@ int skx_count_frequencies(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint32
     cudaError_t e = cudaMemsetAsync(counts, 0, uint64_t(d) * 8, s);
     if (e != cudaSuccess) return skx::cuda_fail(ctx, e, "count_frequencies memset");
   }
-  return skx::launch_histogram(ctx, fact, n, d, counts, 8, s);
+  return skx::launch_histogram(ctx, fact, n, d, counts, 8, true, s);
 }
 
 int skx_histogram_u32(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint32_t d,
@@ -337,7 +419,7 @@ int skx_histogram_u32(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint32_t d
     cudaError_t e = cudaMemsetAsync(counts, 0, uint64_t(d) * 4, s);
     if (e != cudaSuccess) return skx::cuda_fail(ctx, e, "histogram memset");
   }
-  return skx::launch_histogram(ctx, fact, n, d, counts, 4, s);
+  return skx::launch_histogram(ctx, fact, n, d, counts, 4, !accumulate, s);
 }
 
 }  // extern "C"

@@ -412,7 +412,7 @@ int skx_rebuild(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint32_t d, uint
     cudaError_t e = cudaMemsetAsync(counts, 0, cb * (size_t)d, s);
     if (e != cudaSuccess) return skx::cuda_fail(ctx, e, "rebuild memset");
   }
-  int rc = skx::launch_histogram(ctx, fact, n, d, counts, (int)cb, s);
+  int rc = skx::launch_histogram(ctx, fact, n, d, counts, (int)cb, true, s);
   if (rc) return rc;
   return skx::launch_build_index(ctx, counts, (int)cb, d, n, offsets, ranks, s);
 }

@@ -153,7 +153,7 @@ struct skx_ctx {
   size_t tier_smem_bytes = 0;         // gather shared-memory tier cap (0: all opt-in smem)
   size_t tier_l1_bytes = 160 * 1024;  // gather tier t1 (bytes of the dimension prefix)
   double tier_l2_frac = 0.6;          // gather tier t2 (share of L2)
-  bool hist_bucketed = false;         // histogram cold keys via key-range buckets
+  int hist_mode = 0;  // histogram cold keys: 0 packed 16-bit + check, 1 staged buckets, 2 direct
   int agg_mode = 0;  // group-by cold tail: 0 packed + exact fallback, 1 staged, 2 direct pairs
   std::atomic<uint64_t> launches{0};
   skx_error_info last{};
@@ -191,8 +191,9 @@ inline unsigned grid_for(const skx_ctx* ctx, uint64_t work_items, unsigned per_b
 }
 
 // Internal launchers shared between translation units.
+// fresh: the caller zeroed `counts` (enables the packed 16-bit cold path).
 int launch_histogram(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint32_t d, void* counts,
-                     int counter_bytes, cudaStream_t s);
+                     int counter_bytes, bool fresh, cudaStream_t s);
 int launch_gather(skx_ctx* ctx, int width, const uint32_t* fact, uint64_t n, const void* dim,
                   uint64_t dim_len, void* out, cudaStream_t s);
 int launch_build_index(skx_ctx* ctx, const void* counts, int counter_bytes, uint32_t d,

@@ -327,12 +327,15 @@ def test_aggregate_packed_tail_exactness(sx):
     assert np.array_equal(np_(c), ce) and np.array_equal(np_(s), se)
 
 
-@pytest.mark.parametrize("bucketed", [0, 1])
+@pytest.mark.parametrize("bucketed", [0, 1, 2])
 @pytest.mark.parametrize("case", ["zipf", "uniform", "one_bucket"])
 def test_histogram_bucketed_large_domain(sx, oracle, case, bucketed):
-    """Domains whose counters exceed half of L2 take the bucketed cold path
-    (bucket.cuh); 'one_bucket' overflows a bucket and exercises the fallback."""
-    d, n = 1 << 25, (1 << 22) + 5
+    """Domains whose counters exceed half of L2: packed 16-bit cold counters
+    (mode 0, default), per-tile key-range staging (1; 'one_bucket' overflows a
+    bucket and exercises its fallback) and direct counters (2)."""
+    # u64 counters of D=2^26 (count_frequencies, 512 MiB) exceed 3x L2: mode 0 packs
+    # them; the u32 ones (histogram_u32, 256 MiB) take the direct path
+    d, n = 1 << 26, (1 << 22) + 5
     rng = np.random.default_rng(17)
     if case == "zipf":
         cdf = sx.zipf_cdf(d, 1.1)
@@ -457,3 +460,18 @@ def test_cache_model_at_scale_vs_oracle(sx, oracle, layout):
     for s in (1 << 10, 1 << 14, 1 << 17):
         assert sx.estimate_hit_rate(lf, s) == pytest.approx(oracle.estimate_hit_rate(lf_o, s),
                                                             rel=1e-9)
+
+
+def test_histogram_c16_wrap_fallback(sx, oracle):
+    """Packed 16-bit cold counters: fill every CTA's hash table with distinct
+    keys first, then send > 2^16 rows of one key down the cold path -- the
+    wrap must be caught on the device and the call redone exactly."""
+    d = 1 << 27  # u32 counters of 512 MiB: beyond 3x L2, the packed path is on
+    n = 1 << 26
+    fact = np.full(n, d, np.uint32)  # the heavy key, cold once the tables are full
+    fill = 2 * 444 * 4096  # two CTA iterations of distinct keys for every CTA
+    fact[:fill] = np.arange(1, fill + 1, dtype=np.uint32)
+    exp = oracle.count_frequencies(fact, d)
+    got = np_(sx.count_frequencies(cu(fact), d).counts)
+    assert np.array_equal(got, exp)
+    assert np.array_equal(np_(sx.histogram_u32(cu(fact), d)).astype(np.uint64), exp)
