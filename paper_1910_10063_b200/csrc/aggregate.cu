@@ -37,7 +37,7 @@ namespace {
 constexpr int kThreads = 1024;
 constexpr int kMaxBuckets = 64;
 #ifndef SKX_AGG_UNROLL
-#define SKX_AGG_UNROLL 2
+#define SKX_AGG_UNROLL 1
 #endif
 constexpr int kAggUnroll = SKX_AGG_UNROLL;
 
@@ -225,18 +225,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   // it streams 4 B/row): all loads first
   // (more bytes in flight per SM), then the updates.
   const uint64_t stride = (uint64_t)gridDim.x * kThreads * U;
+#ifndef SKX_AGG_PIPE
+#define SKX_AGG_PIPE 1
+#endif
   // Block-uniform trip count: the warp collectives below need every lane.
-  for (uint64_t vb0 = (uint64_t)blockIdx.x * kThreads * U; vb0 < nvec; vb0 += stride) {
-    const uint64_t vb = vb0 + threadIdx.x;
-    uint4 f[U];
-    unsigned long long m[U][4];
+  // The next iteration's FK and measure vectors are loaded before this one's
+  // updates (software pipelining), so the streams stay in flight while the
+  // shared-memory and global reductions issue.
+  uint4 f[U];
+  unsigned long long m[U][4];
+  const uint64_t vstart = (uint64_t)blockIdx.x * kThreads * U;
+  auto load = [&](uint64_t vb0, uint4 (&ff)[U], unsigned long long (&mm)[U][4]) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const uint64_t vi = vb + (uint64_t)u * kThreads;
+      const uint64_t vi = vb0 + threadIdx.x + (uint64_t)u * kThreads;
       if (vi < nvec) {
-        f[u] = ld_cs_v4(fv + vi);
-        load_measure4<MW>(measure, head + vi * 4, mvec, pol, m[u]);
+        ff[u] = ld_cs_v4(fv + vi);
+        load_measure4<MW>(measure, head + vi * 4, mvec, pol, mm[u]);
       }
+    }
+  };
+  if (SKX_AGG_PIPE && vstart < nvec) load(vstart, f, m);
+  for (uint64_t vb0 = vstart; vb0 < nvec; vb0 += stride) {
+    const uint64_t vb = vb0 + threadIdx.x;
+    uint4 nf[U];
+    unsigned long long nm[U][4];
+    if (SKX_AGG_PIPE) {
+      if (vb0 + stride < nvec) load(vb0 + stride, nf, nm);
+    } else {
+      load(vb0, f, m);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -252,6 +269,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         // __reduce_add_sync was measured 3.4x slower at Zipf 1.5: the
         // hardware already merges same-address 32-bit shared adds.)
         if (ok) agg_row<MW, PACK>(idx, m[u][j], hot, limit, b, t, pt);
+      }
+    }
+    if (SKX_AGG_PIPE) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        f[u] = nf[u];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) m[u][j] = nm[u][j];
       }
     }
   }
