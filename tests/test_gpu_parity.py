@@ -475,3 +475,31 @@ def test_histogram_c16_wrap_fallback(sx, oracle):
     got = np_(sx.count_frequencies(cu(fact), d).counts)
     assert np.array_equal(got, exp)
     assert np.array_equal(np_(sx.histogram_u32(cu(fact), d)).astype(np.uint64), exp)
+
+
+@pytest.mark.parametrize("d,n,hot", [((1 << 22) + 1, 1000, 0), ((1 << 22) + 1, (1 << 20) + 7, 0),
+                                     ((1 << 23) + 17, (1 << 21) + 3, 5000), (3, 1, 0),
+                                     ((1 << 24), 1 << 22, 0)])
+def test_aggregate_tier_edges(sx, oracle, d, n, hot):
+    """Domain sizes at and around the far-tier switch (D > 2^22), tiny inputs,
+    an explicit hot threshold together with the far tier, both measure widths."""
+    rng = np.random.default_rng(d ^ n)
+    fact = sx.generate_zipf(cu(sx.zipf_cdf(d, 0.9)), n, 13)  # rank space, skewed
+    for dt in (np.int64, np.uint32):
+        meas = rng.integers(0, 3000, size=n).astype(dt)
+        c, s = sx.aggregate_count_sum(fact, cu(meas), d, hot_threshold=hot)
+        ce, se = oracle.aggregate_count_sum(np_(fact), meas.view(np.uint64) if dt == np.int64 else meas, d)
+        assert np.array_equal(np_(c), ce) and np.array_equal(np_(s), se)
+    c = sx.aggregate_count(fact, d, hot_threshold=hot)
+    assert np.array_equal(np_(c), oracle.aggregate_count_sum(np_(fact), None, d)[0])
+
+
+@pytest.mark.parametrize("n", [1, 255, 256, 257, 4097])
+def test_select_tiny_and_slice_edges(sx, oracle, n):
+    """Row counts around the 256-row slice and 4-row vector boundaries."""
+    d = 1000
+    rng = np.random.default_rng(n)
+    fact = rng.integers(1, d + 1, size=n, dtype=np.uint32)
+    bm = sx.build_bitmap_lt(cu(rng.integers(0, 1000, size=d, dtype=np.int32)), 300)
+    got = np_(sx.select(cu(fact), bm))
+    assert np.array_equal(got, oracle.select_offsets(fact, np_(bm.words), d))
