@@ -13,7 +13,8 @@
 // private hot region.  Bins use 32-bit shared atomics only: sm_100a has no
 // native 64-bit shared add (it compiles to a compare-and-swap spin loop that
 // serialises on the hottest keys), while 32-bit adds are native and merge
-// same-address lanes.  A 64-bit per-bin sum is kept as lo/hi words.
+// same-address lanes.  A bin is {u32 count, u32 sum lo}; the rare bits above
+// 32 go straight to the key's global sum.
 //
 // Tail keys (id > H), default "packed" mode: ONE fire-and-forget 64-bit
 // reduction of (1 << 40 | m) per cold row into an 8 B/key accumulator, so a
@@ -29,6 +30,10 @@
 // mismatch three gated kernels, already queued behind the decode, redo the
 // whole call with two exact reductions per cold row on an interleaved
 // {count, sum} pair (mode 2); otherwise they exit at once.  No host sync.
+// For domains above 2^22 the rarest keys (ids >= 2^18 per 2^30 rows) use
+// 4-byte words (count << 21 | sum) under the same check, so the accumulator
+// set fits the ~64 MB the L2 offers random accesses.  COUNT-only calls count
+// into exact u32 counters (below 2^32 rows) widened at the end.
 #include "skx_internal.cuh"
 
 namespace skx {

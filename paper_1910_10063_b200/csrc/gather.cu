@@ -12,16 +12,17 @@
 //  * HBM roofline: algorithmic bytes per row = 4 (FK) + w (output).  The
 //    dimension reads are data-dependent and are what the skew-aware index
 //    turns into on-chip hits: the reordered hot ids form a contiguous prefix.
-//  * FK stream: 128-bit ld.global.nc.L1::no_allocate with an L2 evict_first
-//    policy; output: 128-bit st.global with evict_first.
+//  * Default policy 129 (profiles/r1_experiments.md): FK stream as 128-bit
+//    ld.global.cs, output as 128-bit st.global.cs, dimension loads on the
+//    read-only path (ld.global.nc, L1-allocating) with an L2 evict_last hint.
+//    The other policy bits are measured alternatives kept for tuning:
 //  * Hot prefix (policy bit 2): the first `hot` dimension values are staged
 //    in shared memory once per CTA (one 1024-thread CTA per SM) and served
-//    from there -- a random shared load costs a few bank wavefronts where a
-//    random global load costs one L1TEX wavefront per lane.
-//  * Remaining dimension loads take the read-only path with L2 evict_last,
-//    optionally without L1 allocation and under an L2 persisting window.
-//  * Each thread keeps UNROLL x 4 independent loads in flight; persistent
-//    grid-stride loop.
+//    from there -- slower in practice: the carve-out starves L1.
+//  * L1 no-allocate / coherent / L2-only dimension loads, an L2 persisting
+//    window, per-id tiered priorities, FK software prefetch: no gain on B200.
+//  * Each thread keeps 32 independent dimension loads in flight (8 FK
+//    vectors); persistent grid-stride loop, 2 CTAs/SM (8/SM for long columns).
 #include "skx_internal.cuh"
 
 namespace skx {
