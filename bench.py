@@ -534,6 +534,26 @@ def run_ours(args):
         cpu = cpu_gather_baseline(data.fact_freq[:m].cpu().numpy(),
                                   data.dim_freq.cpu().numpy().view(np.uint64))
 
+    if not args.no_extras:
+        # The rest of the BASELINE C2 sweep (s = 0.5 and 1.5; s = 1.0 is the headline),
+        # both layouts, same kernel and timing rules.
+        sweep = {}
+        for zz in (0.5, 1.5):
+            g = ds_mod.make_gather_dataset(d, n_total, zz, SEED, torch.int64, shard)
+            for lay, f, dm in (("freq", g.fact_freq, g.dim_freq), ("rand", g.fact_rand, g.dim_rand)):
+                ts, per_s, _ = timed_launches(
+                    lambda f=f, dm=dm: sx.materialize(f, dm, out=out, ctx=ctx, sync=False),
+                    max(3, min(args.steps, 10)), args.warmup, stream, dist_on)
+                ts = max_over_ranks(ts, dist_on)
+                ms = ts / max(3, min(args.steps, 10))
+                sweep[f"s{zz}_{lay}"] = {"ms_per_step": ms,
+                                         "value": n_total / (ms * 1e-3), "unit": "rows/s",
+                                         "roofline_frac": alg_bytes / (statistics.mean(per_s) * 1e-3)
+                                         / 1e9 / peak}
+            del g
+            torch.cuda.empty_cache()
+        extras["c2_s_sweep"] = sweep
+
     groupby = None
     if not args.no_extras:
         del data, out, out_freq
