@@ -1,5 +1,6 @@
 """The reference's OWN test files for the path (proj/tests/test_permindex.cpp,
-test_operators.cpp, test_parallel.cpp, test_cachemodel.cpp), compiled unmodified by oracle/Makefile
+test_operators.cpp, test_parallel.cpp, test_cachemodel.cpp, test_columns.cpp), compiled
+unmodified by oracle/Makefile
 against the B200 drop-in (paper_1910_10063_b200/cpp/include + libskewdx_b200.so,
 every hot-path call on the GPU) and a minimal doctest-compatible shim.  They
 must pass on a B200 exactly as they pass against the reference library."""
@@ -10,7 +11,7 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REF = os.path.join(ROOT, "oracle", "_ref")
-SUITES = ["test_permindex", "test_operators", "test_parallel", "test_cachemodel"]
+SUITES = ["test_permindex", "test_operators", "test_parallel", "test_cachemodel", "test_columns"]
 
 pytestmark = pytest.mark.gpu
 

@@ -110,3 +110,16 @@ def test_cpp_dropin_exports_reference_api():
                "skewdx::generate_fact_column(", "skewdx::read_index(", "skewdx::write_index("]:
         assert fn in syms, fn
     assert "libskx.so" in os.popen(f"ldd {so}").read()
+
+
+def test_reference_columns_suite_on_host():
+    """The reference's own proj/tests/test_columns.cpp (generator, random_bijection,
+    SKDX/SKC8 file I/O -- host-side in the drop-in too) built against the drop-in
+    headers by oracle/Makefile; needs no GPU."""
+    import subprocess
+    exe = os.path.join(ROOT, "oracle", "_ref", "refsuite_test_columns")
+    if not os.path.exists(exe):
+        pytest.skip("refsuite not built (make -C oracle refsuite needs /root/reference)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "0 failed" in r.stdout
