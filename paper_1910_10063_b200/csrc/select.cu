@@ -41,6 +41,14 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kWarpRows = 256;                 // rows per warp slice
 constexpr int kItems = kWarpRows / 128;        // 4 items of 128 rows (4 per lane)
 constexpr uint32_t kCap = 64;                  // compacted entries kept per slice
+#ifndef SKX_SEL_GROUP
+#define SKX_SEL_GROUP 4
+#endif
+#ifndef SKX_SEL_PER
+#define SKX_SEL_PER 4
+#endif
+constexpr int kGroup = SKX_SEL_GROUP;          // pass 2: slices per warp iteration
+constexpr int kPer = SKX_SEL_PER;              // pass 2: entries per lane in flight
 constexpr int kThreads1 = 1024;                // pass 1 CTA (shares one bitmap prefix)
 constexpr uint32_t kSmemCategories = 2048;     // fp64 fallback: 8 warps x 2048 x 8 B
 constexpr uint32_t kFixedCategories = 4096;    // fixed point: 3 x 4096 x 4 B per CTA
@@ -210,10 +218,67 @@ __device__ __forceinline__ uint32_t item_count(const uint32_t (&b)[4]) {
   return __popc(b[0]) + __popc(b[1]) + __popc(b[2]) + __popc(b[3]);
 }
 
+// 8 consecutive FKs of one lane (16-byte aligned): one 256-bit load when
+// 32-byte aligned, else two 128-bit loads.
+__device__ __forceinline__ void load_rows8(const uint32_t* p, bool v8, uint32_t (&fk)[8]) {
+  if (v8) {
+    asm volatile("ld.global.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(fk[0]), "=r"(fk[1]), "=r"(fk[2]), "=r"(fk[3]), "=r"(fk[4]), "=r"(fk[5]),
+                   "=r"(fk[6]), "=r"(fk[7])
+                 : "l"(p));
+  } else {
+    const uint4 a = __ldcs(reinterpret_cast<const uint4*>(p));
+    const uint4 b = __ldcs(reinterpret_cast<const uint4*>(p) + 1);
+    fk[0] = a.x, fk[1] = a.y, fk[2] = a.z, fk[3] = a.w;
+    fk[4] = b.x, fk[5] = b.y, fk[6] = b.z, fk[7] = b.w;
+  }
+}
+
+// Pass 1, any slice (unaligned column, empty domain): per-item ballots.
+template <bool VEC>
+__device__ __forceinline__ void count_slice_generic(const uint32_t* __restrict__ fact, uint64_t n,
+                                                 uint64_t sl, const uint32_t* __restrict__ words32,
+                                                 uint32_t bits32, uint32_t sw, uint32_t s_base,
+                                                 uint2* __restrict__ entries,
+                                                 uint32_t* __restrict__ slice_counts, DevErr* err) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
+  const uint64_t row0 = sl * kWarpRows;
+  const bool full = row0 + kWarpRows <= n;  // warp-uniform
+  uint32_t fk[kItems][4];
+  load_slice<VEC>(fact, n, row0, full, lane, fk);
+  uint32_t sel[kItems];
+  if (full)
+    probe_slice<true>(fk, row0, n, bits32, sw, s_base, words32, lane, err, sel);
+  else
+    probe_slice<false>(fk, row0, n, bits32, sw, s_base, words32, lane, err, sel);
+  uint2* out = entries + sl * kCap;
+  const uint32_t row_l = (uint32_t)row0 + 4u * lane;  // n < 2^32
+  uint32_t run = 0;
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    uint32_t b[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = __ballot_sync(0xffffffffu, (sel[i] >> j) & 1u);
+    if (sel[i]) {
+      uint32_t pos = run + item_base(b, lt);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if ((sel[i] >> j) & 1u) {
+          if (pos < kCap) out[pos] = make_uint2(fk[i][j] - 1u, row_l + i * 128 + j);
+          ++pos;
+        }
+      }
+    }
+    run += item_count(b);
+  }
+  if (lane == 0) slice_counts[sl] = run;
+}
+
 // Pass 1: probe every row once; each warp compacts its slice's selected rows
 // (dimension index, row) in row order into entries[slice][kCap] and writes
 // the slice count.
-template <bool VEC>
+template <bool VEC, bool FAST>
 __global__ void __launch_bounds__(kThreads1, 1)
     k_select_count(const uint32_t* __restrict__ fact, uint64_t n,
                    const uint32_t* __restrict__ words32, uint64_t bits,
@@ -224,42 +289,79 @@ __global__ void __launch_bounds__(kThreads1, 1)
   const uint64_t nslices = (n + kWarpRows - 1) / kWarpRows;
   const uint32_t bits32 = bits < 0xFFFFFFFFull ? (uint32_t)bits : 0xFFFFFFFFu;
   const uint32_t s_base = (uint32_t)__cvta_generic_to_shared(s_words);
-  const uint32_t lt = lanemask_lt();
   for (uint32_t i = threadIdx.x; i < sw; i += kThreads1) s_words[i] = __ldg(words32 + i);
   __syncthreads();
+  const uint32_t maxw = bits32 ? (bits32 - 1u) >> 5 : 0u;
+  const bool v8 = (reinterpret_cast<uintptr_t>(fact) & 31u) == 0;
   const uint64_t warps = (uint64_t)gridDim.x * (kThreads1 / 32);
   for (uint64_t sl = (uint64_t)blockIdx.x * (kThreads1 / 32) + (threadIdx.x >> 5); sl < nslices;
        sl += warps) {
     const uint64_t row0 = sl * kWarpRows;
     const bool full = row0 + kWarpRows <= n;  // warp-uniform
-    uint32_t fk[kItems][4];
-    load_slice<VEC>(fact, n, row0, full, lane, fk);
-    uint32_t sel[kItems];
-    if (full)
-      probe_slice<true>(fk, row0, n, bits32, sw, s_base, words32, lane, err, sel);
-    else
-      probe_slice<false>(fk, row0, n, bits32, sw, s_base, words32, lane, err, sel);
-    uint2* out = entries + sl * kCap;
-    const uint32_t row_l = (uint32_t)row0 + 4u * lane;  // n < 2^32
-    uint32_t run = 0;
+    if constexpr (FAST) {
+      // Fast path: lane l owns the 8 consecutive rows row0 + 8l + j, so the
+      // slice's row order is (lane, j) and one warp scan of the per-lane
+      // counts places every selected row -- ~half the instructions of the
+      // per-item ballots below (pass 1 is issue-bound).  Out-of-domain ids
+      // read a clamped word; their rows are reported (the call fails), so
+      // their selection bit does not matter.
+      uint32_t fk[8];
+      uint32_t live = 0xffu;
+      if (full) {
+        load_rows8(fact + row0 + 8 * lane, v8, fk);
+      } else {  // the column's last slice
+        live = 0u;
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-      uint32_t b[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = __ballot_sync(0xffffffffu, (sel[i] >> j) & 1u);
-      if (sel[i]) {
-        uint32_t pos = run + item_base(b, lt);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if ((sel[i] >> j) & 1u) {
-            if (pos < kCap) out[pos] = make_uint2(fk[i][j] - 1u, row_l + i * 128 + j);
-            ++pos;
-          }
+        for (int j = 0; j < 8; ++j) {
+          const uint64_t r = row0 + 8 * lane + j;
+          fk[j] = r < n ? __ldcs(fact + r) : 1u;
+          live |= (r < n ? 1u : 0u) << j;
         }
       }
-      run += item_count(b);
+      uint32_t sel = 0;
+      bool bad = false;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t idx = fk[j] - 1u;
+        bad |= idx >= bits32;  // padding rows read id 1
+        const uint32_t wv = probe_word(min(idx >> 5, maxw), sw, s_base, words32);
+        sel |= ((wv >> (idx & 31)) & 1u) << j;
+      }
+      sel &= live;
+      if (__any_sync(0xffffffffu, bad)) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (((live >> j) & 1u) && fk[j] - 1u >= bits32) record_violation(err, row0 + 8 * lane + j, fk[j]);
+      }
+      const uint32_t c = __popc(sel);
+      uint32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const uint32_t row_l = (uint32_t)row0 + 8u * lane;  // n < 2^32
+      if (sel) {
+        uint32_t pos = incl - c;
+        uint2* o = entries + sl * kCap + pos;
+        if (incl <= kCap) {  // all of this lane's rows fit: predicated stores only
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if ((sel >> j) & 1u) *o++ = make_uint2(fk[j] - 1u, row_l + j);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if ((sel >> j) & 1u) {
+              if (pos < kCap) *o = make_uint2(fk[j] - 1u, row_l + j);
+              ++o, ++pos;
+            }
+        }
+      }
+      if (lane == 31) slice_counts[sl] = incl;
+    } else {
+      count_slice_generic<VEC>(fact, n, sl, words32, bits32, sw, s_base, entries, slice_counts,
+                               err);
     }
-    if (lane == 0) slice_counts[sl] = run;
   }
 }
 
@@ -298,10 +400,11 @@ __device__ __forceinline__ void emit_row(uint64_t p, uint32_t row, const Rec8& r
   }
 }
 
-// Pass 2: every warp takes slices; a slice's selected rows go to
+// Pass 2: every warp takes groups of slices; a slice's selected rows go to
 // slice_off[slice] + rank.  Slices with <= kCap rows copy pass 1's entries
-// (4 independent rows per lane in flight); denser slices are re-derived from
-// the FK column and the bitmap (global probes).
+// (a group's entries flattened over the lanes, kPer rows per lane in flight);
+// denser slices are re-derived from the FK column and the bitmap (global
+// probes).
 template <bool FUSED, bool VEC>
 __global__ void __launch_bounds__(kThreads)
     k_select_write(const uint32_t* __restrict__ fact, uint64_t n,
@@ -328,55 +431,102 @@ __global__ void __launch_bounds__(kThreads)
   const uint32_t bits32 = bits < 0xFFFFFFFFull ? (uint32_t)bits : 0xFFFFFFFFu;
   const uint32_t lt = lanemask_lt();
   const uint64_t warps = (uint64_t)gridDim.x * kWarps;
-  for (uint64_t sl = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); sl < nslices;
-       sl += warps) {
-    const uint32_t cnt = __ldg(slice_counts + sl);
-    const uint64_t ob = __ldg(slice_off + sl);
+  // One slice at a time: its entries, or (dense) a re-derivation from the FK
+  // column and the bitmap.
+  auto write_slice = [&](uint64_t sl, uint32_t cnt, uint64_t ob) {
     if (cnt <= kCap) {
       const uint2* src = entries + sl * kCap;
-      for (uint32_t j0 = 0; j0 < cnt; j0 += 64) {
-        // two entries per lane: both record loads in flight before any store
-        const uint32_t ja = j0 + lane, jb = j0 + 32 + lane;
+      for (uint32_t j0 = 0; j0 < cnt; j0 += 32) {
+        const uint32_t ja = j0 + lane;
         const uint2 ea = ja < cnt ? __ldcs(src + ja) : make_uint2(0u, 0u);
-        const uint2 eb = jb < cnt ? __ldcs(src + jb) : make_uint2(0u, 0u);
-        Rec8 ra{}, rb{};
-        if (FUSED) {
-          if (ja < cnt) ra = load_rec(cols.rec, ea.x);
-          if (jb < cnt) rb = load_rec(cols.rec, eb.x);
-        }
+        Rec8 ra{};
+        if (FUSED && ja < cnt) ra = load_rec(cols.rec, ea.x);
         if (ja < cnt) emit_row<FUSED>(ob + ja, ea.y, ra, base_off, out_off, cols, fixed, S, s_acc);
-        if (jb < cnt) emit_row<FUSED>(ob + jb, eb.y, rb, base_off, out_off, cols, fixed, S, s_acc);
       }
-    } else {
-      const uint64_t row0 = sl * kWarpRows;
-      const bool full = row0 + kWarpRows <= n;
-      uint32_t fk[kItems][4];
-      load_slice<VEC>(fact, n, row0, full, lane, fk);
-      uint32_t sel[kItems];
-      // domain already checked in pass 1 (err = nullptr)
-      if (full)
-        probe_slice<true>(fk, row0, n, bits32, 0u, 0u, words32, lane, nullptr, sel);
-      else
-        probe_slice<false>(fk, row0, n, bits32, 0u, 0u, words32, lane, nullptr, sel);
-      const uint32_t row_l = (uint32_t)row0 + 4u * lane;
-      uint32_t run = 0;
+      return;
+    }
+    const uint64_t row0 = sl * kWarpRows;
+    const bool full = row0 + kWarpRows <= n;
+    uint32_t fk[kItems][4];
+    load_slice<VEC>(fact, n, row0, full, lane, fk);
+    uint32_t sel[kItems];
+    // domain already checked in pass 1 (err = nullptr)
+    if (full)
+      probe_slice<true>(fk, row0, n, bits32, 0u, 0u, words32, lane, nullptr, sel);
+    else
+      probe_slice<false>(fk, row0, n, bits32, 0u, 0u, words32, lane, nullptr, sel);
+    const uint32_t row_l = (uint32_t)row0 + 4u * lane;
+    uint32_t run = 0;
 #pragma unroll
-      for (int i = 0; i < kItems; ++i) {
-        uint32_t b[4];
+    for (int i = 0; i < kItems; ++i) {
+      uint32_t b[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) b[j] = __ballot_sync(0xffffffffu, (sel[i] >> j) & 1u);
-        uint32_t pos = run + item_base(b, lt);
+      for (int j = 0; j < 4; ++j) b[j] = __ballot_sync(0xffffffffu, (sel[i] >> j) & 1u);
+      uint32_t pos = run + item_base(b, lt);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if ((sel[i] >> j) & 1u) {
-            Rec8 r{};
-            if (FUSED) r = load_rec(cols.rec, fk[i][j] - 1u);
-            emit_row<FUSED>(ob + pos, row_l + i * 128 + j, r, base_off, out_off, cols, fixed, S,
-                            s_acc);
-            ++pos;
-          }
+      for (int j = 0; j < 4; ++j) {
+        if ((sel[i] >> j) & 1u) {
+          Rec8 r{};
+          if (FUSED) r = load_rec(cols.rec, fk[i][j] - 1u);
+          emit_row<FUSED>(ob + pos, row_l + i * 128 + j, r, base_off, out_off, cols, fixed, S,
+                          s_acc);
+          ++pos;
         }
-        run += item_count(b);
+      }
+      run += item_count(b);
+    }
+  };
+  // Warps take groups of kGroup consecutive slices.  Their outputs are one
+  // contiguous run (slice offsets are the exclusive scan of the counts), so
+  // the group's entries are flattened over the lanes: up to kPer entries per
+  // lane with all entry and record loads in flight before any store -- a
+  // slice alone holds ~20 selected rows at C5's selectivity, too few to hide
+  // the count -> entries -> record latency chain.
+  const uint64_t ngroups = (nslices + kGroup - 1) / kGroup;
+  for (uint64_t g = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); g < ngroups; g += warps) {
+    const uint64_t sl0 = g * kGroup;
+    const uint32_t ns = (uint32_t)(nslices - sl0 < (uint64_t)kGroup ? nslices - sl0 : kGroup);
+    const uint32_t c_l = (uint32_t)lane < ns ? __ldg(slice_counts + sl0 + lane) : 0u;
+    const uint64_t ob0 = __ldg(slice_off + sl0);
+    if (__any_sync(0xffffffffu, c_l > kCap)) {  // a dense slice: one slice at a time
+      for (uint32_t s2 = 0; s2 < ns; ++s2) {
+        const uint32_t c = __shfl_sync(0xffffffffu, c_l, (int)s2);
+        write_slice(sl0 + s2, c, s2 ? (uint64_t)__ldg(slice_off + sl0 + s2) : ob0);
+      }
+      continue;
+    }
+    uint32_t pre[kGroup];  // warp-uniform inclusive prefix of the counts
+    uint32_t acc = 0;
+#pragma unroll
+    for (int s2 = 0; s2 < kGroup; ++s2) {
+      acc += __shfl_sync(0xffffffffu, c_l, s2);
+      pre[s2] = acc;
+    }
+    const uint32_t T = pre[kGroup - 1];
+    for (uint32_t j0 = 0; j0 < T; j0 += 32 * kPer) {
+      uint2 e[kPer];
+      Rec8 r[kPer];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const uint32_t f = j0 + u * 32 + lane;
+        e[u] = make_uint2(0u, 0u);
+        if (f < T) {
+          uint32_t s2 = 0, pb = 0;
+#pragma unroll
+          for (int q = 0; q < kGroup - 1; ++q)
+            if (f >= pre[q]) s2 = q + 1, pb = pre[q];
+          e[u] = __ldcs(entries + (sl0 + s2) * kCap + (f - pb));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        r[u] = Rec8{};
+        if (FUSED && j0 + u * 32 + lane < T) r[u] = load_rec(cols.rec, e[u].x);
+      }
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const uint32_t f = j0 + u * 32 + lane;
+        if (f < T) emit_row<FUSED>(ob0 + f, e[u].y, r[u], base_off, out_off, cols, fixed, S, s_acc);
       }
     }
   }
@@ -549,7 +699,8 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
   const size_t smem1 = (size_t)sw * 4;
   const uint64_t cta1 = (nslices + kThreads1 / 32 - 1) / (kThreads1 / 32);
   const unsigned grid1 = (unsigned)(cta1 < (uint64_t)ctx->num_sms ? cta1 : ctx->num_sms);
-  auto k1 = vec ? k_select_count<true> : k_select_count<false>;
+  auto k1 = vec ? (bits ? k_select_count<true, true> : k_select_count<true, false>)
+                : k_select_count<false, false>;
   cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
   k1<<<grid1, kThreads1, smem1, s>>>(fact, n, w32, bits, entries, counts, sw, ctx->err);
   ctx->launches++;

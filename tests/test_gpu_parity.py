@@ -503,3 +503,29 @@ def test_select_tiny_and_slice_edges(sx, oracle, n):
     bm = sx.build_bitmap_lt(cu(rng.integers(0, 1000, size=d, dtype=np.int32)), 300)
     got = np_(sx.select(cu(fact), bm))
     assert np.array_equal(got, oracle.select_offsets(fact, np_(bm.words), d))
+
+
+@pytest.mark.parametrize("off", [0, 4, 8])
+def test_select_fast_path_alignment_and_tail(sx, oracle, off):
+    """Pass 1's fast path: 32-byte aligned (one 256-bit load per lane), 16-byte
+    aligned (two 128-bit loads), a partial last slice, a mixed-density bitmap,
+    and the first out-of-domain row inside the last slice."""
+    from paper_1910_10063_b200 import DomainViolation
+    d, n = 1 << 14, (1 << 18) + 77
+    rng = np.random.default_rng(off)
+    buf = cu(rng.integers(1, d + 1, size=n + off, dtype=np.uint32))
+    fact = buf[off:]
+    cat = rng.integers(0, 1000, size=d, dtype=np.int32)
+    cat[:64] = 0  # the hottest-looking ids always selected: dense and sparse slices mix
+    f_np = np_(fact)
+    f_np[: 1 << 12] = rng.integers(1, 65, size=1 << 12, dtype=np.uint32)
+    fact.copy_(cu(f_np))
+    bm = sx.build_bitmap_lt(cu(cat), 100)
+    got = np_(sx.select(fact, bm, base=5))
+    assert np.array_equal(got, oracle.select_offsets(f_np, np_(bm.words), d, base=5))
+    bad = f_np.copy()
+    bad[n - 3] = d + 1
+    bad[n - 1] = 0
+    with pytest.raises(DomainViolation) as e:
+        sx.select(cu(bad), bm)
+    assert e.value.row() == n - 3 and e.value.value() == d + 1
