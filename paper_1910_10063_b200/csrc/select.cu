@@ -44,6 +44,12 @@ constexpr uint32_t kCap = 64;                  // compacted entries kept per sli
 #ifndef SKX_SEL_GROUP
 #define SKX_SEL_GROUP 4
 #endif
+#ifndef SKX_SEL_P2_MINB
+#define SKX_SEL_P2_MINB 3   // pass 2 CTAs per SM the registers must allow (80 regs)
+#endif
+#ifndef SKX_SEL_P1_PREF
+#define SKX_SEL_P1_PREF 0   // pass 1: next slice's FKs in flight while probing
+#endif
 #ifndef SKX_SEL_PER
 #define SKX_SEL_PER 4
 #endif
@@ -294,74 +300,96 @@ __global__ void __launch_bounds__(kThreads1, 1)
   const uint32_t maxw = bits32 ? (bits32 - 1u) >> 5 : 0u;
   const bool v8 = (reinterpret_cast<uintptr_t>(fact) & 31u) == 0;
   const uint64_t warps = (uint64_t)gridDim.x * (kThreads1 / 32);
-  for (uint64_t sl = (uint64_t)blockIdx.x * (kThreads1 / 32) + (threadIdx.x >> 5); sl < nslices;
-       sl += warps) {
-    const uint64_t row0 = sl * kWarpRows;
-    const bool full = row0 + kWarpRows <= n;  // warp-uniform
-    if constexpr (FAST) {
-      // Fast path: lane l owns the 8 consecutive rows row0 + 8l + j, so the
-      // slice's row order is (lane, j) and one warp scan of the per-lane
-      // counts places every selected row -- ~half the instructions of the
-      // per-item ballots below (pass 1 is issue-bound).  Out-of-domain ids
-      // read a clamped word; their rows are reported (the call fails), so
-      // their selection bit does not matter.
-      uint32_t fk[8];
-      uint32_t live = 0xffu;
-      if (full) {
-        load_rows8(fact + row0 + 8 * lane, v8, fk);
-      } else {  // the column's last slice
-        live = 0u;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint64_t r = row0 + 8 * lane + j;
-          fk[j] = r < n ? __ldcs(fact + r) : 1u;
-          live |= (r < n ? 1u : 0u) << j;
-        }
-      }
-      uint32_t sel = 0;
-      bool bad = false;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t idx = fk[j] - 1u;
-        bad |= idx >= bits32;  // padding rows read id 1
-        const uint32_t wv = probe_word(min(idx >> 5, maxw), sw, s_base, words32);
-        sel |= ((wv >> (idx & 31)) & 1u) << j;
-      }
-      sel &= live;
-      if (__any_sync(0xffffffffu, bad)) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (((live >> j) & 1u) && fk[j] - 1u >= bits32) record_violation(err, row0 + 8 * lane + j, fk[j]);
-      }
-      const uint32_t c = __popc(sel);
-      uint32_t incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      const uint32_t row_l = (uint32_t)row0 + 8u * lane;  // n < 2^32
-      if (sel) {
-        uint32_t pos = incl - c;
-        uint2* o = entries + sl * kCap + pos;
-        if (incl <= kCap) {  // all of this lane's rows fit: predicated stores only
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if ((sel >> j) & 1u) *o++ = make_uint2(fk[j] - 1u, row_l + j);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if ((sel >> j) & 1u) {
-              if (pos < kCap) *o = make_uint2(fk[j] - 1u, row_l + j);
-              ++o, ++pos;
-            }
-        }
-      }
-      if (lane == 31) slice_counts[sl] = incl;
-    } else {
+  const uint64_t first = (uint64_t)blockIdx.x * (kThreads1 / 32) + (threadIdx.x >> 5);
+  if constexpr (!FAST) {
+    for (uint64_t sl = first; sl < nslices; sl += warps)
       count_slice_generic<VEC>(fact, n, sl, words32, bits32, sw, s_base, entries, slice_counts,
                                err);
+    return;
+  }
+  // Fast path: lane l owns the 8 consecutive rows row0 + 8l + j, so the
+  // slice's row order is (lane, j) and one warp scan of the per-lane counts
+  // places every selected row -- ~half the instructions of the per-item
+  // ballots of the generic path (pass 1 is issue-bound).  Out-of-domain ids
+  // read a clamped word; their rows are reported (the call fails), so their
+  // selection bit does not matter.  The next slice's FKs are loaded before
+  // this one is probed (SKX_SEL_P1_PREF).
+  auto load8 = [&](uint64_t sl, uint32_t (&fk)[8]) -> uint32_t {  // returns the live-row mask
+    const uint64_t row0 = sl * kWarpRows;
+    if (sl >= nslices) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) fk[j] = 1u;
+      return 0u;
     }
+    if (row0 + kWarpRows <= n) {
+      load_rows8(fact + row0 + 8 * lane, v8, fk);
+      return 0xffu;
+    }
+    uint32_t live = 0u;  // the column's last slice
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint64_t r = row0 + 8 * lane + j;
+      fk[j] = r < n ? __ldcs(fact + r) : 1u;
+      live |= (r < n ? 1u : 0u) << j;
+    }
+    return live;
+  };
+  uint32_t fk[8];
+  uint32_t live = load8(first, fk);
+  for (uint64_t sl = first; sl < nslices; sl += warps) {
+    const uint64_t row0 = sl * kWarpRows;
+#if SKX_SEL_P1_PREF
+    uint32_t fkn[8];
+    const uint32_t liven = load8(sl + warps, fkn);
+#endif
+    uint32_t sel = 0;
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t idx = fk[j] - 1u;
+      bad |= idx >= bits32;  // padding rows read id 1
+      const uint32_t wv = probe_word(min(idx >> 5, maxw), sw, s_base, words32);
+      sel |= ((wv >> (idx & 31)) & 1u) << j;
+    }
+    sel &= live;
+    if (__any_sync(0xffffffffu, bad)) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (((live >> j) & 1u) && fk[j] - 1u >= bits32)
+          record_violation(err, row0 + 8 * lane + j, fk[j]);
+    }
+    const uint32_t c = __popc(sel);
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const uint32_t row_l = (uint32_t)row0 + 8u * lane;  // n < 2^32
+    if (sel) {
+      uint32_t pos = incl - c;
+      uint2* o = entries + sl * kCap + pos;
+      if (incl <= kCap) {  // all of this lane's rows fit: predicated stores only
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if ((sel >> j) & 1u) *o++ = make_uint2(fk[j] - 1u, row_l + j);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if ((sel >> j) & 1u) {
+            if (pos < kCap) *o = make_uint2(fk[j] - 1u, row_l + j);
+            ++o, ++pos;
+          }
+      }
+    }
+    if (lane == 31) slice_counts[sl] = incl;
+#if SKX_SEL_P1_PREF
+#pragma unroll
+    for (int j = 0; j < 8; ++j) fk[j] = fkn[j];
+    live = liven;
+#else
+    live = load8(sl + warps, fk);
+#endif
   }
 }
 
@@ -406,7 +434,7 @@ __device__ __forceinline__ void emit_row(uint64_t p, uint32_t row, const Rec8& r
 // denser slices are re-derived from the FK column and the bitmap (global
 // probes).
 template <bool FUSED, bool VEC>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, SKX_SEL_P2_MINB)
     k_select_write(const uint32_t* __restrict__ fact, uint64_t n,
                    const uint32_t* __restrict__ words32, uint64_t bits,
                    const uint2* __restrict__ entries, const uint32_t* __restrict__ slice_counts,
