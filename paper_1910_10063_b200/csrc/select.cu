@@ -9,15 +9,16 @@
 //
 // B200 design: two passes with a device scan
 // between them, no inter-CTA ordering inside a kernel.  Pass 1 streams the
-// FK column once (128-bit loads, 4 rows per lane; the bitmap prefix that
-// holds the hot ids of a reordered column sits in shared memory), and every
-// warp compacts the selected rows of its 512-row slice in row order into a
-// private slot of up to 128 (dimension index, row) entries plus a count.  The
-// scan turns the 2^k slice counts into output offsets.  Pass 2 walks the
-// slices: each warp copies its entries to offset + rank -- ascending row
-// order, exactly the reference's chunk-ordered concatenation -- so the FK
-// column is read once.  A slice with more than 128 selected rows (dense
-// selections) is re-derived in pass 2 from the FK column and the bitmap.
+// FK column once (one 256-bit load of 8 consecutive rows per lane; the bitmap
+// prefix that holds the hot ids of a reordered column sits in shared memory),
+// and every warp places the selected rows of its 256-row slice in row order
+// (one warp scan of the lanes' popcounts) into a private slot of up to 64
+// (dimension index, row) entries plus a count.  The scan turns the slice
+// counts into output offsets.  Pass 2 walks groups of 4 slices: each warp
+// copies their entries (flattened over the lanes) to offset + rank --
+// ascending row order, exactly the reference's chunk-ordered concatenation --
+// so the FK column is read once.  A slice with more than 64 selected rows
+// (dense selections) is re-derived in pass 2 from the FK column and bitmap.
 // (A single-pass decoupled look-back version was measured ~2x slower on
 // B200, profiles/r1_experiments.md.)
 //
