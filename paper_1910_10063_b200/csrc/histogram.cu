@@ -5,20 +5,22 @@
 //
 // B200 design.  Before the reorder the hot
 // keys are scattered ids (a Zipf(1.25) key alone is ~22% of all rows), so:
-//  1. every lane adds 1 to a per-CTA shared-memory open-addressing table
-//     (key -> count) that captures the keys the CTA sees first -- for skewed
-//     data the hot ones -- claiming slots with CAS; same-key lanes of a warp
-//     are merged by the shared-memory atomic unit itself (a __match_any_sync
-//     pre-aggregation was measured 2.4x slower at C4);
-//  3. a key that finds no slot within kProbe probes is cold: for small
-//     domains (counters L2-resident) it is a global red.add; for large ones
-//     (counters >> L2) the CTA collects the cold (key, count) pairs of each
-//     4096-row tile in shared memory, partitions them by key range (64
-//     ranges) and appends each range's run to that range's global bucket
-//     with one cursor atomic; a second kernel applies each bucket while its
-//     counter slice is L2-resident -- so no cold update read-modify-writes an
-//     HBM line (on B200 every L2 miss moves a 128-byte line,
-//     profiles/r1_experiments.md §7);
+//  1. every lane adds 1 to a per-CTA shared-memory table (key -> count)
+//     that captures the keys the CTA sees first -- for skewed data the hot
+//     ones -- claiming slots with CAS.  Each key has two candidate slots,
+//     read together (no probe loop for the warp to diverge on); same-key
+//     lanes of a warp are merged by the shared-memory atomic unit itself (a
+//     __match_any_sync pre-aggregation was measured 2.4x slower at C4);
+//  2. a key with neither slot is cold: a global red.add into the counters
+//     (direct, default), or into packed 16-bit halves for counter arrays
+//     beyond 3x L2 (that mode keeps linear probing, see SKX_HIST_2CHOICE);
+//  3. opt-in (skx_set_histogram_mode(1)): for large domains the CTA collects
+//     the cold (key, count) pairs of each 4096-row tile in shared memory,
+//     partitions them by key range (64 ranges) and appends each range's run
+//     to that range's global bucket with one cursor atomic; a second kernel
+//     applies each bucket while its counter slice is L2-resident -- so no
+//     cold update read-modify-writes an HBM line (on B200 every L2 miss
+//     moves a 128-byte line, profiles/r1_experiments.md §7);
 //  4. each CTA flushes its table once.
 // The FK column is streamed once with 128-bit evict_first loads; the domain
 // check is fused (first bad row via atomicMin, reported at skx_sync).
@@ -39,6 +41,18 @@ namespace {
 constexpr int kThreads = SKX_HIST_THREADS;
 constexpr int kTableBits = SKX_HIST_TBITS;  // default 8192 slots x 8 B = 64 KB per CTA
 constexpr int kTable = 1 << kTableBits;
+// Two-choice table (default): each key has two candidate slots, read at once,
+// no probe loop -- the warp no longer pays a divergent probe sequence for its
+// cold lanes (C4 histogram 2.52 -> 2.15 ms; 16K slots at 1 CTA/SM 2.44,
+// 4K slots at 6 CTAs/SM 3.36).  The packed 16-bit cold counters keep the
+// linear probes: with two choices their halves wrap and the exact recount
+// runs (C2 index 15.3 -> 33 ms).
+#ifndef SKX_HIST_2CHOICE_C16
+#define SKX_HIST_2CHOICE_C16 0
+#endif
+#ifndef SKX_HIST_2CHOICE
+#define SKX_HIST_2CHOICE 1
+#endif
 #ifndef SKX_HIST_PROBES
 #define SKX_HIST_PROBES 3
 #endif
@@ -57,6 +71,9 @@ constexpr int kLocalBits = 26;    // entry = (count << 26) | (idx - bucket base)
 
 __device__ __forceinline__ uint32_t slot_hash(uint32_t id) {
   return (id * 0x9E3779B1u) >> (32 - kTableBits);
+}
+__device__ __forceinline__ uint32_t slot_hash2(uint32_t id) {
+  return (id * 0x85EBCA77u + 0x6A09E667u) >> (32 - kTableBits);
 }
 
 template <typename CT>
@@ -111,6 +128,36 @@ __device__ __forceinline__ void count_one(uint32_t id, bool valid, uint32_t* key
   const bool leader = key != 0u;
   const uint32_t c = 1u;
   bool cold = false;
+#if SKX_HIST_2CHOICE
+  if (leader && (!C16 || SKX_HIST_2CHOICE_C16)) {
+    // Two-choice table: both candidate slots read at once, no probe loop.
+    // A key may end up in both slots after a race; every row still adds to
+    // exactly one slot or counter, and the flush adds every slot.
+    const uint32_t h1 = slot_hash(key), h2 = slot_hash2(key);
+    const uint32_t k1 = keys[h1], k2 = keys[h2];
+    int slot = k1 == key ? (int)h1 : (k2 == key ? (int)h2 : -1);
+    if (slot < 0 && k1 == 0u) {
+      const uint32_t o = atomicCAS(&keys[h1], 0u, key);
+      if (o == 0u || o == key) slot = (int)h1;
+    }
+    if (slot < 0 && k2 == 0u) {
+      const uint32_t o = atomicCAS(&keys[h2], 0u, key);
+      if (o == 0u || o == key) slot = (int)h2;
+    }
+    if (slot >= 0) {
+      atomicAdd(&cnts[slot], c);
+    } else if (!BK) {
+      if (C16) {
+        const uint32_t idx = key - 1u;
+        atomicAdd(&c16[idx >> 1], 1u << ((idx & 1u) * 16));
+        ++cold_rows;
+      } else {
+        global_add<CT>(counts, key - 1, c);
+      }
+    }
+    cold = slot < 0;
+  } else
+#endif
   if (leader) {
     uint32_t h = slot_hash(key);
     cold = true;
