@@ -11,9 +11,13 @@
 //     slot offsets[nnz + z] / ranks without sorting; non-zero ids become
 //     (key = total - count, id) pairs in ascending id order.  At BASELINE
 //     config 4 only ~19% of the 2^26 ids are non-zero.
-//  2. stable LSD radix sort of the pairs on 8-bit digits, only over the
-//     bits of (total - 1) (4 passes at 2^30 rows).  Ascending key = descending
-//     count; stability on an ascending-id input gives the id tie-break.
+//  2. one stable counting pass over all pairs places every id with count
+//     < 255 at its final rank (digit 255 - count) and moves the ids with
+//     count >= 255 -- at most total / 255 of them -- to a prefix, which then
+//     takes a stable LSD radix sort on 8-bit digits over the bits of
+//     (total - 1) (4 passes at 2^30 rows) on a tile grid sized for that
+//     bound.  Ascending key = descending count; stability on an ascending-id
+//     input gives the id tie-break (C4 sort 1.20 -> 0.82 ms).
 //     Per pass: upsweep (per-tile digit counts), device scan over the
 //     digit-major tile histogram, downsweep (stable warp-level multisplit with
 //     __match_any_sync, then scatter).
@@ -188,12 +192,24 @@ __global__ void __launch_bounds__(kTileThreads)
 }
 
 // --------------------------------------------------------------------------
-// Radix sort passes.
+// Radix sort passes.  SMALL: the one counting pass over all pairs -- digit
+// 255 - count for counts 1..254 (ascending digit = descending count, final
+// order), digit 0 for counts >= 255 (the "big" keys, sorted afterwards by
+// ordinary LSD passes over that prefix only).  Otherwise digit = 8 key bits.
 // --------------------------------------------------------------------------
-template <typename K>
+template <bool SMALL, typename K>
+__device__ __forceinline__ uint32_t radix_digit(K key, int shift, unsigned long long total) {
+  if (SMALL) {
+    const unsigned long long c = total - (unsigned long long)key;  // the id's count, >= 1
+    return c >= 255ull ? 0u : 255u - (uint32_t)c;
+  }
+  return (uint32_t)((key >> shift) & 0xFF);
+}
+
+template <typename K, bool SMALL = false>
 __global__ void __launch_bounds__(kTileThreads)
     k_radix_upsweep(const K* __restrict__ keys, const uint32_t* __restrict__ nnz_dev, int shift,
-                    uint32_t* __restrict__ hist, uint32_t ntiles) {
+                    uint32_t* __restrict__ hist, uint32_t ntiles, unsigned long long total = 0) {
   __shared__ uint32_t wcnt[kWarps][256];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < kWarps * 256; i += kTileThreads) (&wcnt[0][0])[i] = 0u;
@@ -205,7 +221,7 @@ __global__ void __launch_bounds__(kTileThreads)
     for (int i = 0; i < kItems; ++i) {
       const uint64_t p = base + w * (kItems * 32) + i * 32 + lane;
       const bool valid = p < nnz;
-      const uint32_t dg = valid ? (uint32_t)((keys[p] >> shift) & 0xFF) : 256u;
+      const uint32_t dg = valid ? radix_digit<SMALL>(keys[p], shift, total) : 256u;
       // (per-lane shared atomics instead: measured slower, C4 sort 1.18 -> 1.21 ms)
       const uint32_t peers = __match_any_sync(0xffffffffu, dg);
       if (valid && lane == __ffs(peers) - 1) wcnt[w][dg] += __popc(peers);
@@ -218,13 +234,15 @@ __global__ void __launch_bounds__(kTileThreads)
   hist[(uint64_t)threadIdx.x * ntiles + blockIdx.x] = t;
 }
 
-template <typename K, bool LAST>
+// LAST: write offsets[pos] = id and ranks[id-1] = pos + 1 (K3 fused).
+// SMALL: LAST for digits >= 1, keys/vals out (the big prefix) for digit 0.
+template <typename K, bool LAST, bool SMALL = false>
 __global__ void __launch_bounds__(kTileThreads)
     k_radix_downsweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
                       const uint32_t* __restrict__ nnz_dev, int shift,
                       const uint32_t* __restrict__ hist, uint32_t ntiles, K* __restrict__ keys_out,
                       uint32_t* __restrict__ vals_out, uint32_t* __restrict__ offsets,
-                      uint32_t* __restrict__ ranks) {
+                      uint32_t* __restrict__ ranks, unsigned long long total = 0) {
   __shared__ uint32_t wcnt[kWarps][256];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t nnz = *nnz_dev;
@@ -247,7 +265,7 @@ __global__ void __launch_bounds__(kTileThreads)
   for (int i = 0; i < kItems; ++i) {
     const uint64_t p = base + w * (kItems * 32) + i * 32 + lane;
     const bool valid = p < nnz;
-    const uint32_t dg = valid ? (uint32_t)((key[i] >> shift) & 0xFF) : 256u;
+    const uint32_t dg = valid ? radix_digit<SMALL>(key[i], shift, total) : 256u;
     // (8 ballots, one per digit bit, instead of __match_any_sync: measured
     // slower on B200, C4 sort 1.18 -> 1.50 ms)
     const uint32_t peers = __match_any_sync(0xffffffffu, dg);
@@ -273,9 +291,9 @@ __global__ void __launch_bounds__(kTileThreads)
   for (int i = 0; i < kItems; ++i) {
     const uint64_t p = base + w * (kItems * 32) + i * 32 + lane;
     if (p < nnz) {
-      const uint32_t dg = (uint32_t)((key[i] >> shift) & 0xFF);
+      const uint32_t dg = radix_digit<SMALL>(key[i], shift, total);
       const uint32_t pos = wcnt[w][dg] + rank[i];
-      if (LAST) {
+      if (LAST || (SMALL && dg != 0u)) {
         offsets[pos] = val[i];
         ranks[val[i] - 1] = pos + 1u;
       } else {
@@ -305,6 +323,7 @@ int build_index_impl(skx_ctx* ctx, const CT* counts, uint32_t d, uint64_t total,
   uint32_t* tile_off = reinterpret_cast<uint32_t*>(sp + 2 * kb + 2 * vb + tb);
   uint32_t* hist = reinterpret_cast<uint32_t*>(sp + 2 * kb + 2 * vb + 2 * tb);
   uint32_t* nnz = reinterpret_cast<uint32_t*>(sp + 2 * kb + 2 * vb + 2 * tb + hb);
+  uint32_t* nbig = nnz + 1;
 
   k_compact_count<CT><<<ntiles, kTileThreads, 0, s>>>(counts, d, tile_nnz, ctx->err);
   int rc = launch_exclusive_scan_u32(ctx, tile_nnz, tile_off, ntiles, nnz, 3, s);
@@ -319,18 +338,46 @@ int build_index_impl(skx_ctx* ctx, const CT* counts, uint32_t d, uint64_t total,
   int passes = (bits + 7) / 8;
   if (passes == 0) passes = 1;
   int cur = 0;
-  for (int pass = 0; pass < passes; ++pass) {
-    const int shift = pass * 8;
-    k_radix_upsweep<K><<<ntiles, kTileThreads, 0, s>>>(keys[cur], nnz, shift, hist, ntiles);
+  const uint32_t* live = nnz;  // device count of the pairs the next pass sorts
+  uint32_t nt = ntiles;        // tiles of the next pass
+  if (passes > 1) {
+    // One counting pass places every id with count < 255 at its final rank
+    // (descending count is ascending 255 - count; ids ascend within a count
+    // by stability) and moves the ids with count >= 255 -- few, they carry
+    // the skew -- to the front of the other buffer; only that prefix then
+    // takes the LSD passes (C4: 4 passes over 12.7 M pairs -> 1 + 4 over a
+    // few thousand).
+    k_radix_upsweep<K, true><<<ntiles, kTileThreads, 0, s>>>(keys[cur], nnz, 0, hist, ntiles, total);
     ctx->launches++;
     rc = launch_exclusive_scan_u32(ctx, hist, hist, (uint64_t)256 * ntiles, nullptr, 3, s);
     if (rc) return rc;
+    // digit 1 starts where the big prefix ends (tile 0's offset for digit 1)
+    cudaError_t e = cudaMemcpyAsync(nbig, hist + ntiles, 4, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "build_index copy");
+    k_radix_downsweep<K, false, true><<<ntiles, kTileThreads, 0, s>>>(
+        keys[cur], vals[cur], nnz, 0, hist, ntiles, keys[cur ^ 1], vals[cur ^ 1], offsets, ranks,
+        total);
+    ctx->launches++;
+    cur ^= 1;
+    live = nbig;
+    // at most total / 255 ids have a count >= 255: size the tile grid of the
+    // remaining passes (and their digit-major histogram) for that bound
+    const uint64_t big_max = (uint64_t)d < total / 255 ? (uint64_t)d : total / 255;
+    const uint64_t tb_ = (big_max + kTile - 1) / kTile;
+    nt = tb_ == 0 ? 1u : (tb_ < ntiles ? (uint32_t)tb_ : ntiles);
+  }
+  for (int pass = 0; pass < passes; ++pass) {
+    const int shift = pass * 8;
+    k_radix_upsweep<K><<<nt, kTileThreads, 0, s>>>(keys[cur], live, shift, hist, nt);
+    ctx->launches++;
+    rc = launch_exclusive_scan_u32(ctx, hist, hist, (uint64_t)256 * nt, nullptr, 3, s);
+    if (rc) return rc;
     if (pass == passes - 1) {
-      k_radix_downsweep<K, true><<<ntiles, kTileThreads, 0, s>>>(
-          keys[cur], vals[cur], nnz, shift, hist, ntiles, nullptr, nullptr, offsets, ranks);
+      k_radix_downsweep<K, true><<<nt, kTileThreads, 0, s>>>(
+          keys[cur], vals[cur], live, shift, hist, nt, nullptr, nullptr, offsets, ranks);
     } else {
-      k_radix_downsweep<K, false><<<ntiles, kTileThreads, 0, s>>>(
-          keys[cur], vals[cur], nnz, shift, hist, ntiles, keys[cur ^ 1], vals[cur ^ 1], nullptr,
+      k_radix_downsweep<K, false><<<nt, kTileThreads, 0, s>>>(
+          keys[cur], vals[cur], live, shift, hist, nt, keys[cur ^ 1], vals[cur ^ 1], nullptr,
           nullptr);
       cur ^= 1;
     }

@@ -529,3 +529,28 @@ def test_select_fast_path_alignment_and_tail(sx, oracle, off):
     with pytest.raises(DomainViolation) as e:
         sx.select(cu(bad), bm)
     assert e.value.row() == n - 3 and e.value.value() == d + 1
+
+
+@pytest.mark.parametrize("case", ["boundary", "all_big", "no_big", "one_big"])
+def test_build_index_small_count_pass(sx, oracle, case):
+    """The counting pass places ids with count < 255 directly and sorts only
+    the ids with count >= 255: counts around the 254/255 boundary with ties,
+    every count big, no big count at all (total >= 256), a single big id."""
+    rng = np.random.default_rng(5)
+    d = 50000
+    if case == "boundary":
+        counts = rng.choice(np.array([0, 1, 2, 253, 254, 255, 256, 511, 70000], np.uint64), size=d)
+    elif case == "all_big":
+        counts = rng.integers(255, 1 << 20, size=d, dtype=np.uint64)
+        counts[::7] = 300  # ties
+    elif case == "no_big":
+        counts = rng.integers(0, 255, size=d, dtype=np.uint64)
+    else:
+        counts = rng.integers(0, 3, size=d, dtype=np.uint64)
+        counts[d // 2] = 1 << 24
+    total = int(counts.sum())
+    idx = sx.build_index(sx.FrequencyProfile(cu(counts), total))
+    off, rk = oracle.build_index(counts, total)
+    assert np.array_equal(np_(idx.offsets), off) and np.array_equal(np_(idx.ranks), rk)
+    idx32 = sx.build_index(sx.FrequencyProfile(cu(counts.astype(np.uint32)), total))
+    assert np.array_equal(np_(idx32.offsets), off)
