@@ -495,7 +495,13 @@ __global__ void __launch_bounds__(256)
     lr += __shfl_down_sync(0xffffffffu, lr, o);
     ls += __shfl_down_sync(0xffffffffu, ls, o);
   }
-  if ((threadIdx.x & 31) == 0) {
+  // one pair of same-address atomics per CTA, not per warp (they serialise)
+  __shared__ unsigned long long s_r[8], s_s[8];
+  if ((threadIdx.x & 31) == 0) s_r[threadIdx.x >> 5] = lr, s_s[threadIdx.x >> 5] = ls;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    lr = ls = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) lr += s_r[w], ls += s_s[w];
     if (lr) atomicAdd(&chk->dec_rows, lr);
     if (ls) atomicAdd(&chk->dec_sum, ls);
   }
