@@ -78,6 +78,19 @@ int skx_device_free(skx_ctx* ctx, void* ptr);
 /* Synchronous copies on the context's device. */
 int skx_copy_to_device(skx_ctx* ctx, void* dst, const void* src, uint64_t bytes);
 int skx_copy_to_host(skx_ctx* ctx, void* dst, const void* src, uint64_t bytes);
+/* Streamed callers (SKDX columns streamed host -> device
+ * through pinned memory; no reference counterpart -- the reference reads a
+ * whole column into a std::vector, column_io.cpp:89-95).  Pinned host
+ * buffers, the context's two host-side streams (slot 0 / 1), and
+ * asynchronous copies on a stream; completion and deferred device errors
+ * are reported by skx_sync(ctx, stream). */
+int skx_pinned_alloc(skx_ctx* ctx, uint64_t bytes, void** ptr);
+int skx_pinned_free(skx_ctx* ctx, void* ptr);
+void* skx_ctx_stream(skx_ctx* ctx, int slot);
+int skx_copy_to_device_async(skx_ctx* ctx, void* dst, const void* src, uint64_t bytes,
+                             void* stream);
+int skx_copy_to_host_async(skx_ctx* ctx, void* dst, const void* src, uint64_t bytes,
+                           void* stream);
 
 /* find_domain_violation (operators.cpp:32-41): *row_out (host) = the first k
  * with fact[k]-1 >= d, or UINT64_MAX.  Synchronous. */

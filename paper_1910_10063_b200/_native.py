@@ -72,6 +72,11 @@ SIGNATURES = {
     "skx_device_free": (_int, [_vp, _vp]),
     "skx_copy_to_device": (_int, [_vp, _vp, _vp, _u64]),
     "skx_copy_to_host": (_int, [_vp, _vp, _vp, _u64]),
+    "skx_pinned_alloc": (_int, [_vp, _u64, C.POINTER(_vp)]),
+    "skx_pinned_free": (_int, [_vp, _vp]),
+    "skx_ctx_stream": (_vp, [_vp, _int]),
+    "skx_copy_to_device_async": (_int, [_vp, _vp, _vp, _u64, _vp]),
+    "skx_copy_to_host_async": (_int, [_vp, _vp, _vp, _u64, _vp]),
     "skx_find_domain_violation": (_int, [_vp, _vp, _u64, _u64, C.POINTER(_u64)]),
     "skx_fill_column": (_int, [_vp, _int, _int, _u64, _u64, _dbl, _dbl, _vp, _vp]),
 }

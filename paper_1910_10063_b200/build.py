@@ -21,6 +21,7 @@ INCLUDE = os.path.join(ROOT, "include")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIBSKX = os.path.join(PKG, "libskx.so")
 LIBSHIM = os.path.join(PKG, "libskewdx_b200.so")
+CLI = os.path.join(PKG, "skewdx_b200_cli")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
@@ -83,9 +84,21 @@ def build_shim(force: bool = False) -> str:
     return LIBSHIM
 
 
+def build_cli(force: bool = False) -> str:
+    """The reference CLI's `index build` / `index apply` over the drop-in."""
+    src = os.path.join(CPP, "skewdx_b200_cli.cpp")
+    hdrs = glob.glob(os.path.join(CPP, "include", "skewdx", "*.hpp"))
+    if force or _stale(CLI, [src, *hdrs, LIBSHIM]):
+        _run(["g++", "-O2", "-std=c++20", "-Wall", "-Wextra", "-I" + INCLUDE,
+              "-I" + os.path.join(CPP, "include"), src, "-o", CLI, "-L" + PKG, "-lskewdx_b200",
+              "-lskx", "-Wl,-rpath,$ORIGIN"])
+    return CLI
+
+
 def build_all(force: bool = False) -> None:
     build_libskx(force)
     build_shim(force)
+    build_cli(force)
 
 
 if __name__ == "__main__":

@@ -22,6 +22,7 @@
 
 #include "skewdx/column.hpp"
 #include "skewdx/column_io.hpp"
+#include "skewdx/column_stream.hpp"
 #include "skewdx/error.hpp"
 #include "skewdx/mix.hpp"
 #include "skewdx/operators.hpp"
@@ -632,6 +633,235 @@ std::vector<std::uint32_t> trace_from_column(const Column& fact, const CacheGeom
                             o.as<std::uint32_t>(), nullptr));
   o.to(out);
   return out;
+}
+
+
+// ---- column_stream.hpp (B200 extension: streamed SKDX files) ----------------
+namespace {
+
+std::uint64_t g_chunk_rows = [] {
+  const char* e = std::getenv("SKX_STREAM_CHUNK_ROWS");
+  const unsigned long long v = e ? std::strtoull(e, nullptr, 10) : 0ull;
+  return v ? static_cast<std::uint64_t>(v) : (std::uint64_t{1} << 24);
+}();
+
+class Pinned {
+ public:
+  explicit Pinned(std::uint64_t bytes) { check(skx_pinned_alloc(ctx(), bytes, &p_)); }
+  Pinned(const Pinned&) = delete;
+  Pinned& operator=(const Pinned&) = delete;
+  ~Pinned() { skx_pinned_free(ctx(), p_); }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p_);
+  }
+
+ private:
+  void* p_ = nullptr;
+};
+
+// SKDX payload read in chunks; the header and the payload length are checked
+// up front exactly as read_column does.
+class SkdxReader {
+ public:
+  explicit SkdxReader(const std::filesystem::path& path) : f_(path, std::ios::binary), path_(path) {
+    if (!f_) throw IoError("cannot open for reading: " + path.string());
+    n_ = read_header(f_, path, "SKDX");
+    const auto here = f_.tellg();
+    f_.seekg(0, std::ios::end);
+    const auto bytes = static_cast<std::uint64_t>(f_.tellg() - here);
+    if (bytes != n_ * 4) throw FormatError("length mismatch against header in " + path.string());
+    payload_ = here;
+    f_.seekg(payload_);
+  }
+  std::uint64_t size() const { return n_; }
+  void read(std::uint32_t* dst, std::uint64_t rows) {
+    f_.read(reinterpret_cast<char*>(dst), static_cast<std::streamsize>(rows * 4));
+    if (!f_) throw FormatError("length mismatch against header in " + path_.string());
+  }
+  void rewind() {
+    f_.clear();
+    f_.seekg(payload_);
+  }
+
+ private:
+  std::ifstream f_;
+  std::filesystem::path path_;
+  std::uint64_t n_ = 0;
+  std::streampos payload_{};
+};
+
+class SkdxWriter {
+ public:
+  SkdxWriter(const std::filesystem::path& path, std::uint64_t n)
+      : f_(path, std::ios::binary | std::ios::trunc), path_(path), n_(n) {
+    if (!f_) throw IoError("cannot open for writing: " + path.string());
+    f_.write("SKDX", 4);
+    f_.write(reinterpret_cast<const char*>(&kVersion), 4);
+    f_.write(reinterpret_cast<const char*>(&n), 8);
+  }
+  void write(const std::uint32_t* src, std::uint64_t rows) {
+    f_.write(reinterpret_cast<const char*>(src), static_cast<std::streamsize>(rows * 4));
+    written_ += rows;
+  }
+  void finish() {
+    f_.flush();
+    if (!f_ || written_ != n_) throw IoError("write failed: " + path_.string());
+    f_.close();
+  }
+  void abandon() {
+    f_.close();
+    std::error_code ec;
+    std::filesystem::remove(path_, ec);
+  }
+
+ private:
+  std::ofstream f_;
+  std::filesystem::path path_;
+  std::uint64_t n_, written_ = 0;
+};
+
+// After the device reported a violation somewhere in the stream: the first
+// offending row, found on the host as find_domain_violation reports it
+// (cold path only).
+[[noreturn]] void throw_first_violation(const std::filesystem::path& path, std::uint64_t d) {
+  SkdxReader rd(path);
+  std::vector<std::uint32_t> buf(std::min<std::uint64_t>(g_chunk_rows, std::max<std::uint64_t>(rd.size(), 1)));
+  for (std::uint64_t b = 0; b < rd.size(); b += buf.size()) {
+    const std::uint64_t m = std::min<std::uint64_t>(buf.size(), rd.size() - b);
+    rd.read(buf.data(), m);
+    for (std::uint64_t k = 0; k < m; ++k)
+      if (static_cast<std::uint32_t>(buf[k] - 1u) >= d) throw DomainViolation(b + k, buf[k], d);
+  }
+  throw Error("libskx: device reported a domain violation the host scan did not find");
+}
+
+// Two chunks in flight on the context's two host streams.
+struct StreamSlots {
+  void* st[2] = {skx_ctx_stream(ctx(), 0), skx_ctx_stream(ctx(), 1)};
+  bool pending[2] = {false, false};
+  bool violation = false;
+  // Waits for slot s; a device-side domain violation is remembered (the host
+  // scan finds the first row afterwards), anything else throws.
+  void drain(int s) {
+    if (!pending[s]) return;
+    pending[s] = false;
+    const int rc = skx_sync(ctx(), st[s]);
+    if (rc == SKX_DOMAIN_VIOLATION)
+      violation = true;
+    else
+      check(rc);
+  }
+};
+
+}  // namespace
+
+void set_stream_chunk_rows(std::uint64_t rows) { g_chunk_rows = rows ? rows : 1; }
+std::uint64_t stream_chunk_rows() { return g_chunk_rows; }
+
+PermutationIndex rebuild_file(const std::filesystem::path& fact_path, std::uint32_t d,
+                              std::uint32_t* d_used) {
+  SkdxReader rd(fact_path);
+  const std::uint64_t n = rd.size();
+  const std::uint64_t chunk = std::min<std::uint64_t>(g_chunk_rows, std::max<std::uint64_t>(n, 1));
+  if (d == 0 && n > 0) {  // D = the largest identifier (generate.cpp:56), a host pass
+    std::vector<std::uint32_t> buf(chunk);
+    std::uint32_t mx = 0;
+    for (std::uint64_t b = 0; b < n; b += chunk) {
+      const std::uint64_t m = std::min(chunk, n - b);
+      rd.read(buf.data(), m);
+      mx = std::max(mx, *std::max_element(buf.begin(), buf.begin() + static_cast<std::ptrdiff_t>(m)));
+    }
+    d = mx;
+    rd.rewind();
+  }
+  if (d_used) *d_used = d;
+  // Empty columns, an empty domain and > 2^32 - 1 rows (u64 counters) take
+  // the in-memory path.
+  if (n == 0 || d == 0 || n > 0xFFFFFFFFull) return rebuild(read_column(fact_path), d);
+  DevBuf counts(std::uint64_t{d} * 4), off(std::uint64_t{d} * 4), rk(std::uint64_t{d} * 4);
+  {
+    Pinned pin0(chunk * 4), pin1(chunk * 4);
+    DevBuf dev0(chunk * 4), dev1(chunk * 4);
+    Pinned* pin[2] = {&pin0, &pin1};
+    DevBuf* dev[2] = {&dev0, &dev1};
+    StreamSlots ss;
+    std::uint64_t i = 0;
+    for (std::uint64_t b = 0; b < n && !ss.violation; b += chunk, ++i) {
+      const int s = static_cast<int>(i & 1);
+      const std::uint64_t m = std::min(chunk, n - b);
+      ss.drain(s);  // its buffers are free again
+      rd.read(pin[s]->as<std::uint32_t>(), m);
+      check(skx_copy_to_device_async(ctx(), dev[s]->as<void>(), pin[s]->as<void>(), m * 4, ss.st[s]));
+      // the first chunk overwrites the counters; the rest add to them, both
+      // streams' atomics landing in the same array
+      check(skx_histogram_u32(ctx(), dev[s]->as<std::uint32_t>(), m, d, counts.as<std::uint32_t>(),
+                              i == 0 ? 0 : 1, ss.st[s]));
+      ss.pending[s] = true;
+      if (i == 0) ss.drain(0);  // counters initialised before stream 1 adds
+    }
+    ss.drain(static_cast<int>(i & 1));
+    ss.drain(static_cast<int>((i + 1) & 1));
+    if (ss.violation) throw_first_violation(fact_path, d);
+  }
+  run(skx_build_index_u32(ctx(), counts.as<std::uint32_t>(), d, n, off.as<std::uint32_t>(),
+                          rk.as<std::uint32_t>(), nullptr));
+  PermutationIndex idx;
+  idx.offsets.resize(d);
+  idx.ranks.resize(d);
+  off.to(idx.offsets);
+  rk.to(idx.ranks);
+  return idx;
+}
+
+void recode_file(const std::filesystem::path& in_path, const std::filesystem::path& out_path,
+                 const PermutationIndex& index) {
+  SkdxReader rd(in_path);
+  const std::uint64_t n = rd.size();
+  const std::uint32_t d = index.domain_cardinality();
+  if (n == 0 || d == 0) {
+    write_column(out_path, recode_fact(read_column(in_path), index));
+    return;
+  }
+  const std::uint64_t chunk = std::min<std::uint64_t>(g_chunk_rows, n);
+  DevBuf ranks(index.ranks);
+  Pinned pin_in0(chunk * 4), pin_in1(chunk * 4), pin_out0(chunk * 4), pin_out1(chunk * 4);
+  DevBuf dev_in0(chunk * 4), dev_in1(chunk * 4), dev_out0(chunk * 4), dev_out1(chunk * 4);
+  Pinned* pin_in[2] = {&pin_in0, &pin_in1};
+  Pinned* pin_out[2] = {&pin_out0, &pin_out1};
+  DevBuf* dev_in[2] = {&dev_in0, &dev_in1};
+  DevBuf* dev_out[2] = {&dev_out0, &dev_out1};
+  std::uint64_t rows[2] = {0, 0};
+  SkdxWriter wr(out_path, n);
+  StreamSlots ss;
+  // Chunk i's output is written when slot i & 1 is drained for chunk i + 2
+  // (or at the end), so the file is written in row order.
+  auto retire = [&](int s) {
+    const bool had = ss.pending[s];
+    ss.drain(s);
+    if (had && !ss.violation) wr.write(pin_out[s]->as<std::uint32_t>(), rows[s]);
+  };
+  std::uint64_t i = 0;
+  for (std::uint64_t b = 0; b < n && !ss.violation; b += chunk, ++i) {
+    const int s = static_cast<int>(i & 1);
+    const std::uint64_t m = std::min(chunk, n - b);
+    retire(s);
+    if (ss.violation) break;
+    rd.read(pin_in[s]->as<std::uint32_t>(), m);
+    check(skx_copy_to_device_async(ctx(), dev_in[s]->as<void>(), pin_in[s]->as<void>(), m * 4, ss.st[s]));
+    check(skx_recode_fact(ctx(), dev_in[s]->as<std::uint32_t>(), m, ranks.as<std::uint32_t>(), d,
+                          dev_out[s]->as<std::uint32_t>(), ss.st[s]));
+    check(skx_copy_to_host_async(ctx(), pin_out[s]->as<void>(), dev_out[s]->as<void>(), m * 4, ss.st[s]));
+    rows[s] = m;
+    ss.pending[s] = true;
+  }
+  retire(static_cast<int>(i & 1));
+  retire(static_cast<int>((i + 1) & 1));
+  if (ss.violation) {
+    wr.abandon();
+    throw_first_violation(in_path, d);
+  }
+  wr.finish();
 }
 
 }  // namespace skewdx

@@ -425,6 +425,44 @@ int skx_copy_to_host(skx_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
   return e == cudaSuccess ? SKX_OK : cuda_fail(ctx, e, "copy_to_host");
 }
 
+int skx_pinned_alloc(skx_ctx* ctx, uint64_t bytes, void** ptr) {
+  if (!ctx || !ptr) return SKX_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  *ptr = nullptr;
+  cudaError_t e = cudaHostAlloc(ptr, bytes ? bytes : 16, cudaHostAllocPortable);
+  return e == cudaSuccess ? SKX_OK : cuda_fail(ctx, e, "pinned_alloc");
+}
+
+int skx_pinned_free(skx_ctx* ctx, void* ptr) {
+  if (!ctx) return SKX_INVALID_ARGUMENT;
+  if (!ptr) return SKX_OK;
+  cudaError_t e = cudaFreeHost(ptr);
+  return e == cudaSuccess ? SKX_OK : cuda_fail(ctx, e, "pinned_free");
+}
+
+void* skx_ctx_stream(skx_ctx* ctx, int slot) {
+  if (!ctx || slot < 0 || slot > 1) return nullptr;
+  return ctx->hstream[slot];
+}
+
+int skx_copy_to_device_async(skx_ctx* ctx, void* dst, const void* src, uint64_t bytes,
+                             void* stream) {
+  if (!ctx) return SKX_INVALID_ARGUMENT;
+  if (!bytes) return SKX_OK;
+  cudaSetDevice(ctx->device);
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, as_stream(stream));
+  return e == cudaSuccess ? SKX_OK : cuda_fail(ctx, e, "copy_to_device_async");
+}
+
+int skx_copy_to_host_async(skx_ctx* ctx, void* dst, const void* src, uint64_t bytes,
+                           void* stream) {
+  if (!ctx) return SKX_INVALID_ARGUMENT;
+  if (!bytes) return SKX_OK;
+  cudaSetDevice(ctx->device);
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, as_stream(stream));
+  return e == cudaSuccess ? SKX_OK : cuda_fail(ctx, e, "copy_to_host_async");
+}
+
 int skx_find_domain_violation(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint64_t d,
                               uint64_t* row_out) {
   if (!ctx || !row_out) return SKX_INVALID_ARGUMENT;
