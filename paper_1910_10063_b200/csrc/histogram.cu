@@ -35,6 +35,12 @@ namespace {
 #ifndef SKX_HIST_TBITS
 #define SKX_HIST_TBITS 13
 #endif
+#ifndef SKX_HIST_PASS_BYTES
+// C16 key-range pass size: packed cold counters per pass (the reductions'
+// L2-resident working set).  C2 index (D=2^27, 256 MB of packed counters):
+// 1 pass 15.2 ms, 2 passes (128 MB) 11.3, 3 (~85 MB) 10.8, 4 13.9, 8 24.8.
+#define SKX_HIST_PASS_BYTES (96ull << 20)
+#endif
 #ifndef SKX_HIST_CTAS
 #define SKX_HIST_CTAS 3
 #endif
@@ -235,7 +241,10 @@ template <typename CT, bool BK, bool C16>
 __global__ void __launch_bounds__(kThreads)
     k_histogram(const uint32_t* __restrict__ fact, uint64_t head, uint64_t nvec, uint64_t n,
                 uint32_t d, CT* __restrict__ counts, Buckets bk, DevErr* err,
-                unsigned int* __restrict__ c16, HistCheck* chk, const HistCheck* gate) {
+                unsigned int* __restrict__ c16, HistCheck* chk, const HistCheck* gate,
+                uint32_t lo = 0u, uint32_t span = 0xFFFFFFFFu) {
+  // Key-range pass (C16 at very large domains): only ids with id - 1 in
+  // [lo, lo + span) are counted; violations are reported by the pass with err.
   if (gate && hist_ok(gate)) return;  // C16 fallback: nothing to redo
   unsigned long long cold_rows = 0;
   extern __shared__ __align__(16) uint32_t smem_tab[];
@@ -273,8 +282,9 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const bool ok = (ids[j] - 1u) < d;
-        if (live && !ok) record_violation(err, head + vi * 4 + j, ids[j]);
-        count_one<CT, BK, C16>(ids[j], live && ok, keys, cnts, counts, tc, c16, cold_rows);
+        if (live && !ok && (!C16 || err)) record_violation(err, head + vi * 4 + j, ids[j]);
+        const bool inr = !C16 || (ids[j] - 1u - lo) < span;  // passes: C16 only
+        count_one<CT, BK, C16>(ids[j], live && ok && inr, keys, cnts, counts, tc, c16, cold_rows);
       }
     }
     if (BK) flush_tile<CT>(tc, bk, counts);
@@ -290,8 +300,9 @@ __global__ void __launch_bounds__(kThreads)
       if (live) k = t < head ? t : tail_b + (t - head);
       const uint32_t id = live ? fact[k] : 0u;
       const bool ok = (id - 1u) < d;
-      if (live && !ok) record_violation(err, k, id);
-      count_one<CT, BK, C16>(id, live && ok, keys, cnts, counts, tc, c16, cold_rows);
+      if (live && !ok && (!C16 || err)) record_violation(err, k, id);
+      const bool inr = !C16 || (id - 1u - lo) < span;
+      count_one<CT, BK, C16>(id, live && ok && inr, keys, cnts, counts, tc, c16, cold_rows);
     }
   }
   if (BK) flush_tile<CT>(tc, bk, counts);  // block-uniform: also blocks != 0
@@ -410,15 +421,26 @@ int histogram_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64_t n
     if (e != cudaSuccess) return cuda_fail(ctx, e, "histogram memset");
     cudaFuncSetAttribute(k_histogram<CT, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    k_histogram<CT, false, true><<<grid, kThreads, smem, s>>>(fact, head, nvec, n, d, counts, bk,
-                                                              ctx->err, c16, chk, nullptr);
+    // Key-range passes: each pass counts the ids of one slice of the domain,
+    // so its packed cold counters (SKX_HIST_PASS_BYTES) stay L2-resident for
+    // the reductions and the CTA tables hold only that slice's keys; the FK
+    // column is re-streamed per pass.
+    const uint64_t pass_keys = std::max<uint64_t>(uint64_t(SKX_HIST_PASS_BYTES) / 2, 1);
+    const uint32_t passes = (uint32_t)(((uint64_t)d + pass_keys - 1) / pass_keys);
+    const uint32_t span = (uint32_t)(((uint64_t)d + passes - 1) / passes);
+    for (uint32_t p = 0; p < passes; ++p) {
+      k_histogram<CT, false, true><<<grid, kThreads, smem, s>>>(
+          fact, head, nvec, n, d, counts, bk, p == 0 ? ctx->err : nullptr, c16, chk, nullptr,
+          p * span, span);
+      ctx->launches++;
+    }
     k_hist_merge16<CT><<<grid_for(ctx, (d + 1) / 2, 256, 8), 256, 0, s>>>(c16, d, counts, chk);
     k_hist_zero_if_failed<CT><<<grid_for(ctx, d, 256, 8), 256, 0, s>>>(counts, d, chk);
     cudaFuncSetAttribute(k_histogram<CT, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     k_histogram<CT, false, false><<<grid, kThreads, smem, s>>>(fact, head, nvec, n, d, counts, bk,
                                                                ctx->err, nullptr, nullptr, chk);
-    ctx->launches += 4;
+    ctx->launches += 3;
   } else {
     cudaFuncSetAttribute(k_histogram<CT, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
