@@ -121,3 +121,20 @@ extern "C" int probe_stream(const uint32_t* a, uint64_t n, const uint8_t* die_of
   k_stream<<<grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(a), n / 4, die_of_sm, ctr, mode, out);
   return (int)cudaGetLastError();
 }
+
+// RED capacity probe: random 32-bit reductions into the half of a 2D-word
+// table that the SM's group owns (as k_split, for atomics).
+__global__ void __launch_bounds__(256) k_red_split(unsigned* __restrict__ tab, uint64_t D,
+                                                   int iters, uint64_t seed,
+                                                   const uint8_t* __restrict__ group) {
+  const uint64_t base = group[smid()] ? D : 0;
+  const uint64_t t = (uint64_t)blockIdx.x * 256 + threadIdx.x;
+#pragma unroll 8
+  for (int i = 0; i < iters; ++i) atomicAdd(tab + base + mix(seed ^ (t * 1000003ull + i)) % D, 1u);
+}
+
+extern "C" int probe_red_split(unsigned* tab, uint64_t D, int iters, uint64_t seed,
+                               const uint8_t* group, int grid, void* stream) {
+  k_red_split<<<grid, 256, 0, (cudaStream_t)stream>>>(tab, D, iters, seed, group);
+  return (int)cudaGetLastError();
+}
