@@ -182,9 +182,13 @@ __global__ void __launch_bounds__(kTileThreads)
     if (p < d) {
       const uint32_t id = (uint32_t)p + 1u;
       const uint32_t nz_rank = nz_before + __popc(nzmask[i] & lt);
+      // ranks is written for every id (0 for the non-zero ones, which the
+      // sort's last pass overwrites), so its sectors are written whole: a
+      // masked store leaves partial sectors that HBM must read back.
       if ((nzmask[i] >> lane) & 1u) {
         keys[nz_rank] = (K)(total - (unsigned long long)counts[p]);
         vals[nz_rank] = id;
+        ranks[id - 1] = 0u;
       } else {
         // zero ids before this one = p - (non-zero ids before this one)
         const uint32_t pos = nnz + ((uint32_t)p - nz_rank);
