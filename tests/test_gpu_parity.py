@@ -470,11 +470,31 @@ def test_histogram_c16_wrap_fallback(sx, oracle):
     n = 1 << 26
     fact = np.full(n, d, np.uint32)  # the heavy key, cold once the tables are full
     fill = 2 * 444 * 4096  # two CTA iterations of distinct keys for every CTA
-    fact[:fill] = np.arange(1, fill + 1, dtype=np.uint32)
+    # the fill keys share the heavy key's key-range pass (the last one), so
+    # they are what the tables hold when the heavy key arrives
+    fact[:fill] = np.arange(d - fill, d, dtype=np.uint32)
     exp = oracle.count_frequencies(fact, d)
     got = np_(sx.count_frequencies(cu(fact), d).counts)
     assert np.array_equal(got, exp)
     assert np.array_equal(np_(sx.histogram_u32(cu(fact), d)).astype(np.uint64), exp)
+
+
+def test_histogram_c16_key_range_passes(sx, oracle):
+    """Packed cold counters at D = 2^27 run as key-range passes (3 slices of
+    the domain): a skewed original-layout column, ids spread over every pass,
+    plus the first and last id of the domain."""
+    d, n = 1 << 27, (1 << 24) + 5
+    r2i = sx.random_bijection(d, 17)
+    fact = sx.generate_zipf(cu(sx.zipf_cdf(d, 1.0)), n, 17, rank_to_id=cu(r2i))
+    f_np = np_(fact).copy()
+    f_np[:3] = [1, d, d // 3]
+    exp = oracle.count_frequencies(f_np, d)
+    assert np.array_equal(np_(sx.histogram_u32(cu(f_np), d)).astype(np.uint64), exp)
+    f_np[n - 2] = d + 1  # violation reported once, by the first pass
+    from paper_1910_10063_b200 import DomainViolation
+    with pytest.raises(DomainViolation) as e:
+        sx.count_frequencies(cu(f_np), d)
+    assert e.value.row() == n - 2 and e.value.value() == d + 1
 
 
 @pytest.mark.parametrize("d,n,hot", [((1 << 22) + 1, 1000, 0), ((1 << 22) + 1, (1 << 20) + 7, 0),
