@@ -162,12 +162,16 @@ __global__ void __launch_bounds__(kTileThreads)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t nnz = *nnz_dev;
   uint32_t nzmask[kItems];
+  CT cv[kItems];  // kept for the key writes (no second read of counts)
   uint32_t wcount = 0;
 #pragma unroll
   for (int i = 0; i < kItems; ++i) {
     const uint64_t p = base + w * (kItems * 32) + i * 32 + lane;
-    const bool nzf = p < d && counts[p] != 0;
-    nzmask[i] = __ballot_sync(0xffffffffu, nzf);
+    cv[i] = p < d ? counts[p] : CT(0);
+  }
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    nzmask[i] = __ballot_sync(0xffffffffu, cv[i] != 0);
     wcount += __popc(nzmask[i]);
   }
   __shared__ uint32_t wn[kWarps];
@@ -186,7 +190,7 @@ __global__ void __launch_bounds__(kTileThreads)
       // sort's last pass overwrites), so its sectors are written whole: a
       // masked store leaves partial sectors that HBM must read back.
       if ((nzmask[i] >> lane) & 1u) {
-        keys[nz_rank] = (K)(total - (unsigned long long)counts[p]);
+        keys[nz_rank] = (K)(total - (unsigned long long)cv[i]);
         vals[nz_rank] = id;
         ranks[id - 1] = 0u;
       } else {
