@@ -337,19 +337,44 @@ __global__ void __launch_bounds__(256)
 }
 
 // C16: counts[i] += half i of the packed words; sums the halves for the check.
+// Four counters per thread (two packed words), read and written whole: a
+// store only where a half is non-zero leaves partial sectors that HBM must
+// read back (0.49 ms at the C2 index before).
+template <typename CT>
+__device__ __forceinline__ void add4(CT* c, uint32_t a, uint32_t b, uint32_t e, uint32_t f);
+template <>
+__device__ __forceinline__ void add4<uint32_t>(uint32_t* c, uint32_t a, uint32_t b, uint32_t e,
+                                               uint32_t f) {
+  uint4 v = *reinterpret_cast<uint4*>(c);
+  v.x += a, v.y += b, v.z += e, v.w += f;
+  *reinterpret_cast<uint4*>(c) = v;
+}
+template <>
+__device__ __forceinline__ void add4<unsigned long long>(unsigned long long* c, uint32_t a,
+                                                         uint32_t b, uint32_t e, uint32_t f) {
+  ulonglong2 v0 = reinterpret_cast<ulonglong2*>(c)[0], v1 = reinterpret_cast<ulonglong2*>(c)[1];
+  v0.x += a, v0.y += b, v1.x += e, v1.y += f;
+  reinterpret_cast<ulonglong2*>(c)[0] = v0;
+  reinterpret_cast<ulonglong2*>(c)[1] = v1;
+}
+
 template <typename CT>
 __global__ void __launch_bounds__(256)
     k_hist_merge16(const unsigned int* __restrict__ c16, uint32_t d, CT* __restrict__ counts,
                    HistCheck* chk) {
   unsigned long long tot = 0;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < ((uint64_t)d + 1) / 2;
-       w += stride) {
-    const unsigned int x = __ldcs(c16 + w);
-    const uint32_t lo = x & 0xFFFFu, hi = x >> 16;
-    if (lo) counts[2 * w] += (CT)lo;
-    if (hi && 2 * w + 1 < d) counts[2 * w + 1] += (CT)hi;
-    tot += lo + hi;
+  const bool vec = (reinterpret_cast<uintptr_t>(counts) % (4 * sizeof(CT))) == 0;
+  const uint64_t nq = vec ? d / 4 : 0;  // whole groups of four counters
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += stride) {
+    const uint2 x = __ldcs(reinterpret_cast<const uint2*>(c16) + q);
+    add4<CT>(counts + 4 * q, x.x & 0xFFFFu, x.x >> 16, x.y & 0xFFFFu, x.y >> 16);
+    tot += (x.x & 0xFFFFu) + (x.x >> 16) + (x.y & 0xFFFFu) + (x.y >> 16);
+  }
+  for (uint64_t i = 4 * nq + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d; i += stride) {
+    const uint32_t h = (c16[i >> 1] >> ((i & 1u) * 16)) & 0xFFFFu;  // ragged tail / unaligned
+    if (h) counts[i] += (CT)h;
+    tot += h;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) tot += __shfl_down_sync(0xffffffffu, tot, o);
