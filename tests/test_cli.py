@@ -145,3 +145,51 @@ def test_cli_domain_default_and_violations(cli, oracle, tmp_path):
                   "--fact-out", tmp_path / "r.skdx", env=env)
     assert rc == 2 and "domain violation at row 200000" in err, err
     assert not (tmp_path / "r.skdx").exists()  # nothing written, as in the reference
+
+
+@pytest.mark.gpu
+def test_pinned_async_entry_points():
+    """The streamed callers' C-ABI entries: pinned buffers, the context's two
+    host streams, asynchronous copies both ways, a histogram on a host stream
+    with a deferred domain violation reported by skx_sync on that stream."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1910_10063_b200 import DomainViolation
+    from paper_1910_10063_b200 import skewdx as sx
+    ctx = sx.context(0)
+    lib, h = ctx.lib, ctx.handle
+    n = 1 << 20
+    pin = C.c_void_p()
+    ctx.check(lib.skx_pinned_alloc(h, n * 4, C.byref(pin)))
+    try:
+        host = np.ctypeslib.as_array(C.cast(pin, C.POINTER(C.c_uint32)), shape=(n,))
+        host[:] = np.arange(1, n + 1, dtype=np.uint32) % 1000 + 1
+        dev = torch.empty(n, dtype=torch.int32, device="cuda")
+        for slot in (0, 1):
+            st = lib.skx_ctx_stream(h, slot)
+            assert st
+            ctx.check(lib.skx_copy_to_device_async(h, C.c_void_p(dev.data_ptr()), pin, n * 4, C.c_void_p(st)))
+            counts = torch.zeros(1000, dtype=torch.int32, device="cuda")
+            ctx.check(lib.skx_histogram_u32(h, C.c_void_p(dev.data_ptr()), n, 1000,
+                                            C.c_void_p(counts.data_ptr()), 0, C.c_void_p(st)))
+            ctx.check(lib.skx_sync(h, C.c_void_p(st)))
+            exp = np.bincount(host.astype(np.int64) - 1, minlength=1000)
+            assert np.array_equal(counts.cpu().numpy().astype(np.int64), exp)
+            host2 = np.zeros(n, np.uint32)
+            ctx.check(lib.skx_copy_to_host_async(h, host2.ctypes.data_as(C.c_void_p),
+                                                 C.c_void_p(dev.data_ptr()), n * 4, C.c_void_p(st)))
+            ctx.check(lib.skx_sync(h, C.c_void_p(st)))
+            assert np.array_equal(host2, host)
+        host[777] = 5000  # out of 1..1000
+        st = lib.skx_ctx_stream(h, 1)
+        ctx.check(lib.skx_copy_to_device_async(h, C.c_void_p(dev.data_ptr()), pin, n * 4, C.c_void_p(st)))
+        ctx.check(lib.skx_histogram_u32(h, C.c_void_p(dev.data_ptr()), n, 1000,
+                                        C.c_void_p(counts.data_ptr()), 1, C.c_void_p(st)))
+        with pytest.raises(DomainViolation) as e:
+            ctx.sync(C.c_void_p(st))
+        assert e.value.row() == 777 and e.value.value() == 5000
+        assert lib.skx_ctx_stream(h, 2) is None
+    finally:
+        ctx.check(lib.skx_pinned_free(h, pin))
