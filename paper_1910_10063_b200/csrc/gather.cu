@@ -31,6 +31,9 @@ namespace {
 constexpr int kThreads = 256;      // plain variant: several CTAs per SM
 constexpr int kThreadsHot = 1024;  // hot-prefix variant: one CTA per SM owns the smem copy
 constexpr int kUnroll = 8;         // uint4 FK vectors per thread per iteration (32 rows)
+#ifndef SKX_GATHER_MINB
+#define SKX_GATHER_MINB 2     // resident CTAs per SM the registers must allow
+#endif
 #ifndef SKX_GATHER_SMALL_CTAS
 #define SKX_GATHER_SMALL_CTAS 2    // CTAs per SM for small columns
 #endif
@@ -137,7 +140,7 @@ __device__ __forceinline__ V ld_dim_l1p(const V* p, uint64_t pol) {
 // Vector body: rows [head, head + 4*nvec) where fact + head is 16B aligned.
 // OUT_VEC: out + head is aligned for Pack4 stores.
 template <typename V, bool OUT_VEC, int F>
-__global__ void __launch_bounds__((F & kPolHot) ? kThreadsHot : kThreads, (F & kPolHot) ? 1 : 2)
+__global__ void __launch_bounds__((F & kPolHot) ? kThreadsHot : kThreads, (F & kPolHot) ? 1 : SKX_GATHER_MINB)
     k_gather_vec(const uint32_t* __restrict__ fact, uint64_t head, uint64_t nvec,
                  const V* __restrict__ dim, uint64_t dim_len, V* __restrict__ out, DevErr* err,
                  GatherTiers tiers) {
