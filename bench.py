@@ -740,7 +740,7 @@ def other_configs(args, ctx, stream, dist_on, rank, world, peak):
         ctx.call("skx_select_gather_sum", C_ptr(fact_f), n5, C_ptr(bm.words), d5, C_ptr(cat),
                  # base 0: shard-local offsets (global ones exceed the reference's u32
                  # row offsets, operators.cpp:88-90, once 2^31 rows per GPU x N > 2^32)
-                 C_ptr(prc), C_ptr(sup), C_ptr(flg), 0, 1000, *[C_ptr(b) for b in bufs],
+                 C_ptr(prc), C_ptr(sup), C_ptr(flg), 0, 1000, cap, *[C_ptr(b) for b in bufs],
                  C_ptr(sums), C_ptr(cnt), ctx.stream(), sync=False)
         if dist_on:  # per-category fp64 partials reduced to rank 0
             reduce_to_root(sums)

@@ -24,9 +24,13 @@
  *    Enqueue one operator and skx_sync() to attribute an error to it; the
  *    C++ drop-in (the cpp/include/skewdx headers over libskewdx_b200.so) does that and rethrows the
  *    reference's exception types.
- *  - A context belongs to one device and one host thread; operators issued on
- *    one context must be ordered on one stream (the context owns scratch).
- *    Callers own every input and output buffer.
+ *  - A context belongs to one device and one host thread.  It owns the
+ *    scratch memory, kept as one set of arenas per stream: operators enqueued
+ *    on the same stream share that stream's set (so they are ordered), and
+ *    operators on different streams never share scratch.  Arenas grow
+ *    stream-ordered (cudaMallocAsync / cudaFreeAsync on the operator's
+ *    stream), so no operator synchronises the device; skx_reserve() grows
+ *    them up front.  Callers own every input and output buffer.
  *  - Host-buffer entry points (suffix _host) copy host -> device, run the
  *    kernel and copy back, pipelined in chunks over two streams; they are
  *    synchronous and report errors directly.
@@ -46,12 +50,14 @@ extern "C" {
 #define SKX_INVALID_ARGUMENT 1 /* skewdx::InvalidArgument */
 #define SKX_DOMAIN_VIOLATION 2 /* skewdx::DomainViolation{row, value, domain} */
 #define SKX_CUDA_ERROR 3
+#define SKX_NCCL_ERROR 4 /* a collective failed (multi-GPU combine steps) */
 #define SKX_ERROR 5 /* any other skewdx::Error */
 
 /* kMaxDomainCardinality, column.hpp:17 */
 #define SKX_MAX_DOMAIN_CARDINALITY 0xFFFFFFFEu
 
 typedef struct skx_ctx skx_ctx;
+typedef struct skx_comm skx_comm;
 
 typedef struct skx_error_info {
   int32_t status;
@@ -71,6 +77,15 @@ int skx_sync(skx_ctx* ctx, void* stream);
 int skx_last_error(const skx_ctx* ctx, skx_error_info* info);
 /* Number of kernels this context has launched since creation (bench evidence). */
 uint64_t skx_launch_count(const skx_ctx* ctx);
+/* Grow scratch arena `slot` (0..3, or -1 = all four) of `stream`'s set to at
+ * least `bytes`, stream-ordered on `stream`.  Operators grow their arenas on
+ * demand the same way; reserving first keeps allocation out of a timed or
+ * captured region.  Slots: 0 histogram / index sort / group-by staging,
+ * 1 rebuild counters / group-by accumulators / cache model, 2 selection,
+ * 3 spare.  No reference counterpart (the reference allocates per call). */
+int skx_reserve(skx_ctx* ctx, int slot, uint64_t bytes, void* stream);
+/* Current arena sizes (bytes[0..4)) of `stream`'s set (0 when it has none). */
+int skx_scratch_bytes(const skx_ctx* ctx, void* stream, uint64_t* bytes);
 
 /* ---- device memory for host-side callers (the C++ drop-in) --------------- */
 int skx_device_alloc(skx_ctx* ctx, uint64_t bytes, void** ptr);
@@ -179,13 +194,33 @@ int skx_build_bitmap_lt_i32(skx_ctx* ctx, const int32_t* dim, uint64_t d, int32_
  * (sums[n_categories] as fp64, overwritten; categories outside
  * [0, n_categories) are not summed): exact 96-bit fixed point when the
  * prices are finite, span <= 2^30 in exponent and n_categories <= 4096,
- * else an fp64 reduction (decided on the device).  Offsets get `base` added. */
+ * else an fp64 reduction (decided on the device).  Offsets get `base` added.
+ * The output columns hold `capacity` rows: *count_dev always receives the
+ * true number of selected rows; when it exceeds capacity only the first
+ * capacity rows are written (and the sums are unspecified) -- call again
+ * with capacity >= *count_dev (the reference returns exactly-sized vectors,
+ * operators.cpp:87-98; a device caller sizes its buffers up front). */
 int skx_select_gather_sum(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uint64_t* words,
                           uint32_t d, const int32_t* cat, const float* price,
                           const uint64_t* supp, const uint16_t* flag, uint32_t base,
-                          uint32_t n_categories, uint32_t* out_off, int32_t* out_cat,
-                          float* out_price, uint64_t* out_supp, uint16_t* out_flag,
-                          double* sums, uint64_t* count_dev, void* stream);
+                          uint32_t n_categories, uint64_t capacity, uint32_t* out_off,
+                          int32_t* out_cat, float* out_price, uint64_t* out_supp,
+                          uint16_t* out_flag, double* sums, uint64_t* count_dev, void* stream);
+
+/* Cross-GPU combine of config 5's category sums: the exact
+ * partial of the last skx_select_gather_sum enqueued on `stream`, as int64
+ * out[2 + 3 * n_categories]: out[0] = 1 if that call summed in 96-bit fixed
+ * point (else 0), out[1] = its scale S, out[2 + 3c ...] = the low / middle
+ * (unsigned) and high (signed) 32-bit limbs of category c's sum.  An
+ * element-wise integer SUM of these over ranks (skx_reduce, SKX_DT_I64) is
+ * exact; skx_select_sums_from_partials then writes sums[c] = total * 2^-S when
+ * all `nranks` ranks summed in fixed point with the same S, and leaves
+ * `sums` (the fp64-reduced sums) untouched otherwise.  The reference sums
+ * nothing across workers for this config; its fold order is the chunk order
+ * of parallel.cpp:102-129. */
+int skx_select_sum_partials(skx_ctx* ctx, uint32_t n_categories, int64_t* out, void* stream);
+int skx_select_sums_from_partials(skx_ctx* ctx, const int64_t* partials, uint32_t n_categories,
+                                  uint32_t nranks, double* sums, void* stream);
 
 /* ---- Q3a heavy hitters (operators.cpp:184-203) ---------------------------- *
  * counts[i] = #rows with id i+1 for i < min(k, d) on a recoded column. */
@@ -249,6 +284,64 @@ int skx_materialize_host(skx_ctx* ctx, int value_width, const uint32_t* fact, ui
 int skx_aggregate_host(skx_ctx* ctx, const uint32_t* fact, const void* measure,
                        int measure_width, uint64_t n, uint32_t d, uint32_t hot_threshold,
                        uint64_t* counts, uint64_t* sums);
+
+/* ---- multi-GPU: NCCL communicators and the combine steps ---------------- *
+ * SURVEY §8(b)/(e).  The reference combines per-worker partials on the host
+ * after its fork-join (parallel.cpp:147-207 fold; parallel_select's ordered
+ * concatenation, parallel.cpp:102-129); across GPUs those folds are NCCL
+ * collectives over NVLink / NVSwitch.  A communicator spans either several
+ * devices of this process (skx_comm_init_all: ncclCommInitAll, one context and
+ * one stream per device -- the C++ drop-in's multi-device overloads) or one
+ * device of a process-per-GPU job (skx_comm_init_rank with the 128-byte id
+ * from skx_comm_unique_id on rank 0).  Collectives take one buffer per LOCAL
+ * device (bufs[0..nlocal)) and optional per-device streams (NULL = the
+ * communicator's own streams), are asynchronous, and are group-launched
+ * across local devices.  Failures return SKX_NCCL_ERROR with the message in
+ * skx_comm_error() and in every local context's skx_last_error(). */
+#define SKX_COMM_MAX_LOCAL 16
+#define SKX_DT_U32 0
+#define SKX_DT_I32 1
+#define SKX_DT_U64 2
+#define SKX_DT_I64 3
+#define SKX_DT_F64 4
+#define SKX_OP_SUM 0
+#define SKX_OP_MIN 1
+#define SKX_OP_MAX 2
+int skx_comm_init_all(int ndev, const int* devices, skx_comm** out);
+int skx_comm_unique_id(void* id128);
+int skx_comm_init_rank(int device, int nranks, int rank, const void* id128, skx_comm** out);
+int skx_comm_destroy(skx_comm* comm);
+int skx_comm_info(const skx_comm* comm, int* nranks, int* rank0, int* nlocal);
+skx_ctx* skx_comm_ctx(skx_comm* comm, int local);
+void* skx_comm_stream(skx_comm* comm, int local);
+const char* skx_comm_error(const skx_comm* comm);
+/* Waits for every local stream and reports asynchronous NCCL errors. */
+int skx_comm_sync(skx_comm* comm);
+int skx_allreduce(skx_comm* comm, void* const* bufs, uint64_t count, int dtype, int op,
+                  void* const* streams);
+int skx_reduce(skx_comm* comm, void* const* bufs, uint64_t count, int dtype, int op, int root,
+               void* const* streams);
+int skx_reduce_scatter(skx_comm* comm, void* const* send, void* const* recv, uint64_t recvcount,
+                       int dtype, int op, void* const* streams);
+int skx_allgather(skx_comm* comm, void* const* send, void* const* recv, uint64_t sendcount,
+                  int dtype, void* const* streams);
+int skx_broadcast(skx_comm* comm, void* const* bufs, uint64_t count, int dtype, int root,
+                  void* const* streams);
+
+/* Group-by partials in the combine layout (config 3's per-GPU partials
+ * reduced to a root): buf (u64[d + hot]) = [counts[0..hot) | sums[0..hot) |
+ * packed[hot..d)] with packed[i] = counts[i] << 40 | sums[i] -- 8 B per tail
+ * key instead of 16.  guard (device u64[2]) = max tail count and max tail
+ * sum of this rank; after a SUM all-reduce of the guards over ranks,
+ * skx_groupby_packed_ok(host copy) says whether a u64 SUM-reduce of the
+ * packed buffers is exact (no field can overflow: counts < 2^24, sums <
+ * 2^40).  Otherwise reduce counts and sums directly.  sums may be NULL
+ * (COUNT only).  The reference's fold is parallel.cpp:155-157. */
+int skx_groupby_pack(skx_ctx* ctx, const uint64_t* counts, const uint64_t* sums, uint32_t d,
+                     uint32_t hot, uint64_t* buf, uint64_t* guard, void* stream);
+int skx_groupby_unpack(skx_ctx* ctx, const uint64_t* buf, uint32_t d, uint32_t hot,
+                       uint64_t* counts, uint64_t* sums, void* stream);
+int skx_groupby_packed_ok(const uint64_t* guard_sum);
 
 /* ---- tuning / evidence ---------------------------------------------------- *
  * Cache policy of the gathers (materialize/recode/permute), a bit set:

@@ -110,6 +110,18 @@ class Oracle:
         L.orc_estimate_hit_rate.argtypes = [vp, u64, u64, vp]
         L.orc_simulate_lru.argtypes = [vp, u64, u64, vp, vp, vp]
         L.orc_trace_from_column.argtypes = [vp, u64, u32, vp, vp, vp]
+        # multi-threaded forms (skx_oracle_mt.c) for BASELINE-scale parity
+        L.orc_find_domain_violation_mt.restype = u64
+        L.orc_find_domain_violation_mt.argtypes = [vp, u64, u64, u32]
+        L.orc_count_frequencies_mt.argtypes = [vp, u64, u32, vp, u32, vp, vp]
+        L.orc_build_index_radix.argtypes = [vp, u32, u64, vp, vp]
+        L.orc_gather_mt.argtypes = [C.c_int, vp, u64, vp, u64, vp, u32, vp, vp]
+        L.orc_aggregate_count_sum_mt.argtypes = [vp, vp, u64, u32, vp, vp, u32, vp, vp]
+        L.orc_select_gather_sum_mt.argtypes = [vp, u64, vp, u32, vp, vp, vp, vp, u32, u32,
+                                               vp, vp, vp, vp, vp, vp, vp, u64, u32, vp, vp]
+        L.orc_build_bitmap_lt_i32.argtypes = [vp, u64, C.c_int32, vp]
+        L.orc_fill_column.argtypes = [C.c_int, C.c_int, u64, u64, dbl, dbl, vp, u32]
+        self.threads = os.cpu_count() or 1
 
     # -- generator ------------------------------------------------------------
     def splitmix64(self, x: int) -> int:
@@ -276,6 +288,88 @@ class Oracle:
         e = _Err()
         e.check(self.L.orc_parallel_gather_u64(_p(fact), len(fact), _p(dim), len(dim), _p(out),
                                                threads, *e.args()))
+        return out
+
+    # -- multi-threaded forms (skx_oracle_mt.c): BASELINE-scale parity --------
+    def find_domain_violation_mt(self, fact, d):
+        fact = _u32(fact)
+        r = self.L.orc_find_domain_violation_mt(_p(fact), len(fact), d, self.threads)
+        return None if r == 2**64 - 1 else r
+
+    def count_frequencies_mt(self, fact, d):
+        fact = _u32(fact)
+        out = np.empty(d, np.uint64)
+        e = _Err()
+        e.check(self.L.orc_count_frequencies_mt(_p(fact), len(fact), d, _p(out), self.threads,
+                                                *e.args()))
+        return out
+
+    def build_index_radix(self, counts, total=None):
+        counts = _u64(counts)
+        d = len(counts)
+        total = int(counts.sum(dtype=np.uint64)) if total is None else total
+        off = np.empty(d, np.uint32)
+        rk = np.empty(d, np.uint32)
+        st = self.L.orc_build_index_radix(_p(counts), d, total, _p(off), _p(rk))
+        if st:
+            raise OracleError(st)
+        return off, rk
+
+    def gather_mt(self, fact, dim, out=None):
+        fact = _u32(fact)
+        dim = np.ascontiguousarray(dim)
+        out = np.empty(len(fact), dim.dtype) if out is None else out
+        e = _Err()
+        e.check(self.L.orc_gather_mt(dim.dtype.itemsize, _p(fact), len(fact), _p(dim), len(dim),
+                                     _p(out), self.threads, *e.args()))
+        return out
+
+    def aggregate_count_sum_mt(self, fact, measure, d):
+        fact = _u32(fact)
+        m = None if measure is None else _u64(measure)
+        counts = np.empty(d, np.uint64)
+        sums = np.empty(d, np.uint64)
+        e = _Err()
+        e.check(self.L.orc_aggregate_count_sum_mt(_p(fact), _p(m), len(fact), d, _p(counts),
+                                                  _p(sums), self.threads, *e.args()))
+        return counts, sums
+
+    def select_gather_sum_mt(self, fact, words, cat, price, supp, flag, n_categories, base=0,
+                             capacity=None):
+        fact = _u32(fact)
+        words = _u64(words)
+        cat = np.ascontiguousarray(cat, np.int32)
+        price = np.ascontiguousarray(price, np.float32)
+        supp = _u64(supp)
+        flag = np.ascontiguousarray(flag, np.uint16)
+        n = len(fact)
+        m = max(n if capacity is None else capacity, 1)
+        outs = [np.empty(m, t) for t in (np.uint32, np.int32, np.float32, np.uint64, np.uint16)]
+        sums = np.empty(n_categories, np.float64)
+        cnt = C.c_uint64(0)
+        e = _Err()
+        st = self.L.orc_select_gather_sum_mt(_p(fact), n, _p(words), len(cat), _p(cat), _p(price),
+                                             _p(supp), _p(flag), base, n_categories,
+                                             *[_p(o) for o in outs], _p(sums), C.byref(cnt), m,
+                                             self.threads, *e.args())
+        if st == INVALID and cnt.value > m:  # more rows selected than `capacity`: exact size
+            return self.select_gather_sum_mt(fact, words, cat, price, supp, flag, n_categories,
+                                             base, capacity=cnt.value)
+        e.check(st)
+        c = cnt.value
+        return tuple(o[:c] for o in outs) + (sums,)
+
+    def build_bitmap_lt_i32(self, dim, threshold):
+        dim = np.ascontiguousarray(dim, np.int32)
+        w = np.empty((len(dim) + 63) // 64, np.uint64)
+        self.L.orc_build_bitmap_lt_i32(_p(dim), len(dim), threshold, _p(w))
+        return w
+
+    def fill_column(self, kind, dtype, n, seed, p0=0.0, p1=0.0):
+        out = np.empty(n, dtype)
+        if self.L.orc_fill_column(kind, out.dtype.itemsize, seed & (2**64 - 1), n, float(p0),
+                                  float(p1), _p(out), self.threads):
+            raise OracleError(INVALID)
         return out
 
     def rolling_checksum(self, v):

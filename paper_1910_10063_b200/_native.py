@@ -13,8 +13,13 @@ from .errors import DomainViolation, Error, InvalidArgument, NativeUnavailable
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIBSKX = os.path.join(PKG, "libskx.so")
+# A/B runs of library variants point SKX_LIBSKX at the variant instead of
+# overwriting the in-tree build (tools/ab.sh).
+LIBSKX_PATH = os.environ.get("SKX_LIBSKX") or LIBSKX
 
-OK, INVALID_ARGUMENT, DOMAIN_VIOLATION, CUDA_ERROR, ERROR = 0, 1, 2, 3, 5
+OK, INVALID_ARGUMENT, DOMAIN_VIOLATION, CUDA_ERROR, NCCL_ERROR, ERROR = 0, 1, 2, 3, 4, 5
+DT_U32, DT_I32, DT_U64, DT_I64, DT_F64 = 0, 1, 2, 3, 4
+OP_SUM, OP_MIN, OP_MAX = 0, 1, 2
 
 
 class ErrorInfo(C.Structure):
@@ -33,6 +38,8 @@ SIGNATURES = {
     "skx_sync": (_int, [_vp, _vp]),
     "skx_last_error": (_int, [_vp, C.POINTER(ErrorInfo)]),
     "skx_launch_count": (_u64, [_vp]),
+    "skx_reserve": (_int, [_vp, _int, _u64, _vp]),
+    "skx_scratch_bytes": (_int, [_vp, _vp, _vp]),
     "skx_gather_u16": (_int, [_vp, _vp, _u64, _vp, _u64, _vp, _vp]),
     "skx_gather_u32": (_int, [_vp, _vp, _u64, _vp, _u64, _vp, _vp]),
     "skx_gather_u64": (_int, [_vp, _vp, _u64, _vp, _u64, _vp, _vp]),
@@ -49,7 +56,7 @@ SIGNATURES = {
     "skx_select_offsets": (_int, [_vp, _vp, _u64, _vp, _u64, _u32, _vp, _vp, _vp]),
     "skx_permute_bitmap": (_int, [_vp, _vp, _u64, _vp, _u32, _vp, _vp]),
     "skx_build_bitmap_lt_i32": (_int, [_vp, _vp, _u64, _i32, _vp, _vp]),
-    "skx_select_gather_sum": (_int, [_vp, _vp, _u64, _vp, _u32, _vp, _vp, _vp, _vp, _u32, _u32,
+    "skx_select_gather_sum": (_int, [_vp, _vp, _u64, _vp, _u32, _vp, _vp, _vp, _vp, _u32, _u32, _u64,
                                      _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "skx_heavy_hitter_count": (_int, [_vp, _vp, _u64, _u32, _u32, _vp, _vp]),
     "skx_zipf_cdf_host": (_int, [_u32, _dbl, _vp]),
@@ -79,13 +86,32 @@ SIGNATURES = {
     "skx_copy_to_host_async": (_int, [_vp, _vp, _vp, _u64, _vp]),
     "skx_find_domain_violation": (_int, [_vp, _vp, _u64, _u64, C.POINTER(_u64)]),
     "skx_fill_column": (_int, [_vp, _int, _int, _u64, _u64, _dbl, _dbl, _vp, _vp]),
+    "skx_select_sum_partials": (_int, [_vp, _u32, _vp, _vp]),
+    "skx_select_sums_from_partials": (_int, [_vp, _vp, _u32, _u32, _vp, _vp]),
+    "skx_groupby_pack": (_int, [_vp, _vp, _vp, _u32, _u32, _vp, _vp, _vp]),
+    "skx_groupby_unpack": (_int, [_vp, _vp, _u32, _u32, _vp, _vp, _vp]),
+    "skx_groupby_packed_ok": (_int, [_vp]),
+    "skx_comm_init_all": (_int, [_int, _vp, C.POINTER(_vp)]),
+    "skx_comm_unique_id": (_int, [_vp]),
+    "skx_comm_init_rank": (_int, [_int, _int, _int, _vp, C.POINTER(_vp)]),
+    "skx_comm_destroy": (_int, [_vp]),
+    "skx_comm_info": (_int, [_vp, C.POINTER(_int), C.POINTER(_int), C.POINTER(_int)]),
+    "skx_comm_ctx": (_vp, [_vp, _int]),
+    "skx_comm_stream": (_vp, [_vp, _int]),
+    "skx_comm_error": (C.c_char_p, [_vp]),
+    "skx_comm_sync": (_int, [_vp]),
+    "skx_allreduce": (_int, [_vp, _vp, _u64, _int, _int, _vp]),
+    "skx_reduce": (_int, [_vp, _vp, _u64, _int, _int, _int, _vp]),
+    "skx_reduce_scatter": (_int, [_vp, _vp, _vp, _u64, _int, _int, _vp]),
+    "skx_allgather": (_int, [_vp, _vp, _vp, _u64, _int, _vp]),
+    "skx_broadcast": (_int, [_vp, _vp, _u64, _int, _int, _vp]),
 }
 
 _lib = None
 _lock = threading.Lock()
 
 
-def load(path: str = LIBSKX) -> C.CDLL:
+def load(path: str = LIBSKX_PATH) -> C.CDLL:
     """Load libskx.so once (building it first if only the sources exist)."""
     global _lib
     with _lock:
@@ -119,4 +145,6 @@ def raise_for(status: int, info: ErrorInfo | None = None) -> None:
         raise InvalidArgument(msg)
     if status == CUDA_ERROR:
         raise Error("CUDA error: " + msg)
+    if status == NCCL_ERROR:
+        raise Error("NCCL error: " + msg)
     raise Error(msg)

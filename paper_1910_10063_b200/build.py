@@ -66,7 +66,9 @@ def build_libskx(force: bool = False, verbose: bool = False) -> str:
             if verbose and (r.stdout or r.stderr):
                 print(r.stdout, r.stderr)
     if force or jobs or _stale(LIBSKX, objs):
-        _run([nvcc, *ARCH, "-shared", "-o", LIBSKX, *objs, "-lcudart_static", "-lrt",
+        # NCCL: the libnccl.so.2 already mapped into the process is reused (torch's
+        # in Python, the system one for C++ hosts) -- one soname, one library
+        _run([nvcc, *ARCH, "-shared", "-o", LIBSKX, *objs, "-lcudart_static", "-lnccl", "-lrt",
               "-lpthread", "-ldl"])
     return LIBSKX
 

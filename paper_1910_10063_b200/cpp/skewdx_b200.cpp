@@ -19,6 +19,9 @@
 #include <fstream>
 #include <numeric>
 #include <random>
+#include <string>
+
+#include <unistd.h>
 
 #include "skewdx/column.hpp"
 #include "skewdx/column_io.hpp"
@@ -691,14 +694,28 @@ class SkdxReader {
   std::streampos payload_{};
 };
 
+// Streams the payload into a temporary file next to out_path and renames it
+// over out_path only in finish(), so an in-place apply (--fact-out == --fact)
+// reads the whole input before the output replaces it -- as the reference's
+// write_column(out, recode_fact(read_column(in))) does -- and any failure
+// (exception, domain violation) leaves out_path untouched: the destructor
+// removes an unfinished temporary.
 class SkdxWriter {
  public:
   SkdxWriter(const std::filesystem::path& path, std::uint64_t n)
-      : f_(path, std::ios::binary | std::ios::trunc), path_(path), n_(n) {
+      : path_(path),
+        tmp_(path.string() + ".tmp." + std::to_string(static_cast<long long>(::getpid()))),
+        n_(n) {
+    f_.open(tmp_, std::ios::binary | std::ios::trunc);
     if (!f_) throw IoError("cannot open for writing: " + path.string());
     f_.write("SKDX", 4);
     f_.write(reinterpret_cast<const char*>(&kVersion), 4);
     f_.write(reinterpret_cast<const char*>(&n), 8);
+  }
+  SkdxWriter(const SkdxWriter&) = delete;
+  SkdxWriter& operator=(const SkdxWriter&) = delete;
+  ~SkdxWriter() {
+    if (!done_) abandon();
   }
   void write(const std::uint32_t* src, std::uint64_t rows) {
     f_.write(reinterpret_cast<const char*>(src), static_cast<std::streamsize>(rows * 4));
@@ -708,17 +725,23 @@ class SkdxWriter {
     f_.flush();
     if (!f_ || written_ != n_) throw IoError("write failed: " + path_.string());
     f_.close();
+    std::error_code ec;
+    std::filesystem::rename(tmp_, path_, ec);
+    if (ec) throw IoError("cannot replace " + path_.string() + ": " + ec.message());
+    done_ = true;
   }
   void abandon() {
-    f_.close();
+    if (f_.is_open()) f_.close();
     std::error_code ec;
-    std::filesystem::remove(path_, ec);
+    std::filesystem::remove(tmp_, ec);
+    done_ = true;
   }
 
  private:
   std::ofstream f_;
-  std::filesystem::path path_;
+  std::filesystem::path path_, tmp_;
   std::uint64_t n_, written_ = 0;
+  bool done_ = false;
 };
 
 // After the device reported a violation somewhere in the stream: the first

@@ -22,11 +22,16 @@
 // both the reductions and the accumulator footprint of the {count, sum} pair
 // layout (tools/probe/agg_probe.cu: 9.6 -> 5.9 ms at C3).  Exactness is
 // proved on the device, not assumed: every CTA also counts its packed rows
-// and their measure sum exactly; the decode pass sums the decoded fields; a
-// key whose sum reached 2^40 (or whose count reached 2^24) makes the decoded
-// totals fall short, because every decoded field is <= its true value with
-// equality iff it did not overflow.  Rows with m >= 2^16 are not packed (so
-// the exact totals cannot wrap) and flag the launch.  On any flag or
+// and their measure sum exactly; the decode pass sums the decoded fields and
+// both totals must match.  The argument, for a key with true count C and sum
+// S whose word is W = (C << 40) + S mod 2^64: the decoded sum is S mod 2^40
+// <= S, with equality iff S < 2^40; the totals cannot wrap (rows with
+// m >= 2^16 are not packed and flag the launch, so the exact sum stays below
+// 2^50), hence equal sum totals prove S < 2^40 for EVERY key.  Only then is
+// there no carry from the sum field into the count field, so the decoded
+// count is C mod 2^24 <= C, with equality iff C < 2^24, and equal count
+// totals prove every count exact.  (Without the sum check a carry could make
+// a decoded count LARGER than C; the count check alone would not be sound.)  On any flag or
 // mismatch three gated kernels, already queued behind the decode, redo the
 // whole call with two exact reductions per cold row on an interleaved
 // {count, sum} pair (mode 2); otherwise they exit at once.  No host sync.
@@ -560,7 +565,7 @@ int aggregate_impl(skx_ctx* ctx, const uint32_t* fact, const void* measure, uint
     t.wshift = wshift;
     t.cap = n / (2 * (uint64_t)t.nb) + 4096;
     const uint64_t kb = ((uint64_t)t.nb * t.cap * 4 + 255) & ~uint64_t(255);
-    char* sp = static_cast<char*>(scratch(ctx, 0, 256 + kb + (uint64_t)t.nb * t.cap * 8));
+    char* sp = static_cast<char*>(scratch(ctx, 0, 256 + kb + (uint64_t)t.nb * t.cap * 8, s));
     if (!sp) return set_error(ctx, SKX_CUDA_ERROR, "aggregate: out of device memory for staging");
     t.cursors = reinterpret_cast<unsigned long long*>(sp);
     t.keys = reinterpret_cast<uint32_t*>(sp + 256);
@@ -603,7 +608,7 @@ int launch_aggregate(skx_ctx* ctx, const uint32_t* fact, const void* measure, in
     if (n == 0) return SKX_OK;
     if (n < 0xFFFFFFFFull && d >= (1u << 20)) {
       // u32 counts are exact below 2^32 rows and halve the tail's footprint
-      unsigned int* c32 = static_cast<unsigned int*>(scratch(ctx, 1, (size_t)d * 4));
+      unsigned int* c32 = static_cast<unsigned int*>(scratch(ctx, 1, (size_t)d * 4, s));
       if (!c32) return set_error(ctx, SKX_CUDA_ERROR, "aggregate: out of device memory");
       e = cudaMemsetAsync(c32, 0, (size_t)d * 4, s);
       if (e != cudaSuccess) return cuda_fail(ctx, e, "aggregate memset");
@@ -638,7 +643,7 @@ int launch_aggregate(skx_ctx* ctx, const uint32_t* fact, const void* measure, in
   const size_t chk_b = 256, hp_b = up((size_t)hot * 16), acc_b = up((size_t)far * 8);
   const size_t acc32_b = up((size_t)(d - far) * 4);
   const size_t pairs_off = pack ? chk_b + hp_b + acc_b + acc32_b : 0;
-  char* base = static_cast<char*>(scratch(ctx, 1, pairs_off + (size_t)d * 16 + 16));
+  char* base = static_cast<char*>(scratch(ctx, 1, pairs_off + (size_t)d * 16 + 16, s));
   if (!base) return set_error(ctx, SKX_CUDA_ERROR, "aggregate: out of device memory");
   unsigned long long* pairs = reinterpret_cast<unsigned long long*>(base + pairs_off);
   unsigned long long* counts64 = reinterpret_cast<unsigned long long*>(counts);

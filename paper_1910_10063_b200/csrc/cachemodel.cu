@@ -182,7 +182,7 @@ int skx_line_frequencies(skx_ctx* ctx, const double* value_freqs, uint32_t d,
                                                                         lines, out);
     ctx->launches++;
   } else {
-    uint32_t* inv = static_cast<uint32_t*>(scratch(ctx, 1, (size_t)d * 4));
+    uint32_t* inv = static_cast<uint32_t*>(scratch(ctx, 1, (size_t)d * 4, s));
     if (!inv) return set_error(ctx, SKX_CUDA_ERROR, "line_frequencies: out of device memory");
     k_invert<<<grid_for(ctx, d, 256, 8), 256, 0, s>>>(rank_to_id, d, inv);
     k_line_freq_scattered<<<grid_for(ctx, lines, 256, 8), 256, 0, s>>>(value_freqs, d, per_line,
@@ -216,7 +216,7 @@ int skx_estimate_hit_rate(skx_ctx* ctx, const double* line_freqs, uint64_t nline
   const size_t tmp_b = (sort_b > scan_b ? sort_b : scan_b);
   auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
   const size_t arr_b = up((size_t)n * 8);
-  char* sp = static_cast<char*>(scratch(ctx, 1, 2 * arr_b + up(tmp_b) + 256));
+  char* sp = static_cast<char*>(scratch(ctx, 1, 2 * arr_b + up(tmp_b) + 256, s));
   if (!sp) return set_error(ctx, SKX_CUDA_ERROR, "estimate_hit_rate: out of device memory");
   double* sorted = reinterpret_cast<double*>(sp);
   double* incl = reinterpret_cast<double*>(sp + arr_b);

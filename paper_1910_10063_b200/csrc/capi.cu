@@ -24,16 +24,17 @@ int cuda_fail(skx_ctx* ctx, cudaError_t e, const char* where) {
   return set_error(ctx, SKX_CUDA_ERROR, "%s: %s", where, cudaGetErrorString(e));
 }
 
-static void* grow(Scratch& sc, size_t bytes) {
+// Stream-ordered growth: the old arena is released after the work already
+// queued on s, the new one is valid for everything enqueued on s afterwards.
+static void* grow(Scratch& sc, size_t bytes, cudaStream_t s) {
   if (sc.bytes >= bytes && sc.ptr) return sc.ptr;
   if (sc.ptr) {
-    cudaDeviceSynchronize();
-    cudaFree(sc.ptr);
+    cudaFreeAsync(sc.ptr, s);
     sc.ptr = nullptr;
     sc.bytes = 0;
   }
   size_t want = bytes < 4096 ? 4096 : bytes;
-  if (cudaMalloc(&sc.ptr, want) != cudaSuccess) {
+  if (cudaMallocAsync(&sc.ptr, want, s) != cudaSuccess) {
     cudaGetLastError();
     sc.ptr = nullptr;
     return nullptr;
@@ -42,8 +43,39 @@ static void* grow(Scratch& sc, size_t bytes) {
   return sc.ptr;
 }
 
-void* scratch(skx_ctx* ctx, int slot, size_t bytes) { return grow(ctx->scratch[slot], bytes); }
-void* host_scratch_dev(skx_ctx* ctx, int slot, size_t bytes) { return grow(ctx->hb[slot], bytes); }
+static ScratchSet* set_for(skx_ctx* ctx, cudaStream_t s) {
+  for (auto& st : ctx->sets)
+    if (st.used && st.stream == s) return &st;
+  for (auto& st : ctx->sets)
+    if (!st.used) {
+      st.used = true;
+      st.stream = s;
+      return &st;
+    }
+  // More streams than sets: recycle the least recently added set once its
+  // stream has drained (rare; callers normally use one or two streams).
+  ScratchSet* victim = &ctx->sets[0];
+  cudaStreamSynchronize(victim->stream);
+  for (auto& sc : victim->slot) {
+    if (sc.ptr) cudaFree(sc.ptr);
+    sc = Scratch{};
+  }
+  for (int i = 0; i + 1 < kScratchSets; ++i) ctx->sets[i] = ctx->sets[i + 1];
+  ScratchSet* st = &ctx->sets[kScratchSets - 1];
+  *st = ScratchSet{};
+  st->used = true;
+  st->stream = s;
+  return st;
+}
+
+ScratchSet* scratch_set(skx_ctx* ctx, cudaStream_t s) { return set_for(ctx, s); }
+
+void* scratch(skx_ctx* ctx, int slot, size_t bytes, cudaStream_t s) {
+  return grow(set_for(ctx, s)->slot[slot], bytes, s);
+}
+void* host_scratch_dev(skx_ctx* ctx, int slot, size_t bytes, cudaStream_t s) {
+  return grow(ctx->hb[slot], bytes, s);
+}
 
 static void reset_err_host(DevErr* e) {
   for (int i = 0; i < kViolSlots; ++i) e->viol[i] = ~0ull;
@@ -111,8 +143,9 @@ int skx_ctx_destroy(skx_ctx* ctx) {
   if (!ctx) return SKX_OK;
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
-  for (auto& sc : ctx->scratch)
-    if (sc.ptr) cudaFree(sc.ptr);
+  for (auto& st : ctx->sets)
+    for (auto& sc : st.slot)
+      if (sc.ptr) cudaFree(sc.ptr);
   for (auto& sc : ctx->hb)
     if (sc.ptr) cudaFree(sc.ptr);
   for (auto& s : ctx->hstream)
@@ -126,6 +159,27 @@ int skx_ctx_destroy(skx_ctx* ctx) {
 }
 
 uint64_t skx_launch_count(const skx_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
+
+int skx_reserve(skx_ctx* ctx, int slot, uint64_t bytes, void* stream) {
+  if (!ctx || slot < -1 || slot >= kScratchSlots) return SKX_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = as_stream(stream);
+  for (int i = (slot < 0 ? 0 : slot); i < (slot < 0 ? kScratchSlots : slot + 1); ++i)
+    if (!scratch(ctx, i, bytes, s))
+      return set_error(ctx, SKX_CUDA_ERROR, "reserve: out of device memory (%llu bytes)",
+                       (unsigned long long)bytes);
+  return SKX_OK;
+}
+
+int skx_scratch_bytes(const skx_ctx* ctx, void* stream, uint64_t* bytes) {
+  if (!ctx || !bytes) return SKX_INVALID_ARGUMENT;
+  cudaStream_t s = as_stream(stream);
+  for (int i = 0; i < kScratchSlots; ++i) bytes[i] = 0;
+  for (const auto& st : ctx->sets)
+    if (st.used && st.stream == s)
+      for (int i = 0; i < kScratchSlots; ++i) bytes[i] = st.slot[i].bytes;
+  return SKX_OK;
+}
 
 int skx_set_gather_policy(skx_ctx* ctx, int policy) {
   if (!ctx || policy < 0 || policy > 2047) return SKX_INVALID_ARGUMENT;
@@ -311,9 +365,9 @@ int skx_materialize_host(skx_ctx* ctx, int w, const uint32_t* fact, uint64_t n, 
   if (w != 2 && w != 4 && w != 8) return set_error(ctx, SKX_INVALID_ARGUMENT, "bad value width");
   cudaSetDevice(ctx->device);
   const uint64_t chunk = uint64_t(1) << 25;  // rows per pipeline stage
-  void* d_dim = host_scratch_dev(ctx, 0, dim_len * w + 16);
-  void* d_fact[2] = {host_scratch_dev(ctx, 1, chunk * 4), host_scratch_dev(ctx, 2, chunk * 4)};
-  void* d_out[2] = {host_scratch_dev(ctx, 3, chunk * w), host_scratch_dev(ctx, 4, chunk * w)};
+  void* d_dim = host_scratch_dev(ctx, 0, dim_len * w + 16, ctx->hstream[0]);
+  void* d_fact[2] = {host_scratch_dev(ctx, 1, chunk * 4, ctx->hstream[0]), host_scratch_dev(ctx, 2, chunk * 4, ctx->hstream[0])};
+  void* d_out[2] = {host_scratch_dev(ctx, 3, chunk * w, ctx->hstream[0]), host_scratch_dev(ctx, 4, chunk * w, ctx->hstream[0])};
   if (!d_dim || !d_fact[0] || !d_fact[1] || !d_out[0] || !d_out[1])
     return set_error(ctx, SKX_CUDA_ERROR, "materialize_host: out of device memory");
   cudaError_t e = cudaMemcpyAsync(d_dim, dim, dim_len * w, cudaMemcpyHostToDevice, ctx->hstream[0]);
@@ -357,9 +411,9 @@ int skx_aggregate_host(skx_ctx* ctx, const uint32_t* fact, const void* measure, 
   if (!ctx) return SKX_INVALID_ARGUMENT;
   if (mw != 0 && mw != 4 && mw != 8) return set_error(ctx, SKX_INVALID_ARGUMENT, "bad measure width");
   cudaSetDevice(ctx->device);
-  void* d_fact = host_scratch_dev(ctx, 1, n * 4 + 16);
-  void* d_meas = mw ? host_scratch_dev(ctx, 3, n * mw + 16) : nullptr;
-  void* d_out = host_scratch_dev(ctx, 0, uint64_t(d) * 16 + 16);
+  void* d_fact = host_scratch_dev(ctx, 1, n * 4 + 16, ctx->hstream[0]);
+  void* d_meas = mw ? host_scratch_dev(ctx, 3, n * mw + 16, ctx->hstream[0]) : nullptr;
+  void* d_out = host_scratch_dev(ctx, 0, uint64_t(d) * 16 + 16, ctx->hstream[0]);
   if (!d_fact || (mw && !d_meas) || !d_out)
     return set_error(ctx, SKX_CUDA_ERROR, "aggregate_host: out of device memory");
   cudaStream_t st = ctx->hstream[0];

@@ -413,7 +413,7 @@ int histogram_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64_t n
     // of 4 so full 8-entry flushes can use 16-byte stores
     bk.cap = (n / kNB + 65536 + 3) & ~uint64_t(3);
     if (bk.cap > 0xFFFFFFFCull) bk.cap = 0xFFFFFFFCull;
-    char* sp = static_cast<char*>(scratch(ctx, 0, (uint64_t)kNB * bk.cap * 4 + 512));
+    char* sp = static_cast<char*>(scratch(ctx, 0, (uint64_t)kNB * bk.cap * 4 + 512, s));
     if (!sp) return set_error(ctx, SKX_CUDA_ERROR, "histogram: out of device memory for buckets");
     bk.cursors = reinterpret_cast<unsigned int*>(sp);
     bk.buf = reinterpret_cast<uint32_t*>(sp + 512);
@@ -438,7 +438,7 @@ int histogram_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64_t n
     // saves: C4 2.89 -> 3.38 ms).  counts were zeroed by the caller, so the
     // gated fallback may zero them again and recount directly.
     const size_t w16 = (((size_t)d + 1) / 2) * 4;
-    char* sp = static_cast<char*>(scratch(ctx, 0, 256 + w16));
+    char* sp = static_cast<char*>(scratch(ctx, 0, 256 + w16, s));
     if (!sp) return set_error(ctx, SKX_CUDA_ERROR, "histogram: out of device memory");
     HistCheck* chk = reinterpret_cast<HistCheck*>(sp);
     unsigned int* c16 = reinterpret_cast<unsigned int*>(sp + 256);

@@ -322,12 +322,17 @@ inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 template <typename CT, typename K>
 int build_index_impl(skx_ctx* ctx, const CT* counts, uint32_t d, uint64_t total,
                      uint32_t* offsets, uint32_t* ranks, cudaStream_t s) {
-  const uint32_t ntiles = (d + kTile - 1) / kTile;
+  // in 64 bits: d up to 0xFFFFFFFE would wrap a 32-bit (d + kTile - 1)
+  const uint64_t ntiles64 = ((uint64_t)d + kTile - 1) / kTile;
+  if (ntiles64 > 0x7FFFFFFFull)
+    return set_error(ctx, SKX_INVALID_ARGUMENT, "build_index: %llu tiles exceed the launch grid",
+                     (unsigned long long)ntiles64);
+  const uint32_t ntiles = (uint32_t)ntiles64;
   // scratch layout: keys[2][d] | vals[2][d] | tile_nnz[ntiles] | tile_off[ntiles] |
   //                 hist[256*ntiles] | nnz
   const size_t kb = align_up(sizeof(K) * (size_t)d), vb = align_up(4 * (size_t)d);
   const size_t tb = align_up(4 * (size_t)ntiles), hb = align_up(4 * 256 * (size_t)ntiles);
-  char* sp = static_cast<char*>(scratch(ctx, 0, 2 * kb + 2 * vb + 2 * tb + hb + 256));
+  char* sp = static_cast<char*>(scratch(ctx, 0, 2 * kb + 2 * vb + 2 * tb + hb + 256, s));
   if (!sp) return set_error(ctx, SKX_CUDA_ERROR, "build_index: out of device memory for scratch");
   K* keys[2] = {reinterpret_cast<K*>(sp), reinterpret_cast<K*>(sp + kb)};
   uint32_t* vals[2] = {reinterpret_cast<uint32_t*>(sp + 2 * kb),
@@ -421,7 +426,7 @@ int launch_exclusive_scan_u32(skx_ctx* ctx, const uint32_t* in, uint32_t* out, u
                               uint32_t* total_dev, int slot, cudaStream_t s) {
   if (m == 0) return SKX_OK;
   const uint64_t np = (m + kTile - 1) / kTile;
-  uint32_t* partials = static_cast<uint32_t*>(scratch(ctx, slot, np * 4 + 64));
+  uint32_t* partials = static_cast<uint32_t*>(scratch(ctx, slot, np * 4 + 64, s));
   if (!partials) return set_error(ctx, SKX_CUDA_ERROR, "scan: out of device memory");
   k_scan_partials<<<(unsigned)np, kTileThreads, 0, s>>>(in, m, partials);
   k_scan_top<<<1, 1024, 0, s>>>(partials, np, total_dev);
@@ -466,7 +471,7 @@ int skx_rebuild(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint32_t d, uint
   // u32 counters suffice below 2^32 rows (halves atomic and scan bytes).
   const bool narrow = n <= 0xFFFFFFFFull;
   const size_t cb = narrow ? 4 : 8;
-  void* counts = skx::scratch(ctx, 1, cb * (size_t)d + 16);
+  void* counts = skx::scratch(ctx, 1, cb * (size_t)d + 16, s);
   if (!counts) return skx::set_error(ctx, SKX_CUDA_ERROR, "rebuild: out of device memory");
   if (d > 0) {
     cudaError_t e = cudaMemsetAsync(counts, 0, cb * (size_t)d, s);

@@ -78,6 +78,7 @@ struct Cols {
   const uint4* rec;          // [d][2]: {cat, price, supp lo, supp hi}, {flag, 0, 0, 0}
   struct SumCtl* ctl;
   unsigned int* acc96;       // [n_categories][4]: lo, mid, hi, pad
+  unsigned long long cap;    // output rows the caller's buffers hold
 };
 
 // Price exponent range for the fixed-point sums (frexp exponent + 1024).
@@ -413,14 +414,17 @@ template <bool FUSED>
 __device__ __forceinline__ void emit_row(uint64_t p, uint32_t row, const Rec8& r,
                                          uint32_t base_off, uint32_t* __restrict__ out_off,
                                          const Cols& cols, bool fixed, int S, unsigned int* s_acc) {
-  out_off[p] = base_off + row;
+  const bool fits = p < cols.cap;  // rows past the caller's capacity are counted, not written
+  if (fits) out_off[p] = base_off + row;
   if (FUSED) {
     const int32_t ct = (int32_t)r.a0;
     const float pr = __uint_as_float(r.a1);
-    cols.out_cat[p] = ct;
-    cols.out_price[p] = pr;
-    cols.out_supp[p] = (unsigned long long)r.a2 | ((unsigned long long)r.a3 << 32);
-    cols.out_flag[p] = (uint16_t)r.b0;
+    if (fits) {
+      cols.out_cat[p] = ct;
+      cols.out_price[p] = pr;
+      cols.out_supp[p] = (unsigned long long)r.a2 | ((unsigned long long)r.a3 << 32);
+      cols.out_flag[p] = (uint16_t)r.b0;
+    }
     const uint32_t ncat = cols.n_categories;
     if (fixed && (uint32_t)ct < ncat) {
       const long long v = __double2ll_rn(ldexp((double)pr, S));
@@ -588,6 +592,44 @@ __global__ void k_sum_finalize(const unsigned int* __restrict__ acc96, const Sum
   }
 }
 
+// Cross-GPU combine of the fixed-point sums (skx_select_sum_partials): the
+// three 32-bit limbs of each category's 96-bit sum, widened to int64 (low and
+// middle unsigned, high signed) so an element-wise integer SUM over ranks is
+// exact; out[0] = 1 when this rank summed in fixed point, out[1] = its scale.
+__global__ void k_sum_partials(const unsigned int* __restrict__ acc96, const SumCtl* ctl,
+                               uint32_t ncat, long long* __restrict__ out) {
+  int S = 0;
+  const bool fx = ctl != nullptr && fixed_ok(ctl, ncat, S);
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t == 0) {
+    out[0] = fx ? 1 : 0;
+    out[1] = fx ? S : 0;
+  }
+  for (uint32_t c = t; c < ncat; c += gridDim.x * blockDim.x) {
+    const unsigned int* g = acc96 + 4 * (uint64_t)c;
+    out[2 + 3 * (uint64_t)c] = fx ? (long long)g[0] : 0;
+    out[3 + 3 * (uint64_t)c] = fx ? (long long)g[1] : 0;
+    out[4 + 3 * (uint64_t)c] = fx ? (long long)(int)g[2] : 0;
+  }
+}
+
+// After the SUM over `nranks` partials: when every rank summed in fixed point
+// with one scale S, sums[c] = (lo + mid 2^32 + hi 2^64) 2^-S, carried exactly
+// in 128 bits and rounded once per part; else the fp64 sums stay as they are.
+__global__ void k_sums_from_partials(const long long* __restrict__ p, uint32_t ncat,
+                                     uint32_t nranks, double* __restrict__ sums) {
+  if (p[0] != (long long)nranks || p[1] % (long long)nranks != 0) return;
+  const int S = (int)(p[1] / (long long)nranks);
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < ncat; c += gridDim.x * blockDim.x) {
+    const __int128 v = (__int128)p[2 + 3 * (uint64_t)c] + ((__int128)p[3 + 3 * (uint64_t)c] << 32) +
+                       ((__int128)p[4 + 3 * (uint64_t)c] << 64);
+    const double top = (double)(long long)(v >> 64);
+    const double mid = (double)(unsigned long long)((unsigned long long)(v >> 32) & 0xffffffffull);
+    const double low = (double)(unsigned long long)((unsigned long long)v & 0xffffffffull);
+    sums[c] = ldexp(ldexp(top, 64) + (ldexp(mid, 32) + low), -S);
+  }
+}
+
 // Pass 3 (C5): SUM(price) per category over the compacted selected rows --
 // a coalesced read of the gathered category/price columns.  Warp-private
 // fp64 shared bins; lanes of one category pre-sum with __match_any_sync +
@@ -595,7 +637,7 @@ __global__ void k_sum_finalize(const unsigned int* __restrict__ acc96, const Sum
 // global fp64 reduction per bin per CTA.
 __global__ void __launch_bounds__(kThreads)
     k_category_sum(const int32_t* __restrict__ cat, const float* __restrict__ price,
-                   const uint32_t* __restrict__ total, uint32_t n_categories,
+                   const uint32_t* __restrict__ total, uint64_t cap, uint32_t n_categories,
                    double* __restrict__ sums, const SumCtl* ctl) {
   int S_unused = 0;
   if (fixed_ok(ctl, n_categories, S_unused)) return;  // summed in pass 2
@@ -607,7 +649,7 @@ __global__ void __launch_bounds__(kThreads)
     __syncthreads();
   }
   constexpr int U = 8;  // rows per thread per iteration, loads issued first
-  const uint64_t cnt = *total;
+  const uint64_t cnt = *total < cap ? *total : cap;
   const uint64_t stride = (uint64_t)gridDim.x * kThreads * U;
   for (uint64_t j0 = (uint64_t)blockIdx.x * kThreads * U; j0 < cnt; j0 += stride) {  // uniform trips
     int32_t ct[U];
@@ -688,7 +730,7 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
     e = cudaMemsetAsync(cols.sums, 0, (size_t)cols.n_categories * 8, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "select memset");
   }
-  if (n == 0) {
+  if (n == 0 && !fused) {
     e = cudaMemsetAsync(count_dev, 0, 8, s);
     return e == cudaSuccess ? SKX_OK : cuda_fail(ctx, e, "select memset");
   }
@@ -699,7 +741,7 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
   const uint64_t base_b = (ent_b + nslices * 8 + 256 + 255) & ~uint64_t(255);
   const uint64_t acc_b = fused ? (((uint64_t)cols.n_categories * 16 + 255) & ~uint64_t(255)) : 0;
   const uint64_t rec_b = fused ? bits * 32 : 0;
-  char* raw = static_cast<char*>(scratch(ctx, 2, base_b + (fused ? 256 : 0) + acc_b + rec_b));
+  char* raw = static_cast<char*>(scratch(ctx, 2, base_b + (fused ? 256 : 0) + acc_b + rec_b, s));
   if (!raw) return set_error(ctx, SKX_CUDA_ERROR, "select: out of device memory");
   uint2* entries = reinterpret_cast<uint2*>(raw);
   uint32_t* counts = reinterpret_cast<uint32_t*>(raw + ent_b);
@@ -709,6 +751,10 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
     cols.ctl = reinterpret_cast<SumCtl*>(raw + base_b);
     cols.acc96 = reinterpret_cast<unsigned int*>(raw + base_b + 256);
     cols.rec = reinterpret_cast<const uint4*>(raw + base_b + 256 + acc_b);
+    ScratchSet* ss = scratch_set(ctx, s);
+    ss->sel_acc = cols.acc96;
+    ss->sel_ctl = cols.ctl;
+    ss->sel_ncat = cols.n_categories;
     e = cudaMemsetAsync(raw + base_b, 0, 256 + acc_b, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "select memset");
     if (bits) {
@@ -716,6 +762,10 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
           cols.cat, cols.price, cols.supp, cols.flag, (uint32_t)bits,
           const_cast<uint4*>(cols.rec), cols.ctl);
       ctx->launches++;
+    }
+    if (n == 0) {  // no rows: zero sums and count; the scale is still recorded for combining
+      e = cudaMemsetAsync(count_dev, 0, 8, s);
+      return e == cudaSuccess ? SKX_OK : cuda_fail(ctx, e, "select memset");
     }
   }
   const bool vec = reinterpret_cast<uintptr_t>(fact) % 16 == 0;
@@ -756,7 +806,7 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
     int per_sm3 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, k_category_sum, kThreads, bsmem);
     k_category_sum<<<(unsigned)ctx->num_sms * (per_sm3 < 1 ? 1 : per_sm3), kThreads, bsmem, s>>>(
-        cols.out_cat, cols.out_price, total, cols.n_categories, cols.sums, cols.ctl);
+        cols.out_cat, cols.out_price, total, cols.cap, cols.n_categories, cols.sums, cols.ctl);
     ctx->launches += 2;
   }
   SKX_CHECK_LAUNCH(ctx, "select");
@@ -773,6 +823,7 @@ int skx_select_offsets(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uin
                        void* stream) {
   if (!ctx) return SKX_INVALID_ARGUMENT;
   skx::Cols cols{};
+  cols.cap = n;  // KernelTable::select_offsets contract: out holds n entries
   return skx::select_impl(ctx, false, fact, n, words, bits, base, out, cols, count_dev,
                           skx::as_stream(stream));
 }
@@ -780,18 +831,45 @@ int skx_select_offsets(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uin
 int skx_select_gather_sum(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uint64_t* words,
                           uint32_t d, const int32_t* cat, const float* price,
                           const uint64_t* supp, const uint16_t* flag, uint32_t base,
-                          uint32_t n_categories, uint32_t* out_off, int32_t* out_cat,
-                          float* out_price, uint64_t* out_supp, uint16_t* out_flag, double* sums,
-                          uint64_t* count_dev, void* stream) {
+                          uint32_t n_categories, uint64_t capacity, uint32_t* out_off,
+                          int32_t* out_cat, float* out_price, uint64_t* out_supp,
+                          uint16_t* out_flag, double* sums, uint64_t* count_dev, void* stream) {
   if (!ctx) return SKX_INVALID_ARGUMENT;
   if (n && (!cat || !price || !supp || !flag || !out_cat || !out_price || !out_supp || !out_flag ||
             (n_categories && !sums)))
     return skx::set_error(ctx, SKX_INVALID_ARGUMENT, "select_gather_sum: null column pointer");
   skx::Cols cols{cat, price, reinterpret_cast<const unsigned long long*>(supp), flag,
                  out_cat, out_price, reinterpret_cast<unsigned long long*>(out_supp), out_flag,
-                 sums, n_categories, nullptr, nullptr, nullptr};
+                 sums, n_categories, nullptr, nullptr, nullptr, capacity};
   return skx::select_impl(ctx, true, fact, n, words, d, base, out_off, cols, count_dev,
                           skx::as_stream(stream));
+}
+
+int skx_select_sum_partials(skx_ctx* ctx, uint32_t n_categories, int64_t* out, void* stream) {
+  if (!ctx || !out) return SKX_INVALID_ARGUMENT;
+  cudaStream_t s = skx::as_stream(stream);
+  skx::ScratchSet* ss = skx::scratch_set(ctx, s);
+  if (!ss->sel_acc || ss->sel_ncat != n_categories)
+    return skx::set_error(ctx, SKX_INVALID_ARGUMENT,
+                          "select_sum_partials: no select_gather_sum with %u categories on this stream",
+                          n_categories);
+  skx::k_sum_partials<<<(n_categories + 255) / 256 + 1, 256, 0, s>>>(
+      static_cast<const unsigned int*>(ss->sel_acc), static_cast<const skx::SumCtl*>(ss->sel_ctl),
+      n_categories, reinterpret_cast<long long*>(out));
+  ctx->launches++;
+  SKX_CHECK_LAUNCH(ctx, "select_sum_partials");
+  return SKX_OK;
+}
+
+int skx_select_sums_from_partials(skx_ctx* ctx, const int64_t* partials, uint32_t n_categories,
+                                  uint32_t nranks, double* sums, void* stream) {
+  if (!ctx || !partials || !sums || nranks == 0) return SKX_INVALID_ARGUMENT;
+  if (n_categories == 0) return SKX_OK;
+  skx::k_sums_from_partials<<<(n_categories + 255) / 256, 256, 0, skx::as_stream(stream)>>>(
+      reinterpret_cast<const long long*>(partials), n_categories, nranks, sums);
+  ctx->launches++;
+  SKX_CHECK_LAUNCH(ctx, "select_sums_from_partials");
+  return SKX_OK;
 }
 
 int skx_permute_bitmap(skx_ctx* ctx, const uint64_t* words, uint64_t bits, const uint32_t* offsets,

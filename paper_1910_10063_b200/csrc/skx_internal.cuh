@@ -135,6 +135,21 @@ struct Scratch {
   void* ptr = nullptr;
   size_t bytes = 0;
 };
+// Scratch arenas are kept per stream: an operator only ever touches the set of
+// the stream it is enqueued on, and a set grows with stream-ordered
+// cudaFreeAsync / cudaMallocAsync on that stream -- no device-wide
+// synchronisation, and two host streams of one context never share scratch.
+constexpr int kScratchSlots = 4;
+constexpr int kScratchSets = 6;
+struct ScratchSet {
+  bool used = false;
+  cudaStream_t stream = nullptr;
+  Scratch slot[kScratchSlots];
+  // the last fused selection on this stream (skx_select_sum_partials)
+  void* sel_acc = nullptr;
+  void* sel_ctl = nullptr;
+  uint32_t sel_ncat = 0;
+};
 
 }  // namespace skx
 
@@ -157,9 +172,9 @@ struct skx_ctx {
   int agg_mode = 0;  // group-by cold tail: 0 packed + exact fallback, 1 staged, 2 direct pairs
   std::atomic<uint64_t> launches{0};
   skx_error_info last{};
-  // scratch arenas (grow-only)
-  skx::Scratch scratch[4];
-  // host-buffer pipeline buffers
+  // scratch arenas (grow-only, stream-ordered), one set per stream
+  skx::ScratchSet sets[skx::kScratchSets];
+  // host-buffer pipeline buffers (grown on hstream[0] by the _host entries)
   skx::Scratch hb[6];
   cudaStream_t hstream[2] = {nullptr, nullptr};
   cudaEvent_t hevent[4] = {};
@@ -169,9 +184,12 @@ namespace skx {
 
 int set_error(skx_ctx* ctx, int status, const char* fmt, ...);
 int cuda_fail(skx_ctx* ctx, cudaError_t e, const char* where);
-// Ensures scratch arena `slot` holds >= bytes; returns device pointer or null.
-void* scratch(skx_ctx* ctx, int slot, size_t bytes);
-void* host_scratch_dev(skx_ctx* ctx, int slot, size_t bytes);
+// Ensures scratch arena `slot` of stream s's set holds >= bytes (growing it in
+// stream order on s); returns the device pointer, or null when out of memory.
+void* scratch(skx_ctx* ctx, int slot, size_t bytes, cudaStream_t s);
+void* host_scratch_dev(skx_ctx* ctx, int slot, size_t bytes, cudaStream_t s);
+// The scratch set of stream s (created on first use).
+ScratchSet* scratch_set(skx_ctx* ctx, cudaStream_t s);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

@@ -23,6 +23,27 @@ import torch
 from . import skewdx as sx
 
 KIND_RAW, KIND_UNIFORM, KIND_LOGNORMAL = 0, 1, 2
+GAMMA = 0x9E3779B97F4A7C15  # splitmix64 increment: fill_column kind 1 keys row i by seed + i*GAMMA
+SEED = 42
+
+
+@dataclass(frozen=True)
+class Workload:
+    """One BASELINE.json config: domain D, total fact rows N, Zipf s, seed."""
+    name: str
+    d: int
+    n: int
+    z: float
+    seed: int
+
+
+# BASELINE.json configs[0..4] at their stated sizes (bench.py and the
+# BASELINE-scale parity tests build exactly these).
+C1 = Workload("C1 FK-join gather (Q1 shape)", 1 << 22, 1 << 24, 1.0, SEED + 7)
+C2 = Workload("C2 large FK-join gather", 1 << 27, 1 << 30, 1.0, SEED)
+C3 = Workload("C3 group-by COUNT+SUM", 1 << 24, 1 << 30, 1.0, SEED + 1)
+C4 = Workload("C4 index build at scale", 1 << 26, 1 << 30, 1.25, SEED + 9)
+C5 = Workload("C5 multi-column FK join with selection", 1 << 25, 1 << 31, 1.0, SEED + 12)
 
 
 def fill_column(kind: int, dtype: torch.dtype, n: int, seed: int, p0: float = 0.0,
@@ -142,15 +163,88 @@ def make_groupby_dataset(d: int, n: int, z: float, seed: int, shard: Shard | Non
     index = build_index_sharded(fact_rand, d, n, ctx)
     fact_freq = sx.recode_fact(fact_rand, index, sync=False)
     del fact_rand, index
-    # quantity uniform 1..100 (int64), keyed by the global row number
-    qty = fill_column(KIND_UNIFORM, torch.int64, shard.rows, seed * 1000003 + shard.begin, 1, 100,
+    # quantity uniform 1..100 (int64), keyed by the GLOBAL row number, so any
+    # sharding of the rows sees the same values
+    qty = fill_column(KIND_UNIFORM, torch.int64, shard.rows, qty_seed(seed, shard.begin), 1, 100,
                       device=device)
     ctx.sync()
     return GroupByDataset(d, n, shard, fact_freq, qty)
 
 
-def host_sample_rank_space(d: int, rows: int, z: float, seed: int) -> np.ndarray:
-    """CPU-side sample for the CPU baselines: Zipf draws whose ids are the
-    distribution ranks (Layout::freq up to empirical ties).  Not used on the
-    GPU path."""
-    raise NotImplementedError  # bench.py builds it with the oracle generator
+def qty_seed(seed: int, row_begin: int) -> int:
+    """fill_column kind-1 seed whose local row i is global row row_begin + i."""
+    return (seed * 1000003 + row_begin * GAMMA) & (2**64 - 1)
+
+
+@dataclass
+class C1Dataset:
+    """configs[0]: D=2^22 int32 price (uniform 1..10^6), 2^24 FKs, s=1.0."""
+    g: GatherDataset
+    price: torch.Tensor
+    price_freq: torch.Tensor
+
+
+def make_c1_dataset(shard: Shard | None = None, w: Workload = C1) -> C1Dataset:
+    shard = shard or shard_of(w.n)
+    g = make_gather_dataset(w.d, w.n, w.z, w.seed, torch.int32, shard)
+    price = fill_column(KIND_UNIFORM, torch.int32, w.d, w.seed + 1, 1, 1000000)
+    price_f = sx.permute_dimension(price, g.index, sync=False)
+    return C1Dataset(g, price, price_f)
+
+
+@dataclass
+class IndexBuildDataset:
+    """configs[3]: the original-layout FK shard and the two dimension columns
+    (int32, float32) the index build permutes."""
+    d: int
+    n: int
+    shard: Shard
+    fact: torch.Tensor
+    dim_i: torch.Tensor
+    dim_f: torch.Tensor
+
+
+def make_index_build_dataset(shard: Shard | None = None, w: Workload = C4) -> IndexBuildDataset:
+    shard = shard or shard_of(w.n)
+    fact = make_rand_fact(w.d, w.n, w.z, w.seed, shard)
+    dim_i = fill_column(KIND_RAW, torch.int32, w.d, w.seed + 1)
+    dim_f = fill_column(KIND_RAW, torch.int32, w.d, w.seed + 2).view(torch.float32)
+    return IndexBuildDataset(w.d, w.n, shard, fact, dim_i, dim_f)
+
+
+@dataclass
+class SelectDataset:
+    """configs[4]: recoded FK shard; category int32 (uniform 0..999), price
+    float32 (lognormal mu=3 sigma=1), supplier int64, flag int16 -- all in the
+    reordered (rank) layout -- and the bitmap of category < 100."""
+    d: int
+    n: int
+    shard: Shard
+    fact: torch.Tensor
+    index: sx.PermutationIndex
+    cat: torch.Tensor
+    price: torch.Tensor
+    supp: torch.Tensor
+    flag: torch.Tensor
+    bitmap: sx.Bitmap
+
+
+def make_select_dataset(shard: Shard | None = None, w: Workload = C5) -> SelectDataset:
+    shard = shard or shard_of(w.n)
+    ctx = sx.context(torch.cuda.current_device())
+    fact = make_rand_fact(w.d, w.n, w.z, w.seed, shard)
+    index = build_index_sharded(fact, w.d, w.n, ctx)
+    fact_f = sx.recode_fact(fact, index, sync=False)
+    del fact
+    cat = sx.permute_dimension(fill_column(KIND_UNIFORM, torch.int32, w.d, w.seed + 1, 0, 1000),
+                               index, sync=False)
+    price = sx.permute_dimension(fill_column(KIND_LOGNORMAL, torch.float32, w.d, w.seed + 2, 3.0,
+                                             1.0), index, sync=False)
+    supp = sx.permute_dimension(fill_column(KIND_RAW, torch.int64, w.d, w.seed + 3), index,
+                                sync=False)
+    flag = sx.permute_dimension(fill_column(KIND_RAW, torch.int16, w.d, w.seed + 4), index,
+                                sync=False)
+    bm = sx.build_bitmap_lt(cat, 100, sync=False)  # category < 100, already in rank space
+    ctx.sync()
+    return SelectDataset(w.d, w.n, shard, fact_f, index, cat, price, supp, flag, bm)
+

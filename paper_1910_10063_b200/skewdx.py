@@ -330,7 +330,7 @@ def aggregate_count(fact, domain_cardinality: int, *, hot_threshold: int = 0, ct
 
 
 def aggregate_count_sum(fact, measure, domain_cardinality: int, *, hot_threshold: int = 0,
-                        ctx=None, sync=True):
+                        ctx=None, sync=True, counts=None, sums=None):
     """COUNT and SUM(measure) per key in one pass (BASELINE config 3).
 
     measure: uint32/int32 (the reference's Column) or uint64/int64 (int64 qty).
@@ -346,8 +346,10 @@ def aggregate_count_sum(fact, measure, domain_cardinality: int, *, hot_threshold
         raise InvalidArgument("aggregate: measure must be a 32- or 64-bit integer column")
     ctx = _ctx_for(fact, ctx)
     d = int(domain_cardinality)
-    counts = torch.empty(d, dtype=torch.uint64, device=fact.device)
-    sums = torch.empty(d, dtype=torch.uint64, device=fact.device)
+    if counts is None:
+        counts = torch.empty(d, dtype=torch.uint64, device=fact.device)
+    if sums is None:
+        sums = torch.empty(d, dtype=torch.uint64, device=fact.device)
     ctx.call("skx_aggregate", _ptr(fact), _ptr(measure), mw, fact.numel(), d, int(hot_threshold),
              _ptr(counts), _ptr(sums), ctx.stream(), sync=sync)
     return counts, sums
@@ -472,26 +474,41 @@ def generate_zipf(cdf: torch.Tensor, n: int, seed: int, *, rank_to_id: torch.Ten
 
 
 def select_gather_sum(fact, bitmap: Bitmap, cat, price, supp, flag, n_categories: int, *,
-                      base: int = 0, ctx=None):
+                      base: int = 0, capacity: int | None = None, ctx=None, sync=True,
+                      out=None):
     """BASELINE config 5 fused: selected offsets, the 4 gathered columns and
-    per-category fp64 SUM(price)."""
+    per-category fp64 SUM(price).
+
+    ``capacity`` sizes the output columns (default: every row).  When more
+    rows are selected than fit, the call is repeated with exactly-sized
+    outputs, so the result is always complete.  ``out`` = (off, cat, price,
+    supp, flag, sums, count) preallocated device tensors (then ``sync=False``
+    keeps the call asynchronous and the caller reads ``count``)."""
     fact = _col(fact)
     ctx = _ctx_for(fact, ctx)
     n = fact.numel()
     dev = fact.device
-    m = max(n, 1)
-    o_off = torch.empty(m, dtype=torch.uint32, device=dev)
-    o_cat = torch.empty(m, dtype=torch.int32, device=dev)
-    o_pr = torch.empty(m, dtype=torch.float32, device=dev)
-    o_su = torch.empty(m, dtype=torch.uint64, device=dev)
-    o_fl = torch.empty(m, dtype=torch.uint16, device=dev)
-    sums = torch.empty(int(n_categories), dtype=torch.float64, device=dev)
-    cnt = torch.zeros(1, dtype=torch.uint64, device=dev)
+    if out is None:
+        m = max(int(n if capacity is None else capacity), 1)
+        out = (torch.empty(m, dtype=torch.uint32, device=dev),
+               torch.empty(m, dtype=torch.int32, device=dev),
+               torch.empty(m, dtype=torch.float32, device=dev),
+               torch.empty(m, dtype=torch.uint64, device=dev),
+               torch.empty(m, dtype=torch.uint16, device=dev),
+               torch.empty(int(n_categories), dtype=torch.float64, device=dev),
+               torch.zeros(1, dtype=torch.uint64, device=dev))
+    o_off, o_cat, o_pr, o_su, o_fl, sums, cnt = out
+    cap = o_off.numel()
     ctx.call("skx_select_gather_sum", _ptr(fact), n, _ptr(bitmap.words), bitmap.size(),
-             _ptr(cat), _ptr(price), _ptr(supp), _ptr(flag), int(base), int(n_categories),
+             _ptr(cat), _ptr(price), _ptr(supp), _ptr(flag), int(base), int(n_categories), cap,
              _ptr(o_off), _ptr(o_cat), _ptr(o_pr), _ptr(o_su), _ptr(o_fl), _ptr(sums), _ptr(cnt),
-             ctx.stream(), sync=True)
+             ctx.stream(), sync=sync)
+    if not sync:
+        return out
     c = int(cnt.item())
+    if c > cap:  # too small: once more with exactly-sized outputs
+        return select_gather_sum(fact, bitmap, cat, price, supp, flag, n_categories, base=base,
+                                 capacity=c, ctx=ctx)
     return o_off[:c], o_cat[:c], o_pr[:c], o_su[:c], o_fl[:c], sums
 
 

@@ -145,6 +145,34 @@ def test_cli_domain_default_and_violations(cli, oracle, tmp_path):
                   "--fact-out", tmp_path / "r.skdx", env=env)
     assert rc == 2 and "domain violation at row 200000" in err, err
     assert not (tmp_path / "r.skdx").exists()  # nothing written, as in the reference
+    # in place: a failed apply leaves the input column untouched, and no temporary behind
+    before = (tmp_path / "b.skdx").read_bytes()
+    rc, err = run(cli, "index", "apply", "--index", tmp_path / "i.skpi", "--fact", tmp_path / "b.skdx",
+                  "--fact-out", tmp_path / "b.skdx", env=env)
+    assert rc == 2 and "domain violation at row 200000" in err, err
+    assert (tmp_path / "b.skdx").read_bytes() == before
+    assert not [p for p in os.listdir(tmp_path) if ".tmp." in p]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("chunk", [65536, 1 << 24])
+def test_cli_apply_in_place(cli, oracle, tmp_path, chunk):
+    """--fact-out == --fact: the reference reads the whole column before it
+    writes (write_column(out, recode_fact(read_column(in)))), so the column is
+    recoded in place; the streamed apply must not truncate its own input."""
+    d, n = 9000, 400003
+    fact = _fact(oracle, d, n, 1.0, 5)
+    write_skdx(tmp_path / "f.skdx", fact)
+    env = {"SKX_STREAM_CHUNK_ROWS": str(chunk)}
+    rc, err = run(cli, "index", "build", "--fact", tmp_path / "f.skdx", "--d", d, "--out",
+                  tmp_path / "i.skpi", env=env)
+    assert rc == 0, err
+    rc, err = run(cli, "index", "apply", "--index", tmp_path / "i.skpi", "--fact", tmp_path / "f.skdx",
+                  "--fact-out", tmp_path / "f.skdx", env=env)
+    assert rc == 0, err
+    _, rk = oracle.build_index(oracle.count_frequencies(fact, d), n)
+    assert np.array_equal(read_skdx(tmp_path / "f.skdx"), oracle.recode_fact(fact, rk))
+    assert not [p for p in os.listdir(tmp_path) if ".tmp." in p]
 
 
 @pytest.mark.gpu

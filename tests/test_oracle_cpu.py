@@ -141,3 +141,70 @@ def test_counter_generator_is_zipf(oracle):
     # position-addressable: a shard equals the slice of the whole
     part = oracle.generate_zipf_counter(cdf, None, 42, 777, 1000)
     assert np.array_equal(part, ranks[777:1777])
+
+
+# ---- the multi-threaded checker forms (skx_oracle_mt.c) used at BASELINE scale
+# are pinned against the single-threaded restatement (and through it the KATs
+# and reference fixtures above) on seeded inputs, including ragged spans,
+# ties, zero counts and domain violations.
+def test_mt_forms_equal_single_thread(oracle, kat, ref_cases):
+    rng = np.random.default_rng(2024)
+    for d, n, z in [(1, 17, 1.0), (97, 10007, 1.3), (5000, 300001, 1.0), (70000, 200003, 0.6)]:
+        cdf = oracle.zipf_cdf(d, z)
+        fact = oracle.generate_zipf_counter(cdf, oracle.random_bijection(d, 3), 3, 0, n)
+        c1 = oracle.count_frequencies(fact, d)
+        assert np.array_equal(oracle.count_frequencies_mt(fact, d), c1)
+        off, rk = oracle.build_index(c1, n)
+        off2, rk2 = oracle.build_index_radix(c1, n)
+        assert np.array_equal(off, off2) and np.array_equal(rk, rk2)
+        for dt in (np.uint16, np.uint32, np.uint64):
+            dim = rng.integers(0, np.iinfo(dt).max, size=d, dtype=dt)
+            assert np.array_equal(oracle.gather_mt(fact, dim), oracle.gather(fact, dim))
+        meas = rng.integers(1, 101, size=n, dtype=np.uint64)
+        ce, se = oracle.aggregate_count_sum(fact, meas, d)
+        cm, sm = oracle.aggregate_count_sum_mt(fact, meas, d)
+        assert np.array_equal(ce, cm) and np.array_equal(se, sm)
+        cat = rng.integers(0, 1000, size=d, dtype=np.int32)
+        price = np.exp(3 + rng.standard_normal(d)).astype(np.float32)
+        supp = rng.integers(0, 2**63, size=d, dtype=np.uint64)
+        flag = rng.integers(0, 2**16, size=d, dtype=np.uint16)
+        words = oracle.build_bitmap_lt_i32(cat, 100)
+        assert np.array_equal(words, words_from_bits(np.nonzero(cat < 100)[0], d))
+        exp = oracle.select_gather_sum(fact, words, cat, price, supp, flag, 1000, base=11)
+        got = oracle.select_gather_sum_mt(fact, words, cat, price, supp, flag, 1000, base=11)
+        for g, e in zip(got[:5], exp[:5]):
+            assert np.array_equal(g, e)
+        assert np.allclose(got[5], exp[5], rtol=1e-12, atol=0)
+    # radix build_index on tie-heavy profiles and the reference KATs
+    for c in kat["build_index"]:
+        o, r = oracle.build_index_radix(np.array(c["counts"], np.uint64), c["total"])
+        assert o.tolist() == c["offsets"] and r.tolist() == c["ranks"]
+    for c in kat["build_index_invalid"]:
+        with pytest.raises(OracleError):
+            oracle.build_index_radix(np.array(c["counts"], np.uint64), c["total"])
+    for _ in range(5):
+        cnt = rng.integers(0, 4, size=20000).astype(np.uint64) * rng.integers(0, 2, size=20000).astype(np.uint64)
+        cnt[rng.integers(0, 20000, 50)] = rng.integers(1, 1 << 20, 50).astype(np.uint64)
+        a = oracle.build_index(cnt)
+        b = oracle.build_index_radix(cnt)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    for i in range(len(ref_cases)):
+        c = ref_cases.case(i)
+        assert np.array_equal(oracle.count_frequencies_mt(c["fact"], c["d"]), c["counts"])
+        o, r = oracle.build_index_radix(c["counts"])
+        assert np.array_equal(o, c["offsets"]) and np.array_equal(r, c["ranks"])
+    # domain violations: the first offending row overall, whichever chunk it is in
+    fact = np.full(100003, 3, np.uint32)
+    fact[77777], fact[90000] = 0, 99
+    assert oracle.find_domain_violation_mt(fact, 10) == 77777
+    for fn in (lambda: oracle.count_frequencies_mt(fact, 10),
+               lambda: oracle.gather_mt(fact, np.arange(10, dtype=np.uint32)),
+               lambda: oracle.aggregate_count_sum_mt(fact, None, 10)):
+        with pytest.raises(OracleError) as e:
+            fn()
+        assert (e.value.status, e.value.row, e.value.value) == (DOMAIN, 77777, 0)
+    # value-column fixtures: kind 0 = the reference bench's dim column formula
+    v = oracle.fill_column(0, np.uint64, 1000, 42)
+    assert all(int(v[i]) == oracle.splitmix64(42 ^ (0xd1000000 + i)) for i in range(0, 1000, 97))
+    q = oracle.fill_column(1, np.int64, 100000, 7, 1, 100)
+    assert q.min() == 1 and q.max() == 100

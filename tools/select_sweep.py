@@ -50,7 +50,7 @@ res = {}
 for name, (f, c_, p_, s_, fl_, b_) in layouts.items():
     def step():
         ctx.call("skx_select_gather_sum", P(f), n, P(b_.words), d, P(c_), P(p_), P(s_), P(fl_), 0,
-                 1000, P(o_off), P(o_cat), P(o_pr), P(o_su), P(o_fl), P(sums), P(cnt), ctx.stream(),
+                 1000, cap, P(o_off), P(o_cat), P(o_pr), P(o_su), P(o_fl), P(sums), P(cnt), ctx.stream(),
                  sync=False)
     for _ in range(3):
         step()
