@@ -7,10 +7,16 @@ drawn Zipf(s) over ranks with ranks scattered to ids by a seeded random
 bijection, the skew-aware index built on the GPU (histogram -> sort-by-count
 -> recode -> permute), and the timed step is one gather
 ``out[k] = dim_freq[fact_freq[k]-1]`` over every fact row of the (reordered)
-layout -- one ``skx_gather_u64`` launch.  Scaling is weak: every GPU owns a
-2^30-row shard of the fact table (rows partitioned, no data-path collective
-for the gather) and the dimension columns are replicated; the index build
-all-reduces the per-GPU histograms.
+layout -- one ``skx_gather_u64`` launch per GPU.
+
+On N GPUs (torchrun, one process per GPU) the BASELINE totals stay fixed
+(strong scaling, the default: 2^30 rows for C2/C3/C4, 2^31 for C5) and each
+rank owns the ``chunk_spans(N_total, N)`` shard of the fact rows
+(parallel.cpp:31-43); dimension columns are replicated.  Every config runs
+through ``paper_1910_10063_b200.dist`` (the multi-GPU orchestration the tests
+cover) on libskx's NCCL communicator; per-phase times (kernels vs
+collectives, max over ranks) are in the line.  ``--scaling weak`` keeps the
+per-GPU rows fixed instead.
 
 Prints ONE JSON line (rank 0).  ``--impl reference`` times the reference's
 CPU path on the host instead.
@@ -45,9 +51,14 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--z", type=float, default=1.0, help="Zipf exponent (C2 sweeps 0.5/1.0/1.5)")
-    p.add_argument("--rows", type=int, default=N_C2, help="fact rows per GPU")
+    p.add_argument("--rows", type=int, default=N_C2,
+                   help="C2 fact rows: the total (strong scaling) or per GPU (weak)")
     p.add_argument("--domain", type=int, default=D_C2)
-    p.add_argument("--no-extras", action="store_true", help="skip rand-layout / group-by lines")
+    p.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                   help="strong: BASELINE totals sharded over the GPUs; weak: totals x N")
+    p.add_argument("--configs", default="",
+                   help="comma list of extra configs to run (c1,c2,c3,c4,c5); default all")
+    p.add_argument("--no-extras", action="store_true", help="headline C2 gather only")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--policy", type=int, default=129,
@@ -240,29 +251,43 @@ def cpu_heavy_hitters_reference(fact_np, d, k=8192):
             "kind": "reference", "sample": f"{len(f)} rows, k={k}, D={d}"}
 
 
-def cpu_rebuild_reference(fact_np, d):
-    """C4 on the host: the reference's rebuild (count_frequencies + build_index,
-    single thread -- the reference has no parallel index build) at the
-    CPU-runnable scale of BASELINE configs[0] (D=2^22, 2^24 rows)."""
+def cpu_index_build_reference(fact_np, d, dim_i, dim_f):
+    """C4 on the host at the SAME domain (D=2^26): the reference's rebuild
+    (count_frequencies + build_index, single thread -- the reference has no
+    parallel index build; the sort over all D ids dominates), recode_fact of a
+    2^24-row fraction of the same FK column, and permute_dimension of the
+    int32 and float32 dimensions, through its public API, once."""
     import ctypes as C
 
     import numpy as np
     from oracle.oracle import Reference
     ref = Reference()
     f = np.ascontiguousarray(fact_np)
-    ns = ref.L.ref_time_rebuild(f.ctypes.data_as(C.c_void_p), len(f), d, 1)
-    return {"rebuild_1thread_ms": ns * 1e-6, "rows_per_s": len(f) / (ns * 1e-9), "kind": "reference",
-            "sample": f"{len(f)} Zipf(1.25) rows over D={d} (configs[0] scale)"}
+    di = np.ascontiguousarray(dim_i)
+    df = np.ascontiguousarray(dim_f)
+    ns = np.zeros(3, np.float64)
+    st = ref.L.ref_time_index_build(f.ctypes.data_as(C.c_void_p), len(f), d,
+                                    di.ctypes.data_as(C.c_void_p), df.ctypes.data_as(C.c_void_p),
+                                    ns.ctypes.data_as(C.c_void_p))
+    if st:
+        raise RuntimeError(f"ref_time_index_build status {st}")
+    return {"rebuild_1thread_ms": ns[0] * 1e-6, "recode_1thread_ms": ns[1] * 1e-6,
+            "permute_2dims_1thread_ms": ns[2] * 1e-6, "total_ms": ns.sum() * 1e-6,
+            "kind": "reference", "threads": 1,
+            "sample": (f"D={d} (same domain as the GPU run), {len(f)} of the FK rows (1/64 of "
+                       "configs[3]'s 2^30; the D-id sort dominates), int32 + float32 dims")}
 
 
-def cpu_select_reference(fact_np, words_np, bits):
-    """C5 selection on the host: the reference's parallel_select
-    (parallel.cpp:102-129, all threads) with the same permuted bitmap on a
-    2^26-row sample of the recoded FK column."""
+def cpu_select_reference(fact_np, words_np, bits, cols=None):
+    """C5 on the host: the reference's parallel_select (parallel.cpp:102-129,
+    all threads) with the same permuted bitmap on a 2^26-row sample of the
+    recoded FK column, and beside it the full config-5 step (select + the four
+    column gathers + fp64 SUM(price) per category) through the multi-threaded
+    restatement (the reference has no multi-column gather or float SUM)."""
     import ctypes as C
 
     import numpy as np
-    from oracle.oracle import Reference
+    from oracle.oracle import Oracle, Reference
     ref = Reference()
     threads = os.cpu_count() or 1
     f = np.ascontiguousarray(fact_np)
@@ -271,9 +296,24 @@ def cpu_select_reference(fact_np, words_np, bits):
     ns = ref.L.ref_time_parallel_select(f.ctypes.data_as(C.c_void_p), len(f),
                                         w.ctypes.data_as(C.c_void_p), bits, threads, 3,
                                         C.byref(sel))
-    return {"parallel_select_rows_per_s": len(f) / (ns * 1e-9), "threads": threads,
-            "selected": int(sel.value), "kind": "reference",
-            "sample": f"{len(f)} rows of the recoded C5 FK column, permuted bitmap over D={bits}"}
+    res = {"parallel_select_rows_per_s": len(f) / (ns * 1e-9), "threads": threads,
+           "selected": int(sel.value), "kind": "reference",
+           "sample": f"{len(f)} rows of the recoded C5 FK column, permuted bitmap over D={bits}"}
+    if cols is not None:
+        orc = Oracle()
+        cat, price, supp, flag = cols
+        args = (f, w, cat, price.view(np.float32), supp.view(np.uint64), flag.view(np.uint16), 1000)
+        orc.select_gather_sum_mt(*args, capacity=len(f) // 5)
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            orc.select_gather_sum_mt(*args, capacity=len(f) // 5)
+            ts.append(time.perf_counter() - t0)
+        res["select_gather_sum_port_rows_per_s"] = len(f) / statistics.median(ts)
+        res["port_note"] = ("select + gather of the 4 columns + fp64 SUM(price) per category, "
+                            f"{threads} threads (oracle/skx_oracle_mt.c, parallel_select's "
+                            "chunking)")
+    return res
 
 
 def run_reference_arm(args):
@@ -315,12 +355,12 @@ def run_reference_arm(args):
         "impl": "reference", "metric": METRIC, "metric_note": METRIC_NOTE,
         "value": value, "unit": "rows/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": "C2 large FK-join gather (BASELINE configs[1])", "domain": d,
                    "rows_per_step_sampled": rows, "z": args.z, "value": "int64",
                    "layout": "freq (skew-reordered)", "seed": SEED},
         "cpu_baseline": {"value": value, "unit": "rows/s", "cores": threads, "kind": kind,
-                         "sample": sample},
+                         "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     line.update(extra)
@@ -330,182 +370,227 @@ def run_reference_arm(args):
 # ---------------------------------------------------------------------------
 # GPU side
 # ---------------------------------------------------------------------------
-def timed_launches(fn, steps, warmup, stream, dist_on, ctx=None):
-    """W warm-ups; then K steps bracketed by barrier + synchronize, one CUDA
-    event per step on the launching stream.  Returns (total_ms, [per-step ms],
-    libskx kernel launches inside the timed region)."""
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def max_over_ranks(x, coll):
+    """Max of a host float over ranks (torch.distributed plumbing)."""
     import torch
     import torch.distributed as dist
-    for _ in range(warmup):
-        fn()
-    torch.cuda.synchronize()
-    if dist_on:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
-    l0 = ctx.launches() if ctx is not None else 0
-    ev[0].record(stream)
-    for i in range(steps):
-        fn()
-        ev[i + 1].record(stream)
-    launches = (ctx.launches() - l0) if ctx is not None else 0
-    torch.cuda.synchronize()
-    if dist_on:
-        dist.barrier()
-    per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
-    return ev[0].elapsed_time(ev[steps]), per, launches
-
-
-def reduce_to_root(t):
-    """NCCL reduce to rank 0 (the BASELINE combine step).  The gloo backend,
-    used only for the single-GPU multi-rank dry run (SKX_BENCH_DIST_BACKEND),
-    all-reduces instead."""
-    import torch.distributed as dist
-    if dist.get_backend() == "nccl":
-        dist.reduce(t, dst=0)
-    else:
-        dist.all_reduce(t)
-
-
-def max_over_ranks(x, dist_on):
-    import torch
-    import torch.distributed as dist
-    if not dist_on:
+    if coll.world == 1:
         return x
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def max_phases(ph, coll):
+    """Per-phase ms, each the max over ranks."""
+    keys = sorted(ph)
+    return {k: round(max_over_ranks(ph[k], coll), 4) for k in keys}
+
+
+def timed(fn, steps, warmup, coll, ctx=None, phases=False):
+    """W warm-ups; then K steps bracketed by barrier + synchronize, one CUDA
+    event per step on the launching stream (and per phase when `phases`).
+    Returns (total_ms, [per-step ms], libskx launches in the timed region,
+    {phase: mean ms})."""
+    import torch
+
+    from paper_1910_10063_b200 import dist as sdist
+    for _ in range(warmup):
+        fn(None)
+    torch.cuda.synchronize()
+    coll.barrier()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    timers = []
+    l0 = ctx.launches() if ctx is not None else 0
+    ev[0].record()
+    for i in range(steps):
+        t = sdist.PhaseTimer() if phases else None
+        fn(t)
+        if t is not None:
+            timers.append(t)
+        ev[i + 1].record()
+    launches = (ctx.launches() - l0) if ctx is not None else 0
+    torch.cuda.synchronize()
+    coll.barrier()
+    per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+    ph = {}
+    for t in timers:
+        for k, v in t.phases_ms().items():
+            ph[k] = ph.get(k, 0.0) + v / len(timers)
+    return ev[0].elapsed_time(ev[steps]), per, launches, ph
+
+
+def roofline(alg_bytes, launch_ms, peak):
+    a = alg_bytes / (launch_ms * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": a, "peak": peak, "unit": "GB/s", "frac": a / peak,
+            "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": launch_ms}
+
+
+class Env:
+    """Per-process bench environment: rank, device, collectives, executor."""
+
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
+
+        from paper_1910_10063_b200 import dist as sdist
+        from paper_1910_10063_b200 import skewdx as sx
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        # SKX_BENCH_ONE_GPU=1 + SKX_BENCH_DIST_BACKEND=gloo: every rank on cuda:0 with
+        # host-side collectives -- a logic dry run of the multi-rank path on a one-GPU box
+        # (no kernel waits on another rank's kernel).  Its timings are not scaling numbers.
+        if os.environ.get("SKX_BENCH_ONE_GPU") == "1":
+            local = 0
+        self.local = local
+        torch.cuda.set_device(local)
+        if self.world > 1:
+            backend = os.environ.get("SKX_BENCH_DIST_BACKEND", "nccl")
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            else:
+                dist.init_process_group(backend)
+        # libskx's own NCCL communicator on NCCL process groups, torch.distributed (gloo) in the
+        # dry run, no-ops on one GPU
+        self.coll = sdist.default_collectives(local)
+        self.ctx = sx.context(local)
+        self.ctx.set_gather_policy(args.policy)
+        self.ex = sdist.GpuExecutor(self.ctx)
+        self.strong = args.scaling == "strong"
+        self.peak, self.peak_kind = load_peaks()
+        self.stream = torch.cuda.current_stream()
+
+    def shard(self, n_total):
+        from paper_1910_10063_b200 import dist as sdist
+        return sdist.shard_for(n_total, self.rank, self.world)
+
+    def total(self, n):
+        """BASELINE's total rows (strong scaling) or n per GPU (weak)."""
+        return n if self.strong else n * self.world
+
+    def close(self):
+        import torch.distributed as dist
+        if hasattr(self.coll, "close"):
+            self.coll.close()
+        if self.world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
 
 
 def run_ours(args):
     import numpy as np
     import torch
-    import torch.distributed as dist
 
-    from paper_1910_10063_b200 import dataset as ds_mod
+    from paper_1910_10063_b200 import dataset as ds
+    from paper_1910_10063_b200 import dist as sdist
     from paper_1910_10063_b200 import skewdx as sx
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    # SKX_BENCH_ONE_GPU=1 + SKX_BENCH_DIST_BACKEND=gloo: every rank on cuda:0, host-side
-    # collectives -- a logic dry run of the multi-rank path on a one-GPU box (no kernel
-    # waits on another rank's kernel).  Timings from it are not scaling numbers.
-    if os.environ.get("SKX_BENCH_ONE_GPU") == "1":
-        local = 0
-    torch.cuda.set_device(local)
-    dist_on = world > 1
-    if dist_on:
-        backend = os.environ.get("SKX_BENCH_DIST_BACKEND", "nccl")
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
-    ctx = sx.context(local)
-    ctx.set_gather_policy(args.policy)
-    peak, peak_kind = load_peaks()
-
+    E = Env(args)
+    coll, ex, ctx, peak = E.coll, E.ex, E.ctx, E.peak
+    only = set(args.configs.split(",")) if args.configs else None
+    want = (lambda c: only is None or c in only)
     d = args.domain
-    rows_local = args.rows  # weak scaling: fixed rows per GPU
-    n_total = rows_local * world
-    shard = ds_mod.Shard(rank, world, rank * rows_local, (rank + 1) * rows_local)
+    n_total = E.total(args.rows)
+    shard = E.shard(n_total)
+    rows_local = shard.rows
     t0 = time.perf_counter()
-    data = ds_mod.make_gather_dataset(d, n_total, args.z, SEED, torch.int64, shard)
+    data = ds.make_gather_dataset(d, n_total, args.z, ds.SEED, torch.int64, shard)
     setup_s = time.perf_counter() - t0
-    stream = torch.cuda.current_stream()
     out = torch.empty(rows_local, dtype=torch.int64, device="cuda")
 
-    def step_freq():
-        sx.materialize(data.fact_freq, data.dim_freq, out=out, ctx=ctx, sync=False)
+    def step_freq(_t):
+        sdist.gather(data.fact_freq, data.dim_freq, ex, out)
 
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(E.local)
     sampler.start()
-    total_ms, per, launches = timed_launches(step_freq, args.steps, args.warmup, stream, dist_on,
-                                             ctx)
+    total_ms, per, launches, _ = timed(step_freq, args.steps, args.warmup, coll, ctx)
     clocks = sampler.stop()
     ctx.sync()  # raises on a deferred domain violation
-    total_ms = max_over_ranks(total_ms, dist_on)
+    total_ms = max_over_ranks(total_ms, coll)
     value = n_total * args.steps / (total_ms * 1e-3)
     alg_bytes = rows_local * (4 + 8)  # FK read + int64 output write per row
-    avg_launch_s = statistics.mean(per) * 1e-3
-    achieved = alg_bytes / avg_launch_s / 1e9
+    rf = roofline(alg_bytes, statistics.mean(per), peak)
     out_freq = out.clone()
 
     extras = {}
-    if not args.no_extras:
+    if not args.no_extras and want("c2"):
         # original (rand) layout through the same kernel, same timing rules
         outr = torch.empty_like(out)
-
-        def step_rand():
-            sx.materialize(data.fact_rand, data.dim_rand, out=outr, ctx=ctx, sync=False)
-        tr, per_r, _ = timed_launches(step_rand, args.steps, args.warmup, stream, dist_on)
-        tr = max_over_ranks(tr, dist_on)
-        # CorrectnessError gate of bench.cpp:300-304: both layouts, same result
-        same = bool(torch.equal(outr, out_freq))
+        tr, per_r, _, _ = timed(lambda _t: sdist.gather(data.fact_rand, data.dim_rand, ex, outr),
+                                args.steps, args.warmup, coll)
+        tr = max_over_ranks(tr, coll)
+        same = bool(torch.equal(outr, out_freq))  # CorrectnessError gate, bench.cpp:300-304
         extras["rand_layout"] = {
             "value": n_total * args.steps / (tr * 1e-3), "unit": "rows/s",
-            "roofline_frac": alg_bytes / (statistics.mean(per_r) * 1e-3) / 1e9 / peak,
-            "freq_over_rand": (n_total * args.steps / (total_ms * 1e-3)) / (n_total * args.steps / (tr * 1e-3)),
-            "outputs_equal": same}
+            "roofline_frac": roofline(alg_bytes, statistics.mean(per_r), peak)["frac"],
+            "freq_over_rand": tr / total_ms, "outputs_equal": same}
         if not same:
             raise SystemExit("CorrectnessError: rand and freq layouts disagree")
         del outr
-        # Index build on this workload, warm (scratch already allocated):
-        # per-GPU u32 histogram -> NCCL all-reduce -> sort -> recode -> permute.
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
-        hist_counts = torch.empty(d, dtype=torch.uint32, device="cuda")
+        # Index build on this workload, warm: per-GPU u32 histogram -> all-reduce -> sort ->
+        # recode of the local shard -> permute of the int64 dim (dist.rebuild, the
+        # multi-GPU orchestration every rank runs)
+        hist = torch.empty(d, dtype=torch.uint32, device="cuda")
         fact_tmp = torch.empty_like(data.fact_rand)
-        ib = []
-        for rep in range(3):
-            if dist_on:
-                dist.barrier()
-            ev[0].record()
-            sx.histogram_u32(data.fact_rand, d, hist_counts, ctx=ctx, sync=False)
-            ev[1].record()
-            ds_mod._allreduce_u32(hist_counts)
-            idx2 = sx.build_index(sx.FrequencyProfile(hist_counts, n_total), ctx=ctx, sync=False)
-            ev[2].record()
-            sx.recode_fact(data.fact_rand, idx2, out=fact_tmp, ctx=ctx, sync=False)
-            ev[3].record()
-            sx.permute_dimension(data.dim_rand, idx2, ctx=ctx, sync=False)
-            ev[4].record()
-            torch.cuda.synchronize()
-            ib.append([ev[i].elapsed_time(ev[i + 1]) for i in range(4)])
+        box = {}
+
+        def ib_step(t):
+            idx, _ = sdist.rebuild(data.fact_rand, d, n_total, ex, coll, shard, hist, t,
+                                   check=False)
+            ex.recode(data.fact_rand, idx, fact_tmp)
+            if t is not None:
+                t.mark("recode")
+            ex.permute(data.dim_rand, idx)
+            if t is not None:
+                t.mark("permute")
+            box["idx"] = idx
+        tib, _, _, ph = timed(ib_step, 3, 1, coll, phases=True)
         ctx.sync()
-        same_idx = bool(torch.equal(idx2.offsets, data.index.offsets)) and bool(
+        same_idx = bool(torch.equal(box["idx"].offsets, data.index.offsets)) and bool(
             torch.equal(fact_tmp, data.fact_freq))
-        best = min(ib, key=sum)
         extras["index_build"] = {
-            "histogram_ms": round(best[0], 3), "allreduce_sort_ms": round(best[1], 3),
-            "recode_ms": round(best[2], 3), "permute_ms": round(best[3], 3),
-            "total_ms": round(sum(best), 3), "deterministic": same_idx,
-            "note": ("per-GPU u32 histogram, NCCL all-reduce (N>1), sort-by-count of D=%d, "
-                     "recode of the local shard, permute of the int64 dim; warm, best of 3, "
+            "ms": round(max_over_ranks(tib / 3, coll), 3), "phases_ms": max_phases(ph, coll),
+            "deterministic": same_idx,
+            "note": ("dist.rebuild (per-GPU u32 histogram, all-reduce, sort-by-count of D=%d) + "
+                     "recode of the local shard + permute of the int64 dim; warm, mean of 3, "
                      "CUDA events" % d)}
-        # Cache model (csrc/cachemodel.cu, SURVEY §8f row 2) on the empirical profile: predicted
-        # dimension line misses of this gather vs the ncu-measured DRAM traffic.
+
         def model():
-            vf = hist_counts.view(torch.int32).long()[idx2.offsets.view(torch.int32).long() - 1]
+            vf = hist.view(torch.int32).long()[box["idx"].offsets.view(torch.int32).long() - 1]
             vf = vf.double() / float(n_total)  # rank order
             geom = sx.CacheGeometry(1, 128, 8)
             eff = 64 << 20  # random-read capacity of the L2 (profiles/r1_experiments.md §10)
             res = {"geometry": "128 B lines of int64, L2 random-read capacity 64 MiB"}
             for name, lay in (("freq", sx.Layout.freq), ("rand", sx.Layout.rand)):
-                lf = sx.line_frequencies(vf, lay, geom, SEED)
+                lf = sx.line_frequencies(vf, lay, geom, ds.SEED)
                 h = sx.estimate_hit_rate(lf, eff // 128)
                 res[name] = {"pred_l2_hit": h, "pred_line_misses": (1.0 - h) * rows_local}
-            tr = ncu_traffic("gather_c2")
-            if tr:
-                res["freq"]["ncu_line_misses"] = (tr - rows_local * 12) / 128.0
+            tr_ = ncu_traffic("gather_c2")
+            if tr_:
+                res["freq"]["ncu_line_misses"] = (tr_ - rows_local * 12) / 128.0
             trr = ncu_traffic("gather_c2_rand")
             if trr:
                 res["rand"]["ncu_line_misses"] = (trr - rows_local * 12) / 128.0
             return res
-        if rank == 0:
+        if E.rank == 0:
             extras["cache_model"] = _cpu_extra(model)
-        del hist_counts, fact_tmp, idx2
+        del hist, fact_tmp, box
 
-    # e2e through the C-ABI host-buffer entry (pinned host fact+dim in, out back)
+    # e2e through the C-ABI host-buffer entry (pinned host fact+dim in, out back), K steps
     e2e = None
     if not args.no_e2e:
         import ctypes as C
@@ -519,122 +604,78 @@ def run_ours(args):
                                                C.c_void_p(d_h.data_ptr()), d,
                                                C.c_void_p(o_h.data_ptr())))
         e2e_step()
-        e_steps = max(1, min(args.steps, 3))
-        if dist_on:
-            dist.barrier()
+        coll.barrier()
         t0 = time.perf_counter()
-        for _ in range(e_steps):
+        for _ in range(args.steps):
             e2e_step()
-        te = max_over_ranks(time.perf_counter() - t0, dist_on)
-        if not torch.equal(o_h[:1 << 20].cuda(), out_freq[:1 << 20]):
+        te = max_over_ranks(time.perf_counter() - t0, coll)
+        if not torch.equal(o_h.cuda(), out_freq):
             raise SystemExit("CorrectnessError: host-buffer path disagrees with device path")
-        e2e = {"value": n_total * e_steps / te, "unit": "rows/s",
+        e2e = {"value": n_total * args.steps / te, "unit": "rows/s",
                "h2d_bytes_per_step": rows_local * 4 + d * 8, "d2h_bytes_per_step": rows_local * 8,
+               "steps": args.steps,
                "path": "skx_materialize_host (pinned host fact+dim -> device -> pinned host out, "
                        "chunked 2-stream pipeline)"}
         del f_h, d_h, o_h
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if E.rank == 0 and E.world == 1 and not args.no_cpu:
         m = min(CPU_SAMPLE_ROWS, rows_local)
         cpu = cpu_gather_baseline(data.fact_freq[:m].cpu().numpy(),
                                   data.dim_freq.cpu().numpy().view(np.uint64))
+        cpu["cpu_model"] = cpu_model()
 
-    if not args.no_extras:
-        # The rest of the BASELINE C2 sweep (s = 0.5 and 1.5; s = 1.0 is the headline),
-        # both layouts, same kernel and timing rules.
+    if not args.no_extras and want("c2"):
+        # the rest of the BASELINE C2 sweep (s = 0.5 and 1.5; s = 1.0 is the headline),
+        # both layouts, same kernel and timing rules
         sweep = {}
+        ks = max(3, min(args.steps, 10))
         for zz in (0.5, 1.5):
-            g = ds_mod.make_gather_dataset(d, n_total, zz, SEED, torch.int64, shard)
+            g = ds.make_gather_dataset(d, n_total, zz, ds.SEED, torch.int64, shard)
             for lay, f, dm in (("freq", g.fact_freq, g.dim_freq), ("rand", g.fact_rand, g.dim_rand)):
-                ts, per_s, _ = timed_launches(
-                    lambda f=f, dm=dm: sx.materialize(f, dm, out=out, ctx=ctx, sync=False),
-                    max(3, min(args.steps, 10)), args.warmup, stream, dist_on)
-                ts = max_over_ranks(ts, dist_on)
-                ms = ts / max(3, min(args.steps, 10))
-                sweep[f"s{zz}_{lay}"] = {"ms_per_step": ms,
-                                         "value": n_total / (ms * 1e-3), "unit": "rows/s",
-                                         "roofline_frac": alg_bytes / (statistics.mean(per_s) * 1e-3)
-                                         / 1e9 / peak}
+                ts, per_s, _, _ = timed(lambda _t, f=f, dm=dm: sdist.gather(f, dm, ex, out), ks,
+                                        args.warmup, coll)
+                ms = max_over_ranks(ts, coll) / ks
+                sweep[f"s{zz}_{lay}"] = {"ms_per_step": ms, "value": n_total / (ms * 1e-3),
+                                         "unit": "rows/s",
+                                         "roofline_frac": roofline(alg_bytes, statistics.mean(per_s),
+                                                                   peak)["frac"]}
             del g
             torch.cuda.empty_cache()
         extras["c2_s_sweep"] = sweep
 
-    groupby = None
+    del data, out, out_freq
+    torch.cuda.empty_cache()
     if not args.no_extras:
-        del data, out, out_freq
-        torch.cuda.empty_cache()
-        gdat = ds_mod.make_groupby_dataset(D_C3, rows_local * world, 1.0, SEED + 1,
-                                           ds_mod.Shard(rank, world, rank * rows_local,
-                                                        (rank + 1) * rows_local))
-        counts = torch.empty(D_C3, dtype=torch.uint64, device="cuda")
-        sums = torch.empty(D_C3, dtype=torch.uint64, device="cuda")
+        if want("c3"):
+            extras["groupby_c3"] = bench_c3(args, E)
+        if want("c1"):
+            extras["gather_c1"] = bench_c1(args, E)
+        if want("c4"):
+            extras["index_build_c4"] = bench_c4(args, E)
+        if want("c5"):
+            extras["select_c5"] = bench_c5(args, E)
 
-        def step_gb():
-            ctx.call("skx_aggregate", C_ptr(gdat.fact_freq), C_ptr(gdat.qty), 8, rows_local, D_C3, 0,
-                     C_ptr(counts), C_ptr(sums), ctx.stream(), sync=False)
-            if dist_on:  # per-GPU partials combined with NCCL reduce (BASELINE config 3)
-                reduce_to_root(counts.view(torch.int64))
-                reduce_to_root(sums.view(torch.int64))
-        tg, per_g, _ = timed_launches(step_gb, args.steps, args.warmup, stream, dist_on)
-        ctx.sync()
-        tg = max_over_ranks(tg, dist_on)
-        gb_bytes = rows_local * 12 + D_C3 * 16
-        groupby = {"workload": "C3 group-by COUNT+SUM(int64 qty), D=2^24, s=1.0, reordered",
-                   "value": rows_local * world * args.steps / (tg * 1e-3), "unit": "rows/s",
-                   "ms_per_step": tg / args.steps,
-                   "roofline": {"bound": "hbm", "achieved": gb_bytes / (statistics.mean(per_g) * 1e-3) / 1e9,
-                                "peak": peak, "unit": "GB/s",
-                                "frac": gb_bytes / (statistics.mean(per_g) * 1e-3) / 1e9 / peak,
-                                "traffic": ncu_traffic("groupby_c3"),
-                                "alg_bytes_per_step": gb_bytes}}
-        # Q3a heavy hitters: counts of the k = 8192 hottest ids of
-        # the recoded C3 column -- the device part of heavy_hitter_count
-        # (operators.cpp:184-203); the top-k ordering of k pairs is host work.
-        hh = torch.empty(8192, dtype=torch.uint64, device="cuda")
-
-        def step_hh():
-            ctx.call("skx_heavy_hitter_count", C_ptr(gdat.fact_freq), rows_local, D_C3, 8192,
-                     C_ptr(hh), ctx.stream(), sync=False)
-            if dist_on:
-                reduce_to_root(hh.view(torch.int64))
-        th, per_h, _ = timed_launches(step_hh, args.steps, args.warmup, stream, dist_on)
-        ctx.sync()
-        th = max_over_ranks(th, dist_on)
-        hb = rows_local * 4 + 8192 * 8
-        groupby["heavy_hitters_k8192"] = {
-            "value": rows_local * world * args.steps / (th * 1e-3), "unit": "rows/s",
-            "ms_per_step": th / args.steps,
-            "roofline_frac": hb / (statistics.mean(per_h) * 1e-3) / 1e9 / peak}
-        del hh
-        if rank == 0 and world == 1 and not args.no_cpu:
-            groupby["cpu_reference"] = _cpu_extra(lambda: cpu_groupby_reference(
-                gdat.fact_freq[:1 << 26].cpu().numpy(), gdat.qty[:1 << 24].cpu().numpy(), D_C3))
-        del gdat, counts, sums
-        torch.cuda.empty_cache()
-        extras.update(other_configs(args, ctx, stream, dist_on, rank, world, peak))
-
-    if rank == 0:
+    if E.rank == 0:
+        rf.update({"peak_kind": E.peak_kind, "frac_vs_nominal_8000": rf["achieved"] / 8000.0,
+                   "traffic": ncu_traffic("gather_c2"),
+                   # DRAM bytes actually moved per launch (ncu) over the live launch time
+                   "traffic_GBps": (ncu_traffic("gather_c2") or 0) / statistics.mean(per) / 1e6})
         line = {
             "metric": METRIC, "metric_note": METRIC_NOTE,
-            "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
+            "value": value, "unit": "rows/s", "n_gpus": E.world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "scaling": "strong" if E.strong else "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic",
             "config": {"workload": "C2 large FK-join gather (BASELINE configs[1])", "domain": d,
-                       "rows_per_gpu": rows_local, "rows_total": n_total, "z": args.z,
-                       "value": "int64", "layout": "freq (skew-reordered)", "seed": SEED,
-                       "parallelism": f"dp{world} (fact rows sharded, dimension replicated)",
-                       "l2": "inputs larger than L2 (4 GiB FK + 8 GiB output + 1 GiB dim per step)",
+                       "rows_total": n_total, "rows_per_gpu": rows_local, "z": args.z,
+                       "value": "int64", "layout": "freq (skew-reordered)", "seed": ds.SEED,
+                       "parallelism": f"dp{E.world} (fact rows sharded by chunk_spans, "
+                                      "dimension replicated)",
+                       "l2": "inputs larger than L2 (4 GiB FK + 8 GiB output + 1 GiB dim per step "
+                             "at N=1)",
                        "gather_policy": args.policy},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "peak_kind": peak_kind,
-                         "frac_vs_nominal_8000": achieved / 8000.0,
-                         "traffic": ncu_traffic("gather_c2"),
-                         # DRAM bytes actually moved per launch (ncu) over the live launch time:
-                         # how close the kernel runs to the HBM peak with its real traffic
-                         "traffic_GBps": (ncu_traffic("gather_c2") or 0) / statistics.mean(per) / 1e6,
-                         "alg_bytes_per_launch": alg_bytes,
-                         "avg_launch_ms": statistics.mean(per)},
+            "roofline": rf,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
@@ -642,126 +683,243 @@ def run_ours(args):
             "setup_s": round(setup_s, 2),
         }
         line.update(extras)
-        if groupby:
-            line["groupby_c3"] = groupby
         print(json.dumps(line), flush=True)
-    if dist_on:
-        dist.barrier()
-        dist.destroy_process_group()
+    E.close()
 
 
-def other_configs(args, ctx, stream, dist_on, rank, world, peak):
-    """The remaining BASELINE configs, each timed like the headline (W
-    warm-ups, K launches between barriers, CUDA events, max over ranks):
-    C1 small gather (both layouts), C4 index build at scale, C5 select +
-    4-column gather + per-category fp64 SUM."""
+def bench_c3(args, E):
+    """configs[2]: COUNT + SUM(int64 qty) per key on the recoded FK column
+    (D=2^24, s=1.0); per-GPU partials combined by dist.aggregate (packed
+    combine reduce to rank 0).  Plus Q3a heavy hitters and the group-by's
+    end-to-end line through skx_aggregate_host."""
+    import torch
+
+    from paper_1910_10063_b200 import dataset as ds
+    from paper_1910_10063_b200 import dist as sdist
+    w = ds.C3
+    coll, ex, ctx, peak = E.coll, E.ex, E.ctx, E.peak
+    n_total = E.total(w.n)
+    shard = E.shard(n_total)
+    gd = ds.make_groupby_dataset(w.d, n_total, w.z, w.seed, shard)
+    rows = shard.rows
+    counts = torch.empty(w.d, dtype=torch.uint64, device="cuda")
+    sums = torch.empty(w.d, dtype=torch.uint64, device="cuda")
+    stats = {}
+
+    def step(t):
+        sdist.aggregate(gd.fact_freq, gd.qty, w.d, ex, coll, shard, counts=counts, sums=sums,
+                        timer=t, check=False, stats=stats)
+    tg, per_g, launches, ph = timed(step, args.steps, args.warmup, coll, ctx, phases=True)
+    ctx.sync()
+    tg = max_over_ranks(tg, coll)
+    gb_bytes = rows * 12 + w.d * 16
+    kernel_ms = ph.get("aggregate", statistics.mean(per_g))
+    res = {"workload": "C3 group-by COUNT+SUM(int64 qty), D=2^24, s=1.0, reordered",
+           "value": n_total * args.steps / (tg * 1e-3), "unit": "rows/s",
+           "ms_per_step": tg / args.steps, "rows_total": n_total, "rows_per_gpu": rows,
+           "phases_ms": max_phases(ph, coll), "gpu_launches": int(launches),
+           "roofline": dict(roofline(gb_bytes, kernel_ms, peak),
+                            traffic=ncu_traffic("groupby_c3"))}
+    if coll.world > 1:
+        res["combine"] = dict(stats, note="per-rank bytes sent in the reduce (packed: 8 B per tail "
+                                          "key + 16 B per hot key + a 16 B guard all-reduce)")
+    # Q3a heavy hitters: counts of the k = 8192 hottest ids of the recoded column
+    # (operators.cpp:184-203); partials reduced like the group-by
+    hh = torch.empty(8192, dtype=torch.uint64, device="cuda")
+
+    def step_hh(_t):
+        ctx.call("skx_heavy_hitter_count", C_ptr(gd.fact_freq), rows, w.d, 8192, C_ptr(hh),
+                 ctx.stream(), sync=False)
+        coll.reduce(hh, 0)
+    th, per_h, _, _ = timed(step_hh, args.steps, args.warmup, coll)
+    ctx.sync()
+    th = max_over_ranks(th, coll)
+    res["heavy_hitters_k8192"] = {
+        "value": n_total * args.steps / (th * 1e-3), "unit": "rows/s", "ms_per_step": th / args.steps,
+        "roofline_frac": roofline(rows * 4 + 8192 * 8, statistics.mean(per_h), peak)["frac"]}
+    del hh
+    # end to end through the C-ABI host-buffer entry (N=1): pinned FK + qty in, counts +
+    # sums back, copies inside the timed region
+    if E.world == 1 and not args.no_e2e:
+        import ctypes as C
+        f_h = gd.fact_freq.cpu().pin_memory()
+        q_h = gd.qty.cpu().pin_memory()
+        c_h = torch.empty(w.d, dtype=torch.int64).pin_memory()
+        s_h = torch.empty(w.d, dtype=torch.int64).pin_memory()
+
+        def e2e():
+            ctx.check(ctx.lib.skx_aggregate_host(ctx.handle, C.c_void_p(f_h.data_ptr()),
+                                                 C.c_void_p(q_h.data_ptr()), 8, rows, w.d, 0,
+                                                 C.c_void_p(c_h.data_ptr()),
+                                                 C.c_void_p(s_h.data_ptr())))
+        e2e()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e()
+        te = time.perf_counter() - t0
+        ok = torch.equal(c_h.cuda(), counts.view(torch.int64)) and torch.equal(
+            s_h.cuda(), sums.view(torch.int64))
+        if not ok:
+            raise SystemExit("CorrectnessError: skx_aggregate_host disagrees with the device path")
+        res["e2e"] = {"value": rows * args.steps / te, "unit": "rows/s",
+                      "h2d_bytes_per_step": rows * 12, "d2h_bytes_per_step": w.d * 16,
+                      "steps": args.steps, "path": "skx_aggregate_host (pinned FK + qty in, "
+                                                   "counts + sums out)"}
+        del f_h, q_h, c_h, s_h
+    if E.rank == 0 and E.world == 1 and not args.no_cpu:
+        res["cpu_reference"] = _cpu_extra(lambda: cpu_groupby_reference(
+            gd.fact_freq[:1 << 26].cpu().numpy(), gd.qty[:1 << 24].cpu().numpy(), w.d))
+    del gd, counts, sums
+    torch.cuda.empty_cache()
+    return res
+
+
+def bench_c1(args, E):
+    """configs[0]: D=2^22 int32 price, 2^24 FKs, both layouts.  The 16 MiB
+    dimension is L2-resident and a launch takes tens of microseconds, so the
+    launches are captured in a CUDA Graph and replayed: per-launch time
+    excludes host launch overhead."""
+    import torch
+
+    from paper_1910_10063_b200 import dataset as ds
+    from paper_1910_10063_b200 import dist as sdist
+    w = ds.C1
+    coll, ex, ctx, peak = E.coll, E.ex, E.ctx, E.peak
+    n_total = E.total(w.n)
+    shard = E.shard(n_total)
+    c1d = ds.make_c1_dataset(shard)
+    o1 = torch.empty(shard.rows, dtype=torch.int32, device="cuda")
+    res = {}
+    per_graph = 20
+    for layout, f, dm in (("freq", c1d.g.fact_freq, c1d.price_freq),
+                          ("rand", c1d.g.fact_rand, c1d.price)):
+        sdist.gather(f, dm, ex, o1)  # warm (function attributes set outside capture)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(per_graph):
+                    sdist.gather(f, dm, ex, o1)
+        torch.cuda.current_stream().wait_stream(s)
+        k = max(3, min(args.steps, 10))
+        t, per, _, _ = timed(lambda _t: g.replay(), k, args.warmup, coll)
+        t = max_over_ranks(t, coll)
+        launch_ms = statistics.mean(per) / per_graph
+        res[layout] = {"value": n_total * k * per_graph / (t * 1e-3), "unit": "rows/s",
+                       "us_per_launch": 1e3 * launch_ms,
+                       "roofline_frac": roofline(shard.rows * 8, launch_ms, peak)["frac"]}
+        del g
+    ctx.sync()
+    ok = torch.equal(sdist.gather(c1d.g.fact_freq, c1d.price_freq, ex).view(torch.int32),
+                     sdist.gather(c1d.g.fact_rand, c1d.price, ex).view(torch.int32))
+    res["outputs_equal"] = bool(ok)
+    res["note"] = (f"L2-resident 16 MiB dimension; {per_graph} launches per CUDA Graph replay "
+                   "(inputs 192 MiB > L2)")
+    del c1d, o1
+    torch.cuda.empty_cache()
+    return res
+
+
+def bench_c4(args, E):
+    """configs[3]: index build at scale (D=2^26, s=1.25, 2^30 rows): per-GPU
+    u32 histogram -> all-reduce -> sort -> recode of the local shard ->
+    permute of the int32 and float32 dimensions."""
     import numpy as np
     import torch
 
-    from paper_1910_10063_b200 import dataset as ds_mod
-    from paper_1910_10063_b200 import skewdx as sx
-    out = {}
-    k = max(3, min(args.steps, 10))
+    from paper_1910_10063_b200 import dataset as ds
+    from paper_1910_10063_b200 import dist as sdist
+    w = ds.C4
+    coll, ex, ctx, peak = E.coll, E.ex, E.ctx, E.peak
+    n_total = E.total(w.n)
+    shard = E.shard(n_total)
+    ib = ds.make_index_build_dataset(shard)
+    counts = torch.empty(w.d, dtype=torch.uint32, device="cuda")
+    ff = torch.empty_like(ib.fact)
 
-    # C1: D=2^22 int32 price (uniform 1..1e6), 2^24 int32 FKs per GPU, s=1.0.
-    d1, n1 = 1 << 22, 1 << 24
-    g = ds_mod.make_gather_dataset(d1, n1 * world, 1.0, SEED + 7, torch.int32,
-                                   ds_mod.Shard(rank, world, rank * n1, (rank + 1) * n1))
-    price = ds_mod.fill_column(ds_mod.KIND_UNIFORM, torch.int32, d1, SEED + 8, 1, 1000000)
-    price_f = sx.permute_dimension(price, g.index, sync=False)
-    o1 = torch.empty(n1, dtype=torch.int32, device="cuda")
-    c1 = {}
-    for layout, f, dm in (("freq", g.fact_freq, price_f), ("rand", g.fact_rand, price)):
-        t, per, _ = timed_launches(lambda f=f, dm=dm: sx.materialize(f, dm, out=o1, ctx=ctx, sync=False),
-                                   k * 10, args.warmup, stream, dist_on)
-        t = max_over_ranks(t, dist_on)
-        c1[layout] = {"value": n1 * world * k * 10 / (t * 1e-3), "unit": "rows/s",
-                      "us_per_launch": 1e3 * t / (k * 10),
-                      "roofline_frac": n1 * 8 / (statistics.mean(per) * 1e-3) / 1e9 / peak}
-    c1["note"] = ("L2-resident 16 MiB dimension; back-to-back launches (inputs 192 MiB > L2), "
-                  "per-launch time includes launch overhead")
-    out["gather_c1"] = c1
-    del g, price, price_f, o1
-
-    # C4: index build at scale, D=2^26, s=1.25, 2^30 rows per GPU.
-    d4, n4 = 1 << 26, 1 << 30
-    sh = ds_mod.Shard(rank, world, rank * n4, (rank + 1) * n4)
-    fact = ds_mod.make_rand_fact(d4, n4 * world, 1.25, SEED + 9, sh)
-    dim_i = ds_mod.fill_column(ds_mod.KIND_RAW, torch.int32, d4, SEED + 10)
-    dim_f = ds_mod.fill_column(ds_mod.KIND_RAW, torch.int32, d4, SEED + 11).view(torch.float32)
-    counts = torch.empty(d4, dtype=torch.uint32, device="cuda")
-    ff = torch.empty_like(fact)
-
-    def c4_step():
-        sx.histogram_u32(fact, d4, counts, ctx=ctx, sync=False)
-        ds_mod._allreduce_u32(counts)
-        idx = sx.build_index(sx.FrequencyProfile(counts, n4 * world), ctx=ctx, sync=False)
-        sx.recode_fact(fact, idx, out=ff, ctx=ctx, sync=False)
-        sx.permute_dimension(dim_i, idx, ctx=ctx, sync=False)
-        sx.permute_dimension(dim_f, idx, ctx=ctx, sync=False)
-    t4, _, _ = timed_launches(c4_step, 3, 1, stream, dist_on)
+    def step(t):
+        idx, _ = sdist.rebuild(ib.fact, w.d, n_total, ex, coll, shard, counts, t, check=False)
+        ex.recode(ib.fact, idx, ff)
+        if t is not None:
+            t.mark("recode")
+        ex.permute(ib.dim_i, idx)
+        ex.permute(ib.dim_f, idx)
+        if t is not None:
+            t.mark("permute")
+    k = 3
+    t4, per4, launches, ph = timed(step, k, 1, coll, ctx, phases=True)
     ctx.sync()
-    t4 = max_over_ranks(t4, dist_on) / 3
-    alg4 = n4 * 12 + d4 * 28
-    out["index_build_c4"] = {"ms_per_build": t4, "rows_per_s": n4 * world / (t4 * 1e-3),
-                             "roofline_frac": alg4 / (t4 * 1e-3) / 1e9 / peak,
-                             "alg_bytes": alg4,
-                             "note": "histogram + all-reduce + sort + recode + permute int32 and "
-                                     "float32 dims; warm"}
-    del fact, dim_i, dim_f, counts, ff
+    t4 = max_over_ranks(t4, coll) / k
+    alg4 = shard.rows * 12 + w.d * 28
+    comp = sum(v for kk, v in ph.items() if kk != "allreduce")
+    res = {"ms_per_build": t4, "rows_per_s": n_total / (t4 * 1e-3), "rows_total": n_total,
+           "rows_per_gpu": shard.rows, "phases_ms": max_phases(ph, coll),
+           "gpu_launches": int(launches),
+           "roofline_frac": alg4 / (t4 * 1e-3) / 1e9 / peak,
+           "roofline_frac_kernels": alg4 / (comp * 1e-3) / 1e9 / peak, "alg_bytes": alg4,
+           "note": "dist.rebuild + recode + permute int32 and float32 dims; warm, mean of 3"}
+    if E.rank == 0 and E.world == 1 and not args.no_cpu:
+        rows = 1 << 24
+        res["cpu_reference"] = _cpu_extra(lambda: cpu_index_build_reference(
+            ib.fact[:rows].cpu().numpy(), w.d, ib.dim_i.cpu().numpy().view(np.uint32),
+            ib.dim_f.view(torch.int32).cpu().numpy().view(np.uint32)))
+    del ib, counts, ff
     torch.cuda.empty_cache()
-    if rank == 0 and world == 1 and not args.no_cpu:
-        small = ds_mod.make_rand_fact(1 << 22, 1 << 24, 1.25, SEED + 9, ds_mod.shard_of(1 << 24))
-        out["index_build_c4"]["cpu_reference"] = _cpu_extra(
-            lambda: cpu_rebuild_reference(small.cpu().numpy(), 1 << 22))
-        del small
+    return res
 
-    # C5: 2^31 rows (per GPU), D=2^25, category < 100, 4-column gather + fp64 SUM(price).
-    d5, n5 = 1 << 25, 1 << 31
-    sh = ds_mod.Shard(rank, world, rank * n5, (rank + 1) * n5)
-    fact = ds_mod.make_rand_fact(d5, n5 * world, 1.0, SEED + 12, sh)
-    counts = sx.histogram_u32(fact, d5, ctx=ctx, sync=False)
-    ds_mod._allreduce_u32(counts)
-    idx = sx.build_index(sx.FrequencyProfile(counts, n5 * world), ctx=ctx, sync=False)
-    fact_f = sx.recode_fact(fact, idx, ctx=ctx, sync=False)
-    del fact, counts
-    cat = sx.permute_dimension(ds_mod.fill_column(ds_mod.KIND_UNIFORM, torch.int32, d5, SEED + 13, 0, 1000), idx)
-    prc = sx.permute_dimension(ds_mod.fill_column(ds_mod.KIND_LOGNORMAL, torch.float32, d5, SEED + 14, 3.0, 1.0), idx)
-    sup = sx.permute_dimension(ds_mod.fill_column(ds_mod.KIND_RAW, torch.int64, d5, SEED + 15), idx)
-    flg = sx.permute_dimension(ds_mod.fill_column(ds_mod.KIND_RAW, torch.int16, d5, SEED + 16), idx)
-    bm = sx.build_bitmap_lt(cat, 100)  # category < 100, already in rank space
-    cap = n5 // 5
-    bufs = [torch.empty(cap, dtype=t, device="cuda")
-            for t in (torch.uint32, torch.int32, torch.float32, torch.int64, torch.int16)]
-    sums = torch.empty(1000, dtype=torch.float64, device="cuda")
-    cnt = torch.zeros(1, dtype=torch.uint64, device="cuda")
 
-    def c5_step():
-        ctx.call("skx_select_gather_sum", C_ptr(fact_f), n5, C_ptr(bm.words), d5, C_ptr(cat),
-                 # base 0: shard-local offsets (global ones exceed the reference's u32
-                 # row offsets, operators.cpp:88-90, once 2^31 rows per GPU x N > 2^32)
-                 C_ptr(prc), C_ptr(sup), C_ptr(flg), 0, 1000, cap, *[C_ptr(b) for b in bufs],
-                 C_ptr(sums), C_ptr(cnt), ctx.stream(), sync=False)
-        if dist_on:  # per-category fp64 partials reduced to rank 0
-            reduce_to_root(sums)
-    t5, per5, _ = timed_launches(c5_step, k, args.warmup, stream, dist_on)
+def bench_c5(args, E):
+    """configs[4]: 2^31 fact rows, D=2^25: select category < 100, gather the
+    four columns, SUM(price) per category (exact fixed point; combined across
+    ranks as int64 limbs by dist.select_gather_sum)."""
+    import numpy as np
+    import torch
+
+    from paper_1910_10063_b200 import dataset as ds
+    from paper_1910_10063_b200 import dist as sdist
+    w = ds.C5
+    coll, ex, ctx, peak = E.coll, E.ex, E.ctx, E.peak
+    n_total = E.total(w.n)
+    shard = E.shard(n_total)
+    sd = ds.make_select_dataset(shard)
+    n = shard.rows
+    cap = n // 5
+    dev = "cuda"
+    out = tuple(torch.empty(cap, dtype=t, device=dev) for t in
+                (torch.uint32, torch.int32, torch.float32, torch.uint64, torch.uint16)) + (
+        torch.empty(1000, dtype=torch.float64, device=dev),
+        torch.zeros(1, dtype=torch.uint64, device=dev))
+    # global row offsets (parallel_select's base) while they fit the reference's u32
+    # offsets (operators.cpp:88-90); shard-local past 2^32 rows (weak scaling only)
+    base = shard.begin if n_total <= 0xFFFFFFFF else 0
+    cols = (sd.cat, sd.price, sd.supp, sd.flag)
+
+    def step(t):
+        sdist.select_gather_sum(sd.fact, sd.bitmap, cols, 1000, ex, coll, shard, root=0,
+                                base=base, out=out, timer=t, check=False)
+    k = max(3, min(args.steps, 10))
+    t5, per5, launches, ph = timed(step, k, args.warmup, coll, ctx, phases=True)
     ctx.sync()
-    t5 = max_over_ranks(t5, dist_on)
-    sel = int(cnt.item())
+    t5 = max_over_ranks(t5, coll)
+    sel = int(out[6].item())
     if sel > cap:
         raise SystemExit("C5 output capacity exceeded")
-    alg5 = n5 * 4 + sel * 22 + 1000 * 8
-    out["select_c5"] = {"value": n5 * world * k / (t5 * 1e-3), "unit": "rows/s",
-                        "ms_per_step": t5 / k, "selected": sel, "selectivity": sel / n5,
-                        "roofline_frac": alg5 / (statistics.mean(per5) * 1e-3) / 1e9 / peak,
-                        "alg_bytes_per_step": alg5}
-    if rank == 0 and world == 1 and not args.no_cpu:
-        out["select_c5"]["cpu_reference"] = _cpu_extra(lambda: cpu_select_reference(
-            fact_f[:1 << 26].cpu().numpy(), bm.words.view(torch.int64).cpu().numpy().view(np.uint64),
-            d5))
-    del fact_f, cat, prc, sup, flg, bm, bufs, sums, cnt, idx
+    alg5 = n * 4 + sel * 22 + 1000 * 8
+    kernel_ms = ph.get("select", statistics.mean(per5))
+    res = {"value": n_total * k / (t5 * 1e-3), "unit": "rows/s", "ms_per_step": t5 / k,
+           "rows_total": n_total, "rows_per_gpu": n, "selected": sel, "selectivity": sel / n,
+           "phases_ms": max_phases(ph, coll), "gpu_launches": int(launches),
+           "roofline_frac": alg5 / (kernel_ms * 1e-3) / 1e9 / peak, "alg_bytes_per_step": alg5}
+    if E.rank == 0 and E.world == 1 and not args.no_cpu:
+        rows = 1 << 26
+        res["cpu_reference"] = _cpu_extra(lambda: cpu_select_reference(
+            sd.fact[:rows].cpu().numpy(), sd.bitmap.words.view(torch.int64).cpu().numpy().view(np.uint64),
+            w.d, cols=[c.cpu().numpy() for c in cols]))
+    del sd, out
     torch.cuda.empty_cache()
-    return out
+    return res
 
 
 def C_ptr(t):

@@ -440,6 +440,7 @@ class Reference:
         L.ref_aggregate_sum.argtypes = [vp, vp, u64, u64, u32, vp, vp, vp]
         L.ref_parallel_aggregate.argtypes = [vp, u64, u32, C.c_uint, ci, u32, vp, vp, vp, vp]
         L.ref_heavy_hitter_count.argtypes = [vp, u64, u32, u32, vp, vp, vp, vp]
+        L.ref_time_index_build.argtypes = [vp, u64, u32, vp, vp, vp]
         L.ref_time_parallel_materialize.restype = dbl
         L.ref_time_parallel_materialize.argtypes = [vp, u64, vp, u64, C.c_uint, ci]
         L.ref_time_gather_kernel.restype = dbl

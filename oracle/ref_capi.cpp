@@ -355,6 +355,30 @@ double ref_time_parallel_select(const std::uint32_t* fact, std::uint64_t n,
   return median(t);
 }
 
+// The config-4 index build through the reference's public API, once (no
+// warm-up: a sort of D ids takes seconds at D = 2^26): rebuild
+// (permindex.cpp:86-88, single thread -- the reference has no parallel index
+// build), recode_fact (:60-64) and permute_dimension (:66-73) of an int32
+// and a float32 (bit-cast) dimension.  ns[0..3) = rebuild, recode, permutes.
+int ref_time_index_build(const std::uint32_t* fact, std::uint64_t n, std::uint32_t d,
+                         const std::uint32_t* dim_i, const std::uint32_t* dim_f, double* ns) {
+  return guarded({nullptr, nullptr}, [&] {
+    const Column f = to_col(fact, n), di = to_col(dim_i, d), df = to_col(dim_f, d);
+    const double t0 = now_ns();
+    const PermutationIndex idx = rebuild(f, d);
+    const double t1 = now_ns();
+    const Column r = recode_fact(f, idx);
+    const double t2 = now_ns();
+    const Column pi = permute_dimension(di, idx);
+    const Column pf = permute_dimension(df, idx);
+    const double t3 = now_ns();
+    ns[0] = t1 - t0;
+    ns[1] = t2 - t1;
+    ns[2] = t3 - t2;
+    if (r.empty() || pi.size() != d || pf.size() != d) throw Error("index build produced nothing");
+  });
+}
+
 // aggregate_sum (operators.cpp:107-118, single thread: the reference has no
 // parallel SUM); median ns over reps after one warm-up.
 double ref_time_aggregate_sum(const std::uint32_t* fact, const std::uint32_t* measure,
