@@ -69,6 +69,8 @@ typedef struct skx_error_info {
 
 /* ---- context ------------------------------------------------------------ */
 int skx_version(void);
+/* Number of visible CUDA devices (0 when none). */
+int skx_device_count(int* count);
 int skx_ctx_create(int device, skx_ctx** out);
 int skx_ctx_destroy(skx_ctx* ctx);
 /* Waits for `stream`, then reports (and clears) any deferred device error. */

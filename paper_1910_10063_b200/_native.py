@@ -33,6 +33,7 @@ _vp, _u64, _u32, _i32, _int, _dbl = (C.c_void_p, C.c_uint64, C.c_uint32, C.c_int
 # name -> (restype, argtypes); mirrors include/skx.h
 SIGNATURES = {
     "skx_version": (_int, []),
+    "skx_device_count": (_int, [C.POINTER(_int)]),
     "skx_ctx_create": (_int, [_int, C.POINTER(_vp)]),
     "skx_ctx_destroy": (_int, [_vp]),
     "skx_sync": (_int, [_vp, _vp]),

@@ -74,15 +74,16 @@ def build_libskx(force: bool = False, verbose: bool = False) -> str:
 
 
 def build_shim(force: bool = False) -> str:
-    """C++ drop-in (namespace skewdx, reference signatures) over the C-ABI."""
-    src = os.path.join(CPP, "skewdx_b200.cpp")
+    """C++ drop-in (namespace skewdx, reference signatures) over the C-ABI,
+    with the multi-device overloads (skewdx/multigpu.hpp)."""
+    srcs = [os.path.join(CPP, "skewdx_b200.cpp"), os.path.join(CPP, "skewdx_b200_multigpu.cpp")]
     hdrs = glob.glob(os.path.join(CPP, "include", "skewdx", "*.hpp"))
-    if not os.path.exists(src):
+    if not os.path.exists(srcs[0]):
         return ""
-    if force or _stale(LIBSHIM, [src, *hdrs, LIBSKX, os.path.join(INCLUDE, "skx.h")]):
-        _run(["g++", "-O2", "-std=c++20", "-fPIC", "-shared", "-Wall", "-Wextra", "-I" + INCLUDE,
-              "-I" + os.path.join(CPP, "include"), src, "-o", LIBSHIM, "-L" + PKG, "-lskx",
-              "-Wl,-rpath,$ORIGIN"])
+    if force or _stale(LIBSHIM, [*srcs, *hdrs, LIBSKX, os.path.join(INCLUDE, "skx.h")]):
+        _run(["g++", "-O2", "-std=c++20", "-fPIC", "-shared", "-Wall", "-Wextra", "-pthread",
+              "-I" + INCLUDE, "-I" + os.path.join(CPP, "include"), *srcs, "-o", LIBSHIM,
+              "-L" + PKG, "-lskx", "-Wl,-rpath,$ORIGIN"])
     return LIBSHIM
 
 

@@ -90,7 +90,17 @@ using namespace skx;
 
 extern "C" {
 
-int skx_version(void) { return 1; }
+int skx_version(void) { return 2; }
+
+int skx_device_count(int* count) {
+  if (!count) return SKX_INVALID_ARGUMENT;
+  *count = 0;
+  if (cudaGetDeviceCount(count) != cudaSuccess) {
+    cudaGetLastError();
+    *count = 0;
+  }
+  return SKX_OK;
+}
 
 int skx_ctx_create(int device, skx_ctx** out) {
   if (!out) return SKX_INVALID_ARGUMENT;
