@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _declared():
     src = open(os.path.join(ROOT, "include", "skx.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|uint64_t|void\s*\*)\s*(skx_\w+)\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|uint64_t|void\s*\*|skx_ctx\s*\*|const char\s*\*)\s*(skx_\w+)\(", src, re.M)))
 
 
 @pytest.fixture(scope="module")
