@@ -627,9 +627,23 @@ def run_ours(args):
 
     if not args.no_extras and want("c2"):
         # the rest of the BASELINE C2 sweep (s = 0.5 and 1.5; s = 1.0 is the headline),
-        # both layouts, same kernel and timing rules
+        # both layouts, same kernel and timing rules; beside each, the threshold-split
+        # two-pass gather (materialize_split) on the reordered layout
         sweep = {}
         ks = max(3, min(args.steps, 10))
+
+        def split_cells(zz, f, dm):
+            for t in sorted({min(1 << 20, d), min(1 << 23, d)}):
+                ts, per_s, _, _ = timed(
+                    lambda _t, t=t: sx.materialize_split(f, dm, t, out=out, ctx=ctx, sync=False),
+                    ks, args.warmup, coll)
+                ms = max_over_ranks(ts, coll) / ks
+                sweep[f"s{zz}_freq_split_t{t}"] = {
+                    "ms_per_step": ms, "value": n_total / (ms * 1e-3), "unit": "rows/s",
+                    "roofline_frac": roofline(alg_bytes, statistics.mean(per_s), peak)["frac"]}
+            ctx.sync()
+        if shard.rows < (1 << 32):
+            split_cells(args.z, data.fact_freq, data.dim_freq)
         for zz in (0.5, 1.5):
             g = ds.make_gather_dataset(d, n_total, zz, ds.SEED, torch.int64, shard)
             for lay, f, dm in (("freq", g.fact_freq, g.dim_freq), ("rand", g.fact_rand, g.dim_rand)):
@@ -640,6 +654,8 @@ def run_ours(args):
                                          "unit": "rows/s",
                                          "roofline_frac": roofline(alg_bytes, statistics.mean(per_s),
                                                                    peak)["frac"]}
+            if shard.rows < (1 << 32):
+                split_cells(zz, g.fact_freq, g.dim_freq)
             del g
             torch.cuda.empty_cache()
         extras["c2_s_sweep"] = sweep

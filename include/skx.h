@@ -129,6 +129,16 @@ int skx_gather_u32(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uint32_
 int skx_gather_u64(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uint64_t* dim,
                    uint64_t dim_len, uint64_t* out, void* stream);
 
+/* Threshold-split materialize: materialize_split
+ * (operators.cpp:68-85) over KernelTable::gather_split_pass1 (kernels.hpp:
+ * 32-39): pass 1 gathers rows with id <= threshold and queues the others,
+ * pass 2 patches the queued rows.  Same result as skx_gather_*; threshold
+ * must lie in 1..dim_len (SKX_INVALID_ARGUMENT otherwise), n < 2^32. */
+int skx_gather_split_u32(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uint32_t* dim,
+                         uint64_t dim_len, uint32_t threshold, uint32_t* out, void* stream);
+int skx_gather_split_u64(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uint64_t* dim,
+                         uint64_t dim_len, uint32_t threshold, uint64_t* out, void* stream);
+
 /* ---- index build (permindex.cpp) ---------------------------------------- */
 /* count_frequencies (permindex.cpp:18-30): counts[id-1] = #rows with id.
  * `counts` (u64[d]) is overwritten. */

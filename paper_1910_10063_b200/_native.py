@@ -44,6 +44,8 @@ SIGNATURES = {
     "skx_gather_u16": (_int, [_vp, _vp, _u64, _vp, _u64, _vp, _vp]),
     "skx_gather_u32": (_int, [_vp, _vp, _u64, _vp, _u64, _vp, _vp]),
     "skx_gather_u64": (_int, [_vp, _vp, _u64, _vp, _u64, _vp, _vp]),
+    "skx_gather_split_u32": (_int, [_vp, _vp, _u64, _vp, _u64, _u32, _vp, _vp]),
+    "skx_gather_split_u64": (_int, [_vp, _vp, _u64, _vp, _u64, _u32, _vp, _vp]),
     "skx_count_frequencies": (_int, [_vp, _vp, _u64, _u32, _vp, _vp]),
     "skx_histogram_u32": (_int, [_vp, _vp, _u64, _u32, _vp, _int, _vp]),
     "skx_build_index": (_int, [_vp, _vp, _u32, _u64, _vp, _vp, _vp]),

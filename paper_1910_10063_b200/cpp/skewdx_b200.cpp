@@ -403,11 +403,17 @@ Column materialize(const Column& fact, const Column& dim, int /*prefetch_distanc
 }
 
 Column materialize_split(const Column& fact, const Column& dim, SplitThreshold threshold) {
-  // The two-pass split is a CPU latency trick (operators.cpp:68-85); on the
-  // GPU the hot prefix lives in L1/L2 and one pass gives the same result.
+  // operators.cpp:68-85 on the device: pass 1 gathers ids <= t and queues the
+  // rest, pass 2 patches them (skx_gather_split_u32).
   if (threshold.t == 0 || threshold.t > dim.size())
     throw InvalidArgument("split threshold must lie in 1..D");
-  return gather(fact, dim);
+  Column out(fact.size());
+  if (fact.empty()) return out;
+  DevBuf f(fact), d(dim), o(out.size() * 4);
+  run(skx_gather_split_u32(ctx(), f.as<std::uint32_t>(), fact.size(), d.as<std::uint32_t>(),
+                           dim.size(), threshold.t, o.as<std::uint32_t>(), nullptr));
+  o.to(out);
+  return out;
 }
 
 std::vector<std::uint32_t> select(const Column& fact, const Bitmap& bitmap) {

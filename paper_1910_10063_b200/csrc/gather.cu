@@ -45,6 +45,9 @@ constexpr int kPolWindow = 4;  // L2 persisting access-policy window over the di
 constexpr int kPolNoL1 = 8;    // dimension loads bypass L1 allocation
 constexpr int kPolPrefetch = 16;  // software-pipeline the FK stream one iteration ahead
 constexpr int kPolTiered = 32;    // per-access cache class from the reordered id (see below)
+constexpr int kPolBulkOut = 2048;  // output staged in shared memory, 8 KB cp.async.bulk stores
+constexpr int kPolSt256 = 4096;    // 256-bit output stores (one per 4-row vector of int64)
+constexpr int kBulkRing = 4;       // 8 KB staging buffers per CTA (kPolBulkOut)
 
 // Cache tiers of a skew-reordered dimension (policy bit 32).  After the
 // index, popularity decreases with the id, so the id alone says how hot an
@@ -165,6 +168,12 @@ __global__ void __launch_bounds__((F & kPolHot) ? kThreadsHot : kThreads, (F & k
   }
   const uint4* fv = reinterpret_cast<const uint4*>(fact + head);
   V* o = out + head;
+  constexpr bool BULK = (F & kPolBulkOut) != 0 && !HOT && OUT_VEC;  // bulk stores: 16 B aligned
+  // kPolBulkOut: for each u the CTA's NT vectors are one contiguous run of
+  // NT * 4 rows (8 KB of int64), staged in a ring of kBulkRing buffers and
+  // written by one cp.async.bulk store with an L2 evict_first hint.
+  V* s_ring = reinterpret_cast<V*>(smem_raw);
+  uint32_t ring_n = 0;
   const uint64_t stride = (uint64_t)gridDim.x * NT * kUnroll;
   uint64_t base = (uint64_t)blockIdx.x * NT * kUnroll + threadIdx.x;
   uint4 f[kUnroll];
@@ -176,7 +185,8 @@ __global__ void __launch_bounds__((F & kPolHot) ? kThreadsHot : kThreads, (F & k
       f[u] = vi < nvec ? ld_stream_v4(fv + vi, pol_s) : make_uint4(1, 1, 1, 1);
     }
   }
-  for (; base < nvec; base += stride) {
+  // BULK: CTA-uniform trip count (the staging barriers)
+  for (; (BULK ? base - threadIdx.x : base) < nvec; base += stride) {
     uint4 fn[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
@@ -231,11 +241,46 @@ __global__ void __launch_bounds__((F & kPolHot) ? kThreadsHot : kThreads, (F & k
         }
       }
     }
+    if constexpr (BULK) {
+      const uint64_t cta0 = base - threadIdx.x;  // first vector of this CTA iteration
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const uint64_t v0 = cta0 + (uint64_t)u * NT;  // CTA-uniform
+        const uint64_t vi = v0 + threadIdx.x;
+        if (v0 + NT <= nvec) {
+          V* buf = s_ring + (size_t)(ring_n % kBulkRing) * NT * 4;
+          if (threadIdx.x == 0)  // the buffer's previous store has finished reading it
+            asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kBulkRing - 1) : "memory");
+          __syncthreads();
+#pragma unroll
+          for (int j = 0; j < 4; ++j) buf[threadIdx.x * 4 + j] = v[u][j];
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(buf);
+            asm volatile(
+                "cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+                ::"l"(o + v0 * 4), "r"(sa), "r"((uint32_t)(NT * 4 * sizeof(V))), "l"(pol_s)
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          ++ring_n;
+        } else if (vi < nvec) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) o[vi * 4 + j] = v[u][j];
+        }
+      }
+    } else {
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const uint64_t vi = base + (uint64_t)u * NT;
       if (vi < nvec) {
-        if (F & 64) {  // diagnostic: keep the loads, drop the output stream
+        if ((F & kPolSt256) && sizeof(V) == 8 && OUT_VEC) {  // one 256-bit store per vector
+          asm volatile("st.global.cs.v4.b64 [%0], {%1,%2,%3,%4};" ::"l"(o + vi * 4),
+                       "l"((uint64_t)v[u][0]), "l"((uint64_t)v[u][1]), "l"((uint64_t)v[u][2]),
+                       "l"((uint64_t)v[u][3])
+                       : "memory");
+        } else if (F & 64) {  // diagnostic: keep the loads, drop the output stream
           dbg ^= (uint64_t)v[u][0] ^ (uint64_t)v[u][1] ^ (uint64_t)v[u][2] ^ (uint64_t)v[u][3];
         } else if (OUT_VEC) {
           if (F & 128) {  // .cs (streaming) cache operator instead of an L2 policy
@@ -254,12 +299,14 @@ __global__ void __launch_bounds__((F & kPolHot) ? kThreadsHot : kThreads, (F & k
         }
       }
     }
+    }  // !BULK
     if (PREF) {
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) f[u] = fn[u];
     }
   }
   if ((F & 64) && dbg == 0x5eed5eed5eedull) o[threadIdx.x] = (V)dbg;
+  if (BULK && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // Scalar rows [b, e) -- the unaligned head and the ragged tail (< 4 rows each).
@@ -292,7 +339,8 @@ cudaError_t launch_vec(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64
                          : grid_for(ctx, nvec, kThreads * kUnroll,
                                     nvec / (kThreads * kUnroll) < 16u * 2u * ctx->num_sms
                                         ? SKX_GATHER_SMALL_CTAS : 8));
-  cfg.dynamicSmemBytes = HOT ? (size_t)hot * sizeof(V) : 0;
+  cfg.dynamicSmemBytes = HOT ? (size_t)hot * sizeof(V)
+                             : ((F & kPolBulkOut) ? (size_t)kBulkRing * kThreads * 4 * sizeof(V) : 0);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   cfg.attrs = attr;
@@ -315,7 +363,7 @@ cudaError_t launch_vec(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64
     attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     cfg.numAttrs = 1;
   }
-  if (HOT)
+  if (HOT || (F & kPolBulkOut))
     cudaFuncSetAttribute(k_gather_vec<V, OUT_VEC, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)cfg.dynamicSmemBytes);
   return cudaLaunchKernelEx(&cfg, k_gather_vec<V, OUT_VEC, F>, fact, head, nvec, dim, dim_len, out,
@@ -334,7 +382,7 @@ cudaError_t dispatch_vec(skx_ctx* ctx, int F, const uint32_t* fact, uint64_t hea
                : launch_vec<V, OUT_VEC, (x)>(ctx, fact, head, nvec, dim, dim_len, out, t, s);
   SKX_F(0) SKX_F(1) SKX_F(3) SKX_F(9) SKX_F(17) SKX_F(19)
   SKX_F(33) SKX_F(35) SKX_F(49) SKX_F(51) SKX_F(65) SKX_F(97) SKX_F(69) SKX_F(129) SKX_F(128)
-  SKX_F(131) SKX_F(385) SKX_F(641) SKX_F(1153)
+  SKX_F(131) SKX_F(385) SKX_F(641) SKX_F(1153) SKX_F(2177) SKX_F(4225)
 #undef SKX_F
   return cudaErrorInvalidValue;
 }
@@ -390,6 +438,84 @@ int gather_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const V* dim, ui
   return SKX_OK;
 }
 
+// ---- threshold-split materialize -------------------------
+// Reference: materialize_split (operators.cpp:68-85) with the table entry
+// gather_split_pass1 (kernels.hpp:32-39, scalar.cpp:44-61, avx2.cpp:100-143):
+// pass 1 gathers the rows whose id <= t (the hot prefix of a reordered
+// dimension) and writes 0 for the others while appending (row, id) to a miss
+// list; pass 2 patches the misses.  On the CPU this keeps the hot gather free
+// of the cold rows' cache pollution.  On B200 pass 1 streams exactly like the
+// one-pass gather; the miss list is compacted per warp (ballot + one atomic),
+// so its order across warps is arbitrary -- pass 2's result does not depend on
+// it (every miss writes its own row).  Pass 2 reads the list coalesced, the
+// dimension at random and stores 8 bytes at random rows (a sector
+// read-modify-write each): measured against the one-pass gather in
+// profiles/r2_experiments.md.
+template <typename V>
+__global__ void __launch_bounds__(256)
+    k_split_pass1(const uint32_t* __restrict__ fact, uint64_t n, const V* __restrict__ dim,
+                  uint64_t dim_len, uint32_t t, V* __restrict__ out, uint2* __restrict__ miss,
+                  unsigned long long* __restrict__ nmiss, DevErr* err) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t pol_d = policy_evict_last();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t n_round = (n + 31) / 32 * 32;  // warp-uniform trips (ballots)
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n_round; k += stride) {
+    const bool live = k < n;
+    const uint32_t id = live ? __ldcs(fact + k) : 1u;
+    const uint32_t idx = id - 1u;
+    const bool in = idx < dim_len;
+    if (live && !in) record_violation(err, k, id);
+    const bool cold = live && in && id > t;
+    V v = 0;
+    if (live && in && !cold) v = ld_dim<V>(dim + idx, pol_d, true);
+    if (live) __stcs(out + k, v);
+    const uint32_t m = __ballot_sync(0xffffffffu, cold);
+    if (m) {
+      unsigned long long at = 0;
+      const int first = __ffs(m) - 1;
+      if (lane == first) at = atomicAdd(nmiss, (unsigned long long)__popc(m));
+      at = __shfl_sync(0xffffffffu, at, first);
+      if (cold) miss[at + __popc(m & lanemask_lt())] = make_uint2((uint32_t)k, id);
+    }
+  }
+}
+
+template <typename V>
+__global__ void __launch_bounds__(256)
+    k_split_pass2(const uint2* __restrict__ miss, const unsigned long long* __restrict__ nmiss,
+                  const V* __restrict__ dim, V* __restrict__ out) {
+  const uint64_t m = *nmiss;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const uint2 e = __ldcs(miss + i);
+    out[e.x] = __ldg(dim + (e.y - 1u));
+  }
+}
+
+template <typename V>
+int gather_split_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const V* dim,
+                      uint64_t dim_len, uint32_t t, V* out, cudaStream_t s) {
+  if (t == 0 || t > dim_len)
+    return set_error(ctx, SKX_INVALID_ARGUMENT, "split threshold must lie in 1..D");
+  if (n > 0xFFFFFFFFull)
+    return set_error(ctx, SKX_INVALID_ARGUMENT, "gather_split: row positions exceed 32 bits");
+  if (n == 0) return SKX_OK;
+  ctx->last_domain = dim_len;
+  char* sp = static_cast<char*>(scratch(ctx, 1, 256 + n * sizeof(uint2), s));
+  if (!sp) return set_error(ctx, SKX_CUDA_ERROR, "gather_split: out of device memory");
+  auto* nmiss = reinterpret_cast<unsigned long long*>(sp);
+  auto* miss = reinterpret_cast<uint2*>(sp + 256);
+  cudaError_t e = cudaMemsetAsync(nmiss, 0, 8, s);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "gather_split memset");
+  k_split_pass1<V><<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(fact, n, dim, dim_len, t, out, miss,
+                                                            nmiss, ctx->err);
+  k_split_pass2<V><<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(miss, nmiss, dim, out);
+  ctx->launches += 2;
+  SKX_CHECK_LAUNCH(ctx, "gather_split");
+  return SKX_OK;
+}
+
 }  // namespace
 
 int launch_gather(skx_ctx* ctx, int width, const uint32_t* fact, uint64_t n, const void* dim,
@@ -433,6 +559,19 @@ int skx_recode_fact(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uint32
                     uint32_t d, uint32_t* out, void* stream) {
   // permindex.cpp:60-64: recode is materialize(fact, ranks).
   return skx::launch_gather(ctx, 4, fact, n, ranks, d, out, skx::as_stream(stream));
+}
+
+int skx_gather_split_u32(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uint32_t* dim,
+                         uint64_t dim_len, uint32_t threshold, uint32_t* out, void* stream) {
+  if (!ctx) return SKX_INVALID_ARGUMENT;
+  return skx::gather_split_impl<uint32_t>(ctx, fact, n, dim, dim_len, threshold, out,
+                                          skx::as_stream(stream));
+}
+int skx_gather_split_u64(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uint64_t* dim,
+                         uint64_t dim_len, uint32_t threshold, uint64_t* out, void* stream) {
+  if (!ctx) return SKX_INVALID_ARGUMENT;
+  return skx::gather_split_impl<uint64_t>(ctx, fact, n, dim, dim_len, threshold, out,
+                                          skx::as_stream(stream));
 }
 
 #define SKX_PERMUTE(W, T)                                                                  \

@@ -41,6 +41,9 @@ namespace {
 // 1 pass 15.2 ms, 2 passes (128 MB) 11.3, 3 (~85 MB) 10.8, 4 13.9, 8 24.8.
 #define SKX_HIST_PASS_BYTES (96ull << 20)
 #endif
+#ifndef SKX_HIST_SAMPLED
+#define SKX_HIST_SAMPLED 1  // direct counters: sampled read-only hot set (k_histogram_seeded)
+#endif
 #ifndef SKX_HIST_CTAS
 #define SKX_HIST_CTAS 3
 #endif
@@ -318,6 +321,128 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// ---- sampled hot set (direct counters) -------------------------------------
+// The dynamic table above keeps the first keys a CTA sees: under Zipf(1.25)
+// many are one-off tail keys, so ~21% of C4's rows still reached global
+// reductions (ncu: 231 M RED sectors per 2^30 rows) although the 8192 most
+// frequent keys carry ~92% of the rows.  Instead, a strided sample of the
+// column is counted first (k_hist_sample, an L2-resident open-addressing
+// table), the keys hit at least twice become the hot set (k_hist_pick), and
+// every CTA loads that set into a read-only two-choice table: no slot claims
+// in the main loop, and the cold reductions fall to the true tail.
+constexpr int kSampleBits = 21;                     // 2M (key, hits) slots = 16 MB
+constexpr uint32_t kHotCap = (kTable * 3) / 4;      // hot keys per table (load 0.75)
+
+__global__ void __launch_bounds__(256)
+    k_hist_sample(const uint32_t* __restrict__ fact, uint64_t step, uint32_t nsamp, uint32_t d,
+                  uint2* __restrict__ tab) {
+  constexpr uint32_t mask = (1u << kSampleBits) - 1u;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nsamp; i += gridDim.x * blockDim.x) {
+    const uint32_t key = __ldg(fact + (uint64_t)i * step);
+    if (key - 1u >= d) continue;  // violations are reported by the counting pass
+    uint32_t h = (key * 0x9E3779B1u) >> (32 - kSampleBits);
+    for (int p = 0; p < 64; ++p, h = (h + 1) & mask) {
+      uint32_t k = tab[h].x;
+      if (k == 0u) {
+        k = atomicCAS(&tab[h].x, 0u, key);
+        if (k == 0u) k = key;
+      }
+      if (k == key) {
+        atomicAdd(&tab[h].y, 1u);
+        break;
+      }
+    }
+  }
+}
+
+// Appends the keys sampled at least `min_hits` times (and, when hi_hits > 0,
+// fewer than hi_hits) to hot[0, cap).
+__global__ void __launch_bounds__(256)
+    k_hist_pick(const uint2* __restrict__ tab, uint32_t min_hits, uint32_t hi_hits,
+                uint32_t* __restrict__ hot, unsigned int* nhot, uint32_t cap) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < (1u << kSampleBits);
+       i += gridDim.x * blockDim.x) {
+    const uint2 e = tab[i];
+    if (e.x != 0u && e.y >= min_hits && (hi_hits == 0u || e.y < hi_hits)) {
+      const unsigned int at = atomicAdd(nhot, 1u);
+      if (at < cap) hot[at] = e.x;
+    }
+  }
+}
+
+template <typename CT>
+__global__ void __launch_bounds__(kThreads)
+    k_histogram_seeded(const uint32_t* __restrict__ fact, uint64_t head, uint64_t nvec, uint64_t n,
+                       uint32_t d, CT* __restrict__ counts, DevErr* err,
+                       const uint32_t* __restrict__ hot, const unsigned int* nhot_p) {
+  extern __shared__ __align__(16) uint32_t smem_tab[];
+  uint32_t* keys = smem_tab;
+  uint32_t* cnts = smem_tab + kTable;
+  for (int i = threadIdx.x; i < kTable; i += kThreads) {
+    keys[i] = 0u;
+    cnts[i] = 0u;
+  }
+  __syncthreads();
+  const uint32_t nh = min(*nhot_p, kHotCap);
+  for (uint32_t i = threadIdx.x; i < nh; i += kThreads) {  // fill once; read-only afterwards
+    const uint32_t key = __ldg(hot + i);
+    if (atomicCAS(&keys[slot_hash(key)], 0u, key) != 0u) atomicCAS(&keys[slot_hash2(key)], 0u, key);
+  }
+  __syncthreads();
+  auto count = [&](uint32_t key) {  // key already domain-checked
+    const uint32_t h1 = slot_hash(key), h2 = slot_hash2(key);
+    const uint32_t k1 = keys[h1], k2 = keys[h2];
+    if (k1 == key)
+      atomicAdd(&cnts[h1], 1u);
+    else if (k2 == key)
+      atomicAdd(&cnts[h2], 1u);
+    else
+      global_add<CT>(counts, key - 1u, 1u);
+  };
+  const uint64_t pol = policy_evict_first();
+  const uint4* fv = reinterpret_cast<const uint4*>(fact + head);
+  const uint64_t per_iter = (uint64_t)kThreads * kUnroll;
+  const uint64_t stride = (uint64_t)gridDim.x * per_iter;
+  for (uint64_t base = (uint64_t)blockIdx.x * per_iter + threadIdx.x; base < nvec; base += stride) {
+    uint4 f[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint64_t vi = base + (uint64_t)u * kThreads;
+      f[u] = vi < nvec ? ld_stream_v4(fv + vi, pol) : make_uint4(1, 1, 1, 1);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint64_t vi = base + (uint64_t)u * kThreads;
+      const uint32_t ids[4] = {f[u].x, f[u].y, f[u].z, f[u].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if ((ids[j] - 1u) < d) {
+          if (vi < nvec) count(ids[j]);
+        } else if (vi < nvec) {
+          record_violation(err, head + vi * 4 + j, ids[j]);
+        }
+      }
+    }
+  }
+  if (blockIdx.x == 0) {  // scalar head [0, head) and tail [head + 4*nvec, n)
+    const uint64_t tail_b = head + nvec * 4;
+    const uint64_t extra = head + (n - tail_b);
+    for (uint64_t t = threadIdx.x; t < extra; t += kThreads) {
+      const uint64_t k = t < head ? t : tail_b + (t - head);
+      const uint32_t id = fact[k];
+      if ((id - 1u) < d)
+        count(id);
+      else
+        record_violation(err, k, id);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kTable; i += kThreads) {
+    const uint32_t k = keys[i];
+    if (k != 0u && cnts[i] != 0u) global_add<CT>(counts, k - 1, cnts[i]);
+  }
+}
+
 // Second kernel: apply the buckets in key-range order; all CTAs sweep bucket
 // b together, so its counter slice (2^shift counters) stays L2-resident and
 // the reductions never read-modify-write HBM lines.
@@ -466,6 +591,33 @@ int histogram_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64_t n
     k_histogram<CT, false, false><<<grid, kThreads, smem, s>>>(fact, head, nvec, n, d, counts, bk,
                                                                ctx->err, nullptr, nullptr, chk);
     ctx->launches += 3;
+  } else if (SKX_HIST_SAMPLED && n >= (uint64_t(1) << 22) && d > (uint32_t)kTable) {
+    // sampled hot set: ~2^20 rows (strided over the whole column) counted
+    // into an L2-resident table, keys hit >= 3 times first, then >= 2
+    const uint32_t nsamp = (uint32_t)std::min<uint64_t>(n / 16, uint64_t(1) << 20);
+    const uint64_t step = n / nsamp;
+    const size_t tab_b = (size_t(1) << kSampleBits) * 8;
+    char* sp = static_cast<char*>(scratch(ctx, 0, tab_b + 256 + (size_t)kHotCap * 4, s));
+    if (!sp) return set_error(ctx, SKX_CUDA_ERROR, "histogram: out of device memory");
+    uint2* tab = reinterpret_cast<uint2*>(sp);
+    unsigned int* nhot = reinterpret_cast<unsigned int*>(sp + tab_b);
+    uint32_t* hot = reinterpret_cast<uint32_t*>(sp + tab_b + 256);
+    cudaError_t e = cudaMemsetAsync(sp, 0, tab_b + 256, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "histogram memset");
+    k_hist_sample<<<grid_for(ctx, nsamp, 256, 8), 256, 0, s>>>(fact, step, nsamp, d, tab);
+    // hottest first: bands of sample hits [lo, hi), so a full hot set never
+    // leaves out a key hotter than one it holds (a top key counted by global
+    // reductions would serialise on one address)
+    const unsigned pick_grid = grid_for(ctx, size_t(1) << kSampleBits, 256, 8);
+    const uint32_t bands[] = {0, 4096, 512, 64, 16, 8, 4, 3, 2};
+    for (int b = 1; b < (int)(sizeof bands / sizeof bands[0]); ++b)
+      k_hist_pick<<<pick_grid, 256, 0, s>>>(tab, bands[b], bands[b - 1], hot, nhot, kHotCap);
+    ctx->launches += (sizeof bands / sizeof bands[0]) - 3;
+    cudaFuncSetAttribute(k_histogram_seeded<CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    k_histogram_seeded<CT><<<grid, kThreads, smem, s>>>(fact, head, nvec, n, d, counts, ctx->err,
+                                                        hot, nhot);
+    ctx->launches += 4;
   } else {
     cudaFuncSetAttribute(k_histogram<CT, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);

@@ -303,6 +303,22 @@ def materialize(fact, dim, *, out=None, ctx=None, sync=True) -> torch.Tensor:
     return out
 
 
+def materialize_split(fact, dim, threshold: int, *, out=None, ctx=None, sync=True) -> torch.Tensor:
+    """operators.cpp:68-85: the same result as materialize, computed in two
+    passes split on the rank threshold t (ids <= t first, then the misses)."""
+    fact = _col(fact)
+    dim = _values(dim)
+    ctx = _ctx_for(fact, ctx)
+    w = _WIDTH[dim.dtype]
+    if w not in (4, 8):
+        raise InvalidArgument("materialize_split: 32- or 64-bit values")
+    if out is None:
+        out = torch.empty(fact.numel(), dtype=dim.dtype, device=fact.device)
+    ctx.call(f"skx_gather_split_u{8 * w}", _ptr(fact), fact.numel(), _ptr(dim), dim.numel(),
+             int(threshold), _ptr(out), ctx.stream(), sync=sync)
+    return out
+
+
 def select(fact, bitmap: Bitmap, *, base: int = 0, ctx=None) -> torch.Tensor:
     """Q2, operators.cpp:87-98: ascending 0-based row offsets whose bit is set."""
     fact = _col(fact)

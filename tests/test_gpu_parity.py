@@ -574,3 +574,56 @@ def test_build_index_small_count_pass(sx, oracle, case):
     assert np.array_equal(np_(idx.offsets), off) and np.array_equal(np_(idx.ranks), rk)
     idx32 = sx.build_index(sx.FrequencyProfile(cu(counts.astype(np.uint32)), total))
     assert np.array_equal(np_(idx32.offsets), off)
+
+
+@pytest.mark.parametrize("policy", [129, 2177, 4225, 1, 0])
+def test_gather_output_store_policies(sx, policy):
+    """Every output-store variant of the gather (128-bit .cs stores, 8 KB
+    shared-memory-staged cp.async.bulk stores, 256-bit stores, plain) writes
+    the same bytes, for ragged sizes, partial CTA chunks and misaligned heads."""
+    ctx = sx.context(0)
+    rng = np.random.default_rng(policy)
+    d = 70001
+    dim_np = rng.integers(0, 2**63, size=d, dtype=np.uint64)
+    dim = cu(dim_np)
+    try:
+        ctx.set_gather_policy(policy)
+        for n in [1, 5, 1023, 1024 * 9 + 3, 1 << 20, (1 << 22) + 777, 40_000_003]:
+            fact_np = rng.integers(1, d + 1, size=n + 1, dtype=np.uint32)
+            full = cu(fact_np)
+            for off in (0, 1):
+                out = sx.materialize(full[off: off + n], dim)
+                exp = dim_np[fact_np[off: off + n].astype(np.int64) - 1]
+                assert np.array_equal(np_(out).view(np.uint64), exp), (policy, n, off)
+    finally:
+        ctx.set_gather_policy(129)
+
+
+@pytest.mark.parametrize("dtype,npdt", [(torch.uint32, np.uint32), (torch.int64, np.int64)])
+def test_materialize_split_two_pass(sx, oracle, dtype, npdt):
+    """materialize_split (operators.cpp:68-85): the two-pass device kernel
+    (hot ids <= t gathered in pass 1, misses patched in pass 2) equals the
+    one-pass gather for every threshold, ragged sizes; bad thresholds and
+    out-of-domain rows raise like the reference."""
+    from paper_1910_10063_b200 import DomainViolation, InvalidArgument
+    rng = np.random.default_rng(5)
+    d = 30011
+    dim_np = rng.integers(0, 2**62, size=d, dtype=np.uint64).astype(npdt)
+    dim = cu(dim_np)
+    cdf = oracle.zipf_cdf(d, 1.0)
+    for n in [1, 31, 33, 100003, (1 << 22) + 5]:
+        fact_np = oracle.generate_zipf_counter(cdf, None, 3, 0, n)
+        f = cu(fact_np)
+        exp = oracle.gather(fact_np, dim_np)
+        for t in [1, 7, 1000, d // 2, d]:
+            got = sx.materialize_split(f, dim, t)
+            assert np.array_equal(np_(got).view(npdt), exp), (n, t)
+    f = cu(np.array([1, 2, 3], np.uint32))
+    for t in (0, d + 1):
+        with pytest.raises(InvalidArgument):
+            sx.materialize_split(f, dim, t)
+    bad = np.ones(5000, np.uint32)
+    bad[4000], bad[4500] = d + 1, 0
+    with pytest.raises(DomainViolation) as e:
+        sx.materialize_split(cu(bad), dim, 10)
+    assert e.value.row() == 4000 and e.value.value() == d + 1
