@@ -332,40 +332,87 @@ __global__ void __launch_bounds__(kThreads)
 // in the main loop, and the cold reductions fall to the true tail.
 constexpr int kSampleBits = 21;                     // 2M (key, hits) slots = 16 MB
 constexpr uint32_t kHotCap = (kTable * 3) / 4;      // hot keys per table (load 0.75)
+constexpr int kBands = 8;                           // sample-hit bands, hottest first
+__constant__ uint32_t c_band_lo[kBands] = {4096, 512, 64, 16, 8, 4, 3, 2};
+constexpr int kSampleSlots = 4096;                  // per-CTA pre-aggregation (32 KB)
 
-__global__ void __launch_bounds__(256)
-    k_hist_sample(const uint32_t* __restrict__ fact, uint64_t step, uint32_t nsamp, uint32_t d,
-                  uint2* __restrict__ tab) {
+__device__ __forceinline__ void sample_add(uint2* tab, uint32_t key, uint32_t c) {
   constexpr uint32_t mask = (1u << kSampleBits) - 1u;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nsamp; i += gridDim.x * blockDim.x) {
-    const uint32_t key = __ldg(fact + (uint64_t)i * step);
-    if (key - 1u >= d) continue;  // violations are reported by the counting pass
-    uint32_t h = (key * 0x9E3779B1u) >> (32 - kSampleBits);
-    for (int p = 0; p < 64; ++p, h = (h + 1) & mask) {
-      uint32_t k = tab[h].x;
-      if (k == 0u) {
-        k = atomicCAS(&tab[h].x, 0u, key);
-        if (k == 0u) k = key;
-      }
-      if (k == key) {
-        atomicAdd(&tab[h].y, 1u);
-        break;
-      }
+  uint32_t h = (key * 0x9E3779B1u) >> (32 - kSampleBits);
+  for (int p = 0; p < 64; ++p, h = (h + 1) & mask) {
+    uint32_t k = tab[h].x;
+    if (k == 0u) {
+      k = atomicCAS(&tab[h].x, 0u, key);
+      if (k == 0u) k = key;
+    }
+    if (k == key) {
+      atomicAdd(&tab[h].y, c);
+      return;
     }
   }
 }
 
-// Appends the keys sampled at least `min_hits` times (and, when hi_hits > 0,
-// fewer than hi_hits) to hot[0, cap).
+// Each CTA counts its share of the strided sample in shared memory first (a
+// Zipf top key alone is ~22% of the samples: one global atomic per CTA
+// instead of ~230K on one address), then merges its entries.
+__global__ void __launch_bounds__(512)
+    k_hist_sample(const uint32_t* __restrict__ fact, uint64_t step, uint32_t nsamp, uint32_t d,
+                  uint2* __restrict__ tab) {
+  __shared__ uint32_t s_key[kSampleSlots], s_cnt[kSampleSlots];
+  for (int i = threadIdx.x; i < kSampleSlots; i += blockDim.x) s_key[i] = 0u, s_cnt[i] = 0u;
+  __syncthreads();
+  const uint32_t per = (nsamp + gridDim.x - 1) / gridDim.x;
+  const uint32_t b = blockIdx.x * per, e = min(nsamp, b + per);
+  for (uint32_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+    const uint32_t key = __ldg(fact + (uint64_t)i * step);
+    if (key - 1u >= d) continue;  // violations are reported by the counting pass
+    uint32_t h = (key * 0x9E3779B1u) >> (32 - 12);
+    bool done = false;
+    for (int p = 0; p < 8 && !done; ++p, h = (h + 1) & (kSampleSlots - 1)) {
+      uint32_t k = s_key[h];
+      if (k == 0u) {
+        k = atomicCAS(&s_key[h], 0u, key);
+        if (k == 0u) k = key;
+      }
+      if (k == key) {
+        atomicAdd(&s_cnt[h], 1u);
+        done = true;
+      }
+    }
+    if (!done) sample_add(tab, key, 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kSampleSlots; i += blockDim.x)
+    if (s_cnt[i]) sample_add(tab, s_key[i], s_cnt[i]);
+}
+
+// One pass over the sample table: keys hit >= 2 times go to the list of their
+// hit band (warp-aggregated cursor atomics); the seeded kernel takes bands in
+// order, so a full hot set never drops a key hotter than one it holds.
 __global__ void __launch_bounds__(256)
-    k_hist_pick(const uint2* __restrict__ tab, uint32_t min_hits, uint32_t hi_hits,
-                uint32_t* __restrict__ hot, unsigned int* nhot, uint32_t cap) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < (1u << kSampleBits);
-       i += gridDim.x * blockDim.x) {
+    k_hist_pick(const uint2* __restrict__ tab, uint32_t* __restrict__ band_keys,
+                unsigned int* __restrict__ band_n) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t total = 1u << kSampleBits;  // a multiple of 32: warp-uniform trips
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const uint2 e = tab[i];
-    if (e.x != 0u && e.y >= min_hits && (hi_hits == 0u || e.y < hi_hits)) {
-      const unsigned int at = atomicAdd(nhot, 1u);
-      if (at < cap) hot[at] = e.x;
+    int band = kBands;
+    if (e.x != 0u)
+#pragma unroll
+      for (int q = kBands - 1; q >= 0; --q)
+        if (e.y >= c_band_lo[q]) band = q;
+#pragma unroll
+    for (int q = 0; q < kBands; ++q) {
+      const uint32_t m = __ballot_sync(0xffffffffu, band == q);
+      if (!m) continue;
+      unsigned int at = 0;
+      const int first = __ffs(m) - 1;
+      if (lane == first) at = atomicAdd(&band_n[q], (unsigned int)__popc(m));
+      at = __shfl_sync(0xffffffffu, at, first);
+      if (band == q) {
+        const unsigned int pos = at + __popc(m & lanemask_lt());
+        if (pos < kHotCap) band_keys[q * kHotCap + pos] = e.x;
+      }
     }
   }
 }
@@ -374,18 +421,29 @@ template <typename CT>
 __global__ void __launch_bounds__(kThreads)
     k_histogram_seeded(const uint32_t* __restrict__ fact, uint64_t head, uint64_t nvec, uint64_t n,
                        uint32_t d, CT* __restrict__ counts, DevErr* err,
-                       const uint32_t* __restrict__ hot, const unsigned int* nhot_p) {
+                       const uint32_t* __restrict__ band_keys, const unsigned int* band_n) {
   extern __shared__ __align__(16) uint32_t smem_tab[];
   uint32_t* keys = smem_tab;
   uint32_t* cnts = smem_tab + kTable;
+  __shared__ uint32_t s_bstart[kBands + 1];
   for (int i = threadIdx.x; i < kTable; i += kThreads) {
     keys[i] = 0u;
     cnts[i] = 0u;
   }
+  if (threadIdx.x == 0) {  // bands concatenated hottest first, capped at kHotCap keys
+    uint32_t acc = 0;
+    for (int q = 0; q < kBands; ++q) {
+      s_bstart[q] = acc;
+      acc = min(kHotCap, acc + min(band_n[q], kHotCap));
+    }
+    s_bstart[kBands] = acc;
+  }
   __syncthreads();
-  const uint32_t nh = min(*nhot_p, kHotCap);
+  const uint32_t nh = s_bstart[kBands];
   for (uint32_t i = threadIdx.x; i < nh; i += kThreads) {  // fill once; read-only afterwards
-    const uint32_t key = __ldg(hot + i);
+    int q = 0;
+    while (i >= s_bstart[q + 1]) ++q;
+    const uint32_t key = __ldg(band_keys + q * kHotCap + (i - s_bstart[q]));
     if (atomicCAS(&keys[slot_hash(key)], 0u, key) != 0u) atomicCAS(&keys[slot_hash2(key)], 0u, key);
   }
   __syncthreads();
@@ -593,31 +651,26 @@ int histogram_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64_t n
     ctx->launches += 3;
   } else if (SKX_HIST_SAMPLED && n >= (uint64_t(1) << 22) && d > (uint32_t)kTable) {
     // sampled hot set: ~2^20 rows (strided over the whole column) counted
-    // into an L2-resident table, keys hit >= 3 times first, then >= 2
+    // into an L2-resident table, banded by hits (>= 2) hottest first
     const uint32_t nsamp = (uint32_t)std::min<uint64_t>(n / 16, uint64_t(1) << 20);
     const uint64_t step = n / nsamp;
     const size_t tab_b = (size_t(1) << kSampleBits) * 8;
-    char* sp = static_cast<char*>(scratch(ctx, 0, tab_b + 256 + (size_t)kHotCap * 4, s));
+    const size_t band_b = (size_t)kBands * kHotCap * 4;
+    char* sp = static_cast<char*>(scratch(ctx, 0, tab_b + 256 + band_b, s));
     if (!sp) return set_error(ctx, SKX_CUDA_ERROR, "histogram: out of device memory");
     uint2* tab = reinterpret_cast<uint2*>(sp);
-    unsigned int* nhot = reinterpret_cast<unsigned int*>(sp + tab_b);
-    uint32_t* hot = reinterpret_cast<uint32_t*>(sp + tab_b + 256);
+    unsigned int* band_n = reinterpret_cast<unsigned int*>(sp + tab_b);
+    uint32_t* band_keys = reinterpret_cast<uint32_t*>(sp + tab_b + 256);
     cudaError_t e = cudaMemsetAsync(sp, 0, tab_b + 256, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "histogram memset");
-    k_hist_sample<<<grid_for(ctx, nsamp, 256, 8), 256, 0, s>>>(fact, step, nsamp, d, tab);
-    // hottest first: bands of sample hits [lo, hi), so a full hot set never
-    // leaves out a key hotter than one it holds (a top key counted by global
-    // reductions would serialise on one address)
-    const unsigned pick_grid = grid_for(ctx, size_t(1) << kSampleBits, 256, 8);
-    const uint32_t bands[] = {0, 4096, 512, 64, 16, 8, 4, 3, 2};
-    for (int b = 1; b < (int)(sizeof bands / sizeof bands[0]); ++b)
-      k_hist_pick<<<pick_grid, 256, 0, s>>>(tab, bands[b], bands[b - 1], hot, nhot, kHotCap);
-    ctx->launches += (sizeof bands / sizeof bands[0]) - 3;
+    k_hist_sample<<<ctx->num_sms, 512, 0, s>>>(fact, step, nsamp, d, tab);
+    k_hist_pick<<<grid_for(ctx, size_t(1) << kSampleBits, 256, 8), 256, 0, s>>>(tab, band_keys,
+                                                                                band_n);
     cudaFuncSetAttribute(k_histogram_seeded<CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     k_histogram_seeded<CT><<<grid, kThreads, smem, s>>>(fact, head, nvec, n, d, counts, ctx->err,
-                                                        hot, nhot);
-    ctx->launches += 4;
+                                                        band_keys, band_n);
+    ctx->launches += 3;
   } else {
     cudaFuncSetAttribute(k_histogram<CT, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
