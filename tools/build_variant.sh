@@ -8,9 +8,10 @@ root=$(cd "$(dirname "$0")/.." && pwd)
 out=$root/tools/variants
 obj=$out/obj_$name
 mkdir -p "$obj"
-for s in "$root"/paper_1910_10063_b200/csrc/*.cu; do
+src=${SKX_VARIANT_SRC:-$root/paper_1910_10063_b200/csrc}  # e.g. a copy holding an older kernel
+for s in "$src"/*.cu; do
   nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -std=c++17 -Xcompiler -fPIC \
-       -I"$root/include" "$@" -c "$s" -o "$obj/$(basename "${s%.cu}").o" &
+       -I"$root/include" -I"$src" "$@" -c "$s" -o "$obj/$(basename "${s%.cu}").o" &
 done
 wait
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$out/libskx_$name.so" "$obj"/*.o \
