@@ -44,6 +44,9 @@ namespace {
 #ifndef SKX_HIST_SAMPLED
 #define SKX_HIST_SAMPLED 1  // direct counters: sampled read-only hot set (k_histogram_seeded)
 #endif
+#ifndef SKX_HIST_TOPREG
+#define SKX_HIST_TOPREG 0  // sampled path: count the hottest key in a register (A/B)
+#endif
 #ifndef SKX_HIST_CTAS
 #define SKX_HIST_CTAS 3
 #endif
@@ -396,6 +399,11 @@ __global__ void __launch_bounds__(256)
   const uint32_t total = 1u << kSampleBits;  // a multiple of 32: warp-uniform trips
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const uint2 e = tab[i];
+#if SKX_HIST_TOPREG
+    if (e.y >= c_band_lo[0])  // the most-sampled key, (hits << 32 | key) in band_n[8..9]
+      atomicMax(reinterpret_cast<unsigned long long*>(band_n + kBands),
+                ((unsigned long long)e.y << 32) | e.x);
+#endif
     int band = kBands;
     if (e.x != 0u)
 #pragma unroll
@@ -440,6 +448,11 @@ __global__ void __launch_bounds__(kThreads)
   }
   __syncthreads();
   const uint32_t nh = s_bstart[kBands];
+#if SKX_HIST_TOPREG
+  // the hottest key (~22% of C4's rows) counts in a register, not a shared slot
+  const uint32_t top = (uint32_t)*reinterpret_cast<const unsigned long long*>(band_n + kBands);
+  uint32_t topc = 0;
+#endif
   for (uint32_t i = threadIdx.x; i < nh; i += kThreads) {  // fill once; read-only afterwards
     int q = 0;
     while (i >= s_bstart[q + 1]) ++q;
@@ -448,6 +461,12 @@ __global__ void __launch_bounds__(kThreads)
   }
   __syncthreads();
   auto count = [&](uint32_t key) {  // key already domain-checked
+#if SKX_HIST_TOPREG
+    if (key == top) {
+      ++topc;
+      return;
+    }
+#endif
     const uint32_t h1 = slot_hash(key), h2 = slot_hash2(key);
     const uint32_t k1 = keys[h1], k2 = keys[h2];
     if (k1 == key)
@@ -494,6 +513,10 @@ __global__ void __launch_bounds__(kThreads)
         record_violation(err, k, id);
     }
   }
+#if SKX_HIST_TOPREG
+  for (int o = 16; o > 0; o >>= 1) topc += __shfl_down_sync(0xffffffffu, topc, o);
+  if ((threadIdx.x & 31) == 0 && topc) global_add<CT>(counts, top - 1u, topc);
+#endif
   __syncthreads();
   for (int i = threadIdx.x; i < kTable; i += kThreads) {
     const uint32_t k = keys[i];
