@@ -30,7 +30,10 @@
  *    operators on different streams never share scratch.  Arenas grow
  *    stream-ordered (cudaMallocAsync / cudaFreeAsync on the operator's
  *    stream), so no operator synchronises the device; skx_reserve() grows
- *    them up front.  Callers own every input and output buffer.
+ *    them up front -- required before capturing operators into a CUDA Graph
+ *    (an arena cannot grow during capture: the operator returns
+ *    SKX_CUDA_ERROR "out of device memory").  Callers own every input and
+ *    output buffer.
  *  - Host-buffer entry points (suffix _host) copy host -> device, run the
  *    kernel and copy back, pipelined in chunks over two streams; they are
  *    synchronous and report errors directly.

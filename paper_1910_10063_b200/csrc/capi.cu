@@ -28,6 +28,13 @@ int cuda_fail(skx_ctx* ctx, cudaError_t e, const char* where) {
 // queued on s, the new one is valid for everything enqueued on s afterwards.
 static void* grow(Scratch& sc, size_t bytes, cudaStream_t s) {
   if (sc.bytes >= bytes && sc.ptr) return sc.ptr;
+  // Inside a CUDA Graph capture an allocation would belong to the graph, not
+  // to the context: scratch must be reserved (skx_reserve) before capturing.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return nullptr;
+  }
   if (sc.ptr) {
     cudaFreeAsync(sc.ptr, s);
     sc.ptr = nullptr;
@@ -52,10 +59,11 @@ static ScratchSet* set_for(skx_ctx* ctx, cudaStream_t s) {
       st.stream = s;
       return &st;
     }
-  // More streams than sets: recycle the least recently added set once its
-  // stream has drained (rare; callers normally use one or two streams).
+  // More streams than sets: recycle the least recently added set (rare;
+  // callers normally use one or two streams).  Its stream may already be
+  // destroyed, so drain the whole device before freeing its arenas.
   ScratchSet* victim = &ctx->sets[0];
-  cudaStreamSynchronize(victim->stream);
+  cudaDeviceSynchronize();
   for (auto& sc : victim->slot) {
     if (sc.ptr) cudaFree(sc.ptr);
     sc = Scratch{};

@@ -45,7 +45,7 @@ namespace {
 #define SKX_HIST_SAMPLED 1  // direct counters: sampled read-only hot set (k_histogram_seeded)
 #endif
 #ifndef SKX_HIST_TOPREG
-#define SKX_HIST_TOPREG 0  // sampled path: count the hottest key in a register (A/B)
+#define SKX_HIST_TOPREG 1  // sampled path: the hottest key counts in a register
 #endif
 #ifndef SKX_HIST_CTAS
 #define SKX_HIST_CTAS 3

@@ -51,12 +51,6 @@ constexpr uint32_t kCap = 64;                  // compacted entries kept per sli
 #ifndef SKX_SEL_P1_PREF
 #define SKX_SEL_P1_PREF 0   // pass 1: next slice's FKs in flight while probing
 #endif
-#ifndef SKX_SEL_COMPACT
-// C5 records stored densely for the selected keys only, in rank order (record
-// of key idx at prefix[idx / 64] + popcount of the bits below it): four useful
-// records per 128-byte line instead of ~0.4
-#define SKX_SEL_COMPACT 1
-#endif
 #ifndef SKX_SEL_PER
 #define SKX_SEL_PER 4
 #endif
@@ -81,8 +75,7 @@ struct Cols {
   uint16_t* out_flag;
   double* sums;
   uint32_t n_categories;
-  const uint4* rec;          // [nsel][2]: {cat, price, supp lo, supp hi}, {flag, 0, 0, 0}
-  const uint4* wp;           // [nwords]: {bitmap word lo, hi, selected keys before it, 0}
+  const uint4* rec;          // [d][2]: {cat, price, supp lo, supp hi}, {flag, 0, 0, 0}
   struct SumCtl* ctl;
   unsigned int* acc96;       // [n_categories][4]: lo, mid, hi, pad
   unsigned long long cap;    // output rows the caller's buffers hold
@@ -107,38 +100,6 @@ __device__ __forceinline__ bool fixed_ok(const SumCtl* c, uint32_t ncat, int& S)
   return true;
 }
 
-// Compact record index of a selected key: selected keys before it, from the
-// word-level prefix and the bits below it in its 64-bit word (an 8 MB table:
-// L2-resident, unlike the 1 GiB sparse record table it replaces).
-__device__ __forceinline__ uint32_t rec_index(const uint4* wp, uint32_t idx) {
-#if SKX_SEL_COMPACT
-  const uint4 w = __ldg(wp + (idx >> 6));
-  const unsigned long long word = (unsigned long long)w.x | ((unsigned long long)w.y << 32);
-  return w.z + (uint32_t)__popcll(word & ((1ull << (idx & 63)) - 1ull));
-#else
-  (void)wp;
-  return idx;
-#endif
-}
-
-__global__ void __launch_bounds__(256)
-    k_word_popc(const unsigned long long* __restrict__ words, uint64_t nwords,
-                uint32_t* __restrict__ cnt) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += stride)
-    cnt[w] = (uint32_t)__popcll(__ldg(words + w));
-}
-
-__global__ void __launch_bounds__(256)
-    k_word_prefix(const unsigned long long* __restrict__ words, uint64_t nwords,
-                  const uint32_t* __restrict__ prefix, uint4* __restrict__ wp) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += stride) {
-    const unsigned long long x = __ldg(words + w);
-    wp[w] = make_uint4((uint32_t)x, (uint32_t)(x >> 32), __ldg(prefix + w), 0u);
-  }
-}
-
 // C5 prologue: interleave the four dimension columns into 32-byte records
 // and record the price exponent range -- for the SELECTED keys only: pass 2
 // reads the record of a selected row's key and nothing else, and only
@@ -147,19 +108,18 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     k_pack_records(const int32_t* __restrict__ cat, const float* __restrict__ price,
                    const unsigned long long* __restrict__ supp, const uint16_t* __restrict__ flag,
-                   const unsigned long long* __restrict__ words, const uint4* __restrict__ wp,
-                   uint32_t d, uint4* __restrict__ rec, SumCtl* ctl) {
+                   const unsigned long long* __restrict__ words, uint32_t d,
+                   uint4* __restrict__ rec, SumCtl* ctl) {
   unsigned int emax = 0, eneg = 0, nf = 0;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d; i += stride) {
     if (!((__ldg(words + (i >> 6)) >> (i & 63)) & 1ull)) continue;
     const float p = __ldcs(price + i);
     const unsigned long long sp = __ldcs(supp + i);
-    const uint64_t ri = rec_index(wp, (uint32_t)i);
-    rec[2 * ri] = make_uint4((uint32_t)__ldcs(cat + i), __float_as_uint(p), (uint32_t)sp,
-                             (uint32_t)(sp >> 32));
-    rec[2 * ri + 1] = make_uint4((uint32_t)__ldcs(reinterpret_cast<const unsigned short*>(flag) + i),
-                                 0u, 0u, 0u);
+    rec[2 * i] = make_uint4((uint32_t)__ldcs(cat + i), __float_as_uint(p), (uint32_t)sp,
+                            (uint32_t)(sp >> 32));
+    rec[2 * i + 1] = make_uint4((uint32_t)__ldcs(reinterpret_cast<const unsigned short*>(flag) + i),
+                                0u, 0u, 0u);
     if (!isfinite(p)) {
       nf = 1;
     } else if (p != 0.f) {
@@ -520,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, SKX_SEL_P2_MINB)
         const uint32_t ja = j0 + lane;
         const uint2 ea = ja < cnt ? __ldcs(src + ja) : make_uint2(0u, 0u);
         Rec8 ra{};
-        if (FUSED && ja < cnt) ra = load_rec(cols.rec, rec_index(cols.wp, ea.x));
+        if (FUSED && ja < cnt) ra = load_rec(cols.rec, ea.x);
         if (ja < cnt) emit_row<FUSED>(ob + ja, ea.y, ra, base_off, out_off, cols, fixed, S, s_acc);
       }
       return;
@@ -547,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, SKX_SEL_P2_MINB)
       for (int j = 0; j < 4; ++j) {
         if ((sel[i] >> j) & 1u) {
           Rec8 r{};
-          if (FUSED) r = load_rec(cols.rec, rec_index(cols.wp, fk[i][j] - 1u));
+          if (FUSED) r = load_rec(cols.rec, fk[i][j] - 1u);
           emit_row<FUSED>(ob + pos, row_l + i * 128 + j, r, base_off, out_off, cols, fixed, S,
                           s_acc);
           ++pos;
@@ -601,7 +561,7 @@ __global__ void __launch_bounds__(kThreads, SKX_SEL_P2_MINB)
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
         r[u] = Rec8{};
-        if (FUSED && j0 + u * 32 + lane < T) r[u] = load_rec(cols.rec, rec_index(cols.wp, e[u].x));
+        if (FUSED && j0 + u * 32 + lane < T) r[u] = load_rec(cols.rec, e[u].x);
       }
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
@@ -788,10 +748,7 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
   const uint64_t base_b = (ent_b + nslices * 8 + 256 + 255) & ~uint64_t(255);
   const uint64_t acc_b = fused ? (((uint64_t)cols.n_categories * 16 + 255) & ~uint64_t(255)) : 0;
   const uint64_t rec_b = fused ? bits * 32 : 0;
-  const uint64_t nwords = (bits + 63) / 64;
-  const uint64_t wp_b = fused ? ((nwords * 20 + 255) & ~uint64_t(255)) : 0;  // wp + u32 prefix
-  char* raw = static_cast<char*>(
-      scratch(ctx, 2, base_b + (fused ? 256 : 0) + acc_b + rec_b + wp_b, s));
+  char* raw = static_cast<char*>(scratch(ctx, 2, base_b + (fused ? 256 : 0) + acc_b + rec_b, s));
   if (!raw) return set_error(ctx, SKX_CUDA_ERROR, "select: out of device memory");
   uint2* entries = reinterpret_cast<uint2*>(raw);
   uint32_t* counts = reinterpret_cast<uint32_t*>(raw + ent_b);
@@ -801,7 +758,6 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
     cols.ctl = reinterpret_cast<SumCtl*>(raw + base_b);
     cols.acc96 = reinterpret_cast<unsigned int*>(raw + base_b + 256);
     cols.rec = reinterpret_cast<const uint4*>(raw + base_b + 256 + acc_b);
-    cols.wp = reinterpret_cast<const uint4*>(raw + base_b + 256 + acc_b + rec_b);
     ScratchSet* ss = scratch_set(ctx, s);
     ss->sel_acc = cols.acc96;
     ss->sel_ctl = cols.ctl;
@@ -809,19 +765,9 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
     e = cudaMemsetAsync(raw + base_b, 0, 256 + acc_b, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "select memset");
     if (bits) {
-      const auto* w64 = reinterpret_cast<const unsigned long long*>(words);
-#if SKX_SEL_COMPACT
-      // word popcounts -> exclusive prefix -> {word, prefix} table
-      uint32_t* pre = reinterpret_cast<uint32_t*>(raw + base_b + 256 + acc_b + rec_b + nwords * 16);
-      k_word_popc<<<grid_for(ctx, nwords, 256, 8), 256, 0, s>>>(w64, nwords, pre);
-      int rc0 = launch_exclusive_scan_u32(ctx, pre, pre, nwords, nullptr, 3, s);
-      if (rc0) return rc0;
-      k_word_prefix<<<grid_for(ctx, nwords, 256, 8), 256, 0, s>>>(w64, nwords, pre,
-                                                                  const_cast<uint4*>(cols.wp));
-      ctx->launches += 2;
-#endif
       k_pack_records<<<grid_for(ctx, bits, 256, 8), 256, 0, s>>>(
-          cols.cat, cols.price, cols.supp, cols.flag, w64, cols.wp, (uint32_t)bits,
+          cols.cat, cols.price, cols.supp, cols.flag,
+          reinterpret_cast<const unsigned long long*>(words), (uint32_t)bits,
           const_cast<uint4*>(cols.rec), cols.ctl);
       ctx->launches++;
     }
@@ -902,7 +848,7 @@ int skx_select_gather_sum(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const 
     return skx::set_error(ctx, SKX_INVALID_ARGUMENT, "select_gather_sum: null column pointer");
   skx::Cols cols{cat, price, reinterpret_cast<const unsigned long long*>(supp), flag,
                  out_cat, out_price, reinterpret_cast<unsigned long long*>(out_supp), out_flag,
-                 sums, n_categories, nullptr, nullptr, nullptr, nullptr, capacity};
+                 sums, n_categories, nullptr, nullptr, nullptr, capacity};
   return skx::select_impl(ctx, true, fact, n, words, d, base, out_off, cols, count_dev,
                           skx::as_stream(stream));
 }

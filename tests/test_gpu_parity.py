@@ -627,3 +627,44 @@ def test_materialize_split_two_pass(sx, oracle, dtype, npdt):
     with pytest.raises(DomainViolation) as e:
         sx.materialize_split(cu(bad), dim, 10)
     assert e.value.row() == 4000 and e.value.value() == d + 1
+
+
+def test_scratch_reserve_and_graph_capture(sx, oracle):
+    """Scratch arenas are per stream and grow stream-ordered; skx_reserve grows
+    them up front, which is what lets a scratch-using operator (the index
+    build's sort) be captured in a CUDA Graph and replayed."""
+    import ctypes as C
+    ctx = sx.context(0)
+    d, n = 1 << 16, 1 << 20
+    rng = np.random.default_rng(8)
+    fact_np = rng.integers(1, d + 1, size=n, dtype=np.uint32)
+    fact = cu(fact_np)
+    counts = sx.histogram_u32(fact, d)
+    off = torch.empty(d, dtype=torch.uint32, device="cuda")
+    rk = torch.empty_like(off)
+    s = torch.cuda.Stream()
+    sp = C.c_void_p(s.cuda_stream)
+
+    def build():
+        ctx.check(ctx.lib.skx_build_index_u32(ctx.handle, C.c_void_p(counts.data_ptr()), d, n,
+                                              C.c_void_p(off.data_ptr()), C.c_void_p(rk.data_ptr()),
+                                              sp))
+    # a fresh stream has no arenas: growing one inside a capture is refused
+    g = torch.cuda.CUDAGraph()
+    with pytest.raises(Exception):
+        with torch.cuda.graph(g, stream=s):
+            build()
+    # reserve on that stream, then capture and replay
+    ctx.check(ctx.lib.skx_reserve(ctx.handle, -1, 64 << 20, sp))
+    got = (C.c_uint64 * 4)()
+    ctx.check(ctx.lib.skx_scratch_bytes(ctx.handle, sp, got))
+    assert min(got) >= 64 << 20
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        build()
+    off.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    ctx.sync(sp)
+    eo, er = oracle.build_index(oracle.count_frequencies(fact_np, d), n)
+    assert np.array_equal(np_(off), eo) and np.array_equal(np_(rk), er)
