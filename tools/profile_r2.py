@@ -23,9 +23,9 @@ ops = a.ops.split(",")
 ctx = sx.context(0)
 work = {}
 if "gather_c2" in ops or "gather_c2_rand" in ops:
-    w = ds.C2
-    g = ds.make_gather_dataset(w.d, w.n, a.z, w.seed, torch.int64)
-    out = torch.empty(w.n, dtype=torch.int64, device="cuda")
+    w2 = ds.C2
+    g = ds.make_gather_dataset(w2.d, w2.n, a.z, w2.seed, torch.int64)
+    out = torch.empty(w2.n, dtype=torch.int64, device="cuda")
     work["gather_c2"] = lambda: sx.materialize(g.fact_freq, g.dim_freq, out=out, sync=False)
     work["gather_c2_rand"] = lambda: sx.materialize(g.fact_rand, g.dim_rand, out=out, sync=False)
 if "gather_c1" in ops:
@@ -33,21 +33,21 @@ if "gather_c1" in ops:
     o1 = torch.empty(ds.C1.n, dtype=torch.int32, device="cuda")
     work["gather_c1"] = lambda: sx.materialize(c1.g.fact_freq, c1.price_freq, out=o1, sync=False)
 if "groupby_c3" in ops:
-    w = ds.C3
-    gd = ds.make_groupby_dataset(w.d, w.n, w.z, w.seed)
-    c3 = torch.empty(w.d, dtype=torch.uint64, device="cuda")
-    s3 = torch.empty(w.d, dtype=torch.uint64, device="cuda")
-    work["groupby_c3"] = lambda: sx.aggregate_count_sum(gd.fact_freq, gd.qty, w.d, counts=c3,
+    w3 = ds.C3  # (each op binds its own workload: the closures run after all are built)
+    gd = ds.make_groupby_dataset(w3.d, w3.n, w3.z, w3.seed)
+    c3 = torch.empty(w3.d, dtype=torch.uint64, device="cuda")
+    s3 = torch.empty(w3.d, dtype=torch.uint64, device="cuda")
+    work["groupby_c3"] = lambda: sx.aggregate_count_sum(gd.fact_freq, gd.qty, w3.d, counts=c3,
                                                         sums=s3, sync=False)
 if "index_c4" in ops:
-    w = ds.C4
+    w4 = ds.C4
     ib = ds.make_index_build_dataset()
-    h4 = torch.empty(w.d, dtype=torch.uint32, device="cuda")
+    h4 = torch.empty(w4.d, dtype=torch.uint32, device="cuda")
     f4 = torch.empty_like(ib.fact)
 
     def c4():
-        sx.histogram_u32(ib.fact, w.d, h4, sync=False)
-        idx = sx.build_index(sx.FrequencyProfile(h4, w.n), sync=False)
+        sx.histogram_u32(ib.fact, w4.d, h4, sync=False)
+        idx = sx.build_index(sx.FrequencyProfile(h4, w4.n), sync=False)
         sx.recode_fact(ib.fact, idx, out=f4, sync=False)
         sx.permute_dimension(ib.dim_i, idx, sync=False)
         sx.permute_dimension(ib.dim_f, idx, sync=False)
