@@ -1,8 +1,8 @@
-# ncu --set full with source counters for the group-by and the sampled histogram; exports the
-# raw page and the SASS-level source page (per-instruction stall samples) as CSV.
+# ncu --set full with source counters for the group-by and the C4 index build; exports the raw
+# page and the SASS-level source pages (per-instruction stall samples) as CSV.
 python tools/profile_r2.py --ops groupby_c3,index_c4 > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none --profile-from-start off \
-    -k regex:"k_aggregate|k_histogram_seeded" -o /tmp/src_prof python tools/profile_r2.py --ops groupby_c3,index_c4 > gpurun_out/src_prof.log 2>&1
+    -o /tmp/src_prof python tools/profile_r2.py --ops groupby_c3,index_c4 > gpurun_out/src_prof.log 2>&1
 ncu -i /tmp/src_prof.ncu-rep --page raw --csv > gpurun_out/src_prof_raw.csv
 ncu -i /tmp/src_prof.ncu-rep --page source --csv --print-source sass -k regex:"k_aggregate<8" > gpurun_out/src_agg_sass.csv 2>&1
 ncu -i /tmp/src_prof.ncu-rep --page source --csv --print-source sass -k regex:"k_histogram_seeded" > gpurun_out/src_hist_sass.csv 2>&1
