@@ -699,6 +699,7 @@ int skx_aggregate(skx_ctx* ctx, const uint32_t* fact, const void* measure, int m
                   uint64_t n, uint32_t d, uint32_t hot_threshold, uint64_t* counts, uint64_t* sums,
                   void* stream) {
   if (!ctx) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   return skx::launch_aggregate(ctx, fact, measure, measure_width, n, d, hot_threshold, counts,
                                sums, skx::as_stream(stream));
 }
@@ -706,6 +707,7 @@ int skx_aggregate(skx_ctx* ctx, const uint32_t* fact, const void* measure, int m
 int skx_heavy_hitter_count(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint32_t d, uint32_t k,
                            uint64_t* counts, void* stream) {
   if (!ctx) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   if (k == 0) return skx::set_error(ctx, SKX_INVALID_ARGUMENT, "heavy_hitter_count: k must be at least 1");
   cudaStream_t s = skx::as_stream(stream);
   const uint32_t cutoff = k < d ? k : d;

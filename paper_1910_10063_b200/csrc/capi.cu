@@ -215,6 +215,7 @@ int skx_set_gather_policy(skx_ctx* ctx, int policy) {
 
 int skx_set_gather_tiers(skx_ctx* ctx, uint64_t smem_bytes, uint64_t l1_bytes, double l2_fraction) {
   if (!ctx || !(l2_fraction >= 0.0 && l2_fraction <= 1.0)) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   ctx->tier_smem_bytes = smem_bytes;
   ctx->tier_l1_bytes = l1_bytes;
   ctx->tier_l2_frac = l2_fraction;
@@ -223,12 +224,14 @@ int skx_set_gather_tiers(skx_ctx* ctx, uint64_t smem_bytes, uint64_t l1_bytes, d
 
 int skx_set_histogram_mode(skx_ctx* ctx, int mode) {
   if (!ctx || mode < 0 || mode > 2) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   ctx->hist_mode = mode;
   return SKX_OK;
 }
 
 int skx_set_aggregate_mode(skx_ctx* ctx, int mode) {
   if (!ctx || mode < 0 || mode > 2) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   ctx->agg_mode = mode;
   return SKX_OK;
 }
@@ -266,6 +269,7 @@ int skx_last_error(const skx_ctx* ctx, skx_error_info* info) {
 
 int skx_sync(skx_ctx* ctx, void* stream) {
   if (!ctx) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   cudaStream_t s = as_stream(stream);
   cudaError_t e = cudaMemcpyAsync(ctx->err_host, ctx->err, sizeof(DevErr), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -380,6 +384,7 @@ int skx_random_bijection_host(uint32_t n, uint64_t seed, uint32_t* map) {
 int skx_materialize_host(skx_ctx* ctx, int w, const uint32_t* fact, uint64_t n, const void* dim,
                          uint64_t dim_len, void* out) {
   if (!ctx) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   if (w != 2 && w != 4 && w != 8) return set_error(ctx, SKX_INVALID_ARGUMENT, "bad value width");
   cudaSetDevice(ctx->device);
   const uint64_t chunk = uint64_t(1) << 25;  // rows per pipeline stage
@@ -427,6 +432,7 @@ int skx_materialize_host(skx_ctx* ctx, int w, const uint32_t* fact, uint64_t n, 
 int skx_aggregate_host(skx_ctx* ctx, const uint32_t* fact, const void* measure, int mw, uint64_t n,
                        uint32_t d, uint32_t hot, uint64_t* counts, uint64_t* sums) {
   if (!ctx) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   if (mw != 0 && mw != 4 && mw != 8) return set_error(ctx, SKX_INVALID_ARGUMENT, "bad measure width");
   cudaSetDevice(ctx->device);
   void* d_fact = host_scratch_dev(ctx, 1, n * 4 + 16, ctx->hstream[0]);
@@ -507,6 +513,7 @@ int skx_pinned_alloc(skx_ctx* ctx, uint64_t bytes, void** ptr) {
 
 int skx_pinned_free(skx_ctx* ctx, void* ptr) {
   if (!ctx) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   if (!ptr) return SKX_OK;
   cudaError_t e = cudaFreeHost(ptr);
   return e == cudaSuccess ? SKX_OK : cuda_fail(ctx, e, "pinned_free");
@@ -514,6 +521,7 @@ int skx_pinned_free(skx_ctx* ctx, void* ptr) {
 
 void* skx_ctx_stream(skx_ctx* ctx, int slot) {
   if (!ctx || slot < 0 || slot > 1) return nullptr;
+  skx::bind(ctx);
   return ctx->hstream[slot];
 }
 
@@ -538,6 +546,7 @@ int skx_copy_to_host_async(skx_ctx* ctx, void* dst, const void* src, uint64_t by
 int skx_find_domain_violation(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint64_t d,
                               uint64_t* row_out) {
   if (!ctx || !row_out) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   *row_out = ~0ull;
   if (n == 0) return SKX_OK;
   if (n > (uint64_t(1) << 34)) return set_error(ctx, SKX_INVALID_ARGUMENT, "more than 2^34 rows");

@@ -79,6 +79,7 @@ extern "C" {
 int skx_groupby_pack(skx_ctx* ctx, const uint64_t* counts, const uint64_t* sums, uint32_t d,
                      uint32_t hot, uint64_t* buf, uint64_t* guard, void* stream) {
   if (!ctx) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   if (!counts || !buf || !guard || hot > d)
     return skx::set_error(ctx, SKX_INVALID_ARGUMENT, "groupby_pack: bad arguments");
   cudaStream_t s = skx::as_stream(stream);
@@ -97,6 +98,7 @@ int skx_groupby_pack(skx_ctx* ctx, const uint64_t* counts, const uint64_t* sums,
 int skx_groupby_unpack(skx_ctx* ctx, const uint64_t* buf, uint32_t d, uint32_t hot,
                        uint64_t* counts, uint64_t* sums, void* stream) {
   if (!ctx) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   if (!buf || hot > d) return skx::set_error(ctx, SKX_INVALID_ARGUMENT, "groupby_unpack: bad arguments");
   if (d == 0) return SKX_OK;
   cudaStream_t s = skx::as_stream(stream);

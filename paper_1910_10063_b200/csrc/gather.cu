@@ -564,12 +564,14 @@ int skx_recode_fact(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uint32
 int skx_gather_split_u32(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uint32_t* dim,
                          uint64_t dim_len, uint32_t threshold, uint32_t* out, void* stream) {
   if (!ctx) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   return skx::gather_split_impl<uint32_t>(ctx, fact, n, dim, dim_len, threshold, out,
                                           skx::as_stream(stream));
 }
 int skx_gather_split_u64(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uint64_t* dim,
                          uint64_t dim_len, uint32_t threshold, uint64_t* out, void* stream) {
   if (!ctx) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   return skx::gather_split_impl<uint64_t>(ctx, fact, n, dim, dim_len, threshold, out,
                                           skx::as_stream(stream));
 }

@@ -735,6 +735,7 @@ extern "C" {
 int skx_count_frequencies(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint32_t d,
                           uint64_t* counts, void* stream) {
   if (!ctx) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   cudaStream_t s = skx::as_stream(stream);
   if (d > 0) {
     cudaError_t e = cudaMemsetAsync(counts, 0, uint64_t(d) * 8, s);
@@ -746,6 +747,7 @@ int skx_count_frequencies(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint32
 int skx_histogram_u32(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint32_t d,
                       uint32_t* counts, int accumulate, void* stream) {
   if (!ctx) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   cudaStream_t s = skx::as_stream(stream);
   if (!accumulate && d > 0) {
     cudaError_t e = cudaMemsetAsync(counts, 0, uint64_t(d) * 4, s);

@@ -452,18 +452,21 @@ extern "C" {
 int skx_build_index(skx_ctx* ctx, const uint64_t* counts, uint32_t d, uint64_t total,
                     uint32_t* offsets, uint32_t* ranks, void* stream) {
   if (!ctx) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   return skx::launch_build_index(ctx, counts, 8, d, total, offsets, ranks, skx::as_stream(stream));
 }
 
 int skx_build_index_u32(skx_ctx* ctx, const uint32_t* counts, uint32_t d, uint64_t total,
                         uint32_t* offsets, uint32_t* ranks, void* stream) {
   if (!ctx) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   return skx::launch_build_index(ctx, counts, 4, d, total, offsets, ranks, skx::as_stream(stream));
 }
 
 int skx_rebuild(skx_ctx* ctx, const uint32_t* fact, uint64_t n, uint32_t d, uint32_t* offsets,
                 uint32_t* ranks, void* stream) {
   if (!ctx) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   if (d > SKX_MAX_DOMAIN_CARDINALITY)
     return skx::set_error(ctx, SKX_INVALID_ARGUMENT, "domain cardinality exceeds the 32-bit identifier space");
   cudaStream_t s = skx::as_stream(stream);

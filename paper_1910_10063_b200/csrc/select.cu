@@ -830,6 +830,7 @@ int skx_select_offsets(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uin
                        uint64_t bits, uint32_t base, uint32_t* out, uint64_t* count_dev,
                        void* stream) {
   if (!ctx) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   skx::Cols cols{};
   cols.cap = n;  // KernelTable::select_offsets contract: out holds n entries
   return skx::select_impl(ctx, false, fact, n, words, bits, base, out, cols, count_dev,
@@ -843,6 +844,7 @@ int skx_select_gather_sum(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const 
                           int32_t* out_cat, float* out_price, uint64_t* out_supp,
                           uint16_t* out_flag, double* sums, uint64_t* count_dev, void* stream) {
   if (!ctx) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   if (n && (!cat || !price || !supp || !flag || !out_cat || !out_price || !out_supp || !out_flag ||
             (n_categories && !sums)))
     return skx::set_error(ctx, SKX_INVALID_ARGUMENT, "select_gather_sum: null column pointer");
@@ -855,6 +857,7 @@ int skx_select_gather_sum(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const 
 
 int skx_select_sum_partials(skx_ctx* ctx, uint32_t n_categories, int64_t* out, void* stream) {
   if (!ctx || !out) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   cudaStream_t s = skx::as_stream(stream);
   skx::ScratchSet* ss = skx::scratch_set(ctx, s);
   if (!ss->sel_acc || ss->sel_ncat != n_categories)
@@ -872,6 +875,7 @@ int skx_select_sum_partials(skx_ctx* ctx, uint32_t n_categories, int64_t* out, v
 int skx_select_sums_from_partials(skx_ctx* ctx, const int64_t* partials, uint32_t n_categories,
                                   uint32_t nranks, double* sums, void* stream) {
   if (!ctx || !partials || !sums || nranks == 0) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   if (n_categories == 0) return SKX_OK;
   skx::k_sums_from_partials<<<(n_categories + 255) / 256, 256, 0, skx::as_stream(stream)>>>(
       reinterpret_cast<const long long*>(partials), n_categories, nranks, sums);
@@ -883,6 +887,7 @@ int skx_select_sums_from_partials(skx_ctx* ctx, const int64_t* partials, uint32_
 int skx_permute_bitmap(skx_ctx* ctx, const uint64_t* words, uint64_t bits, const uint32_t* offsets,
                        uint32_t d, uint64_t* out_words, void* stream) {
   if (!ctx) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   if (bits != d)
     return skx::set_error(ctx, SKX_INVALID_ARGUMENT, "bitmap size does not match index cardinality");
   if (bits == 0) return SKX_OK;
@@ -899,6 +904,7 @@ int skx_permute_bitmap(skx_ctx* ctx, const uint64_t* words, uint64_t bits, const
 int skx_build_bitmap_lt_i32(skx_ctx* ctx, const int32_t* dim, uint64_t d, int32_t threshold,
                             uint64_t* out_words, void* stream) {
   if (!ctx) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
   if (d == 0) return SKX_OK;
   cudaStream_t s = skx::as_stream(stream);
   const uint64_t nwords = (d + 63) / 64;

@@ -193,6 +193,14 @@ ScratchSet* scratch_set(skx_ctx* ctx, cudaStream_t s);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Makes the context's device current for the calling thread (an entry point
+// may be called from a thread whose current device is another one, e.g. the
+// C++ drop-in's multi-device overloads).
+inline void bind(const skx_ctx* c) {
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur != c->device) cudaSetDevice(c->device);
+}
+
 #define SKX_CHECK_LAUNCH(ctx, where)                              \
   do {                                                            \
     cudaError_t e_ = cudaGetLastError();                          \
