@@ -9,7 +9,7 @@ rtol 1e-6 (the fp64 category sums, north_star's tolerance).
 
 Sizes verified:
   C2  D=2^27, N=2^30, s in {0.5, 1.0, 1.5}: histogram, index, recode, permuted
-      int64 dim, gather in both layouts
+      int64 dim, gather in both layouts (and the two-pass split gather at s=1.0)
   C3  D=2^24, N=2^30, s=1.0 (far tier active): COUNT + SUM(int64 qty) in every
       tail mode, COUNT only, heavy hitters
   C4  D=2^26, N=2^30, s=1.25: u32 histogram, index, recode, int32 + float32
@@ -109,6 +109,10 @@ def test_c2_gather_at_scale(env, oracle, z):
     out.fill_(0)
     sx.materialize(g.fact_rand, g.dim_rand, out=out)  # original layout
     assert same(out, exp)
+    if z == 1.0:  # the threshold-split two-pass gather (materialize_split) at full size
+        out.fill_(0)
+        sx.materialize_split(g.fact_freq, g.dim_freq, 1 << 23, out=out)
+        assert same(out, exp)
     del g, out, exp, fact, dim, counts, off, rk
     free()
 
