@@ -273,3 +273,53 @@ def test_shard_for_matches_chunk_spans():
         for r in range(w):
             s = sdist.shard_for(n, r, w)
             assert (s.begin, s.end) == spans[r]
+
+
+def _worker_small(rank, world, port, n, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1910_10063_b200 import dist as sdist
+    from paper_1910_10063_b200.errors import DomainViolation
+    o = Oracle()
+    ex = OracleExecutor()
+    coll = sdist.default_collectives()
+    d = 7
+    full = (np.arange(n, dtype=np.uint32) * 5) % d + 1
+    shard = sdist.shard_for(n)
+    fact = torch.from_numpy(full[shard.begin:shard.end].copy())
+    (off, rk), _ = sdist.rebuild(fact, d, n, ex, coll, shard)
+    meas = torch.ones(shard.rows, dtype=torch.int64)
+    c, s = sdist.aggregate(fact, meas, d, ex, coll, shard, hot=2)
+    # violations in two shards: the smaller global row wins on every rank
+    bad = fact.clone()
+    if shard.rows and rank in (1, world - 1):
+        bad[0] = 0 if rank == 1 else d + 1
+    try:
+        sdist.rebuild(bad, d, n, ex, coll, shard)
+        raised = -1
+    except DomainViolation as e:
+        raised = e.row()
+    np.savez(os.path.join(out_dir, f"s{rank}.npz"), off=off.numpy(), c=c.numpy(), s=s.numpy(),
+             raised=np.array([raised]), rows=np.array([shard.rows]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(4, 3), (3, 10)])
+def test_uneven_and_empty_shards(tmp_path, world, n):
+    """chunk_spans shards of unequal length, including empty ones (n < world):
+    the index and the reduced counts equal the whole-column results, and with
+    violations in two shards every rank raises the smaller global row."""
+    mp.spawn(_worker_small, args=(world, _free_port(), n, str(tmp_path)), nprocs=world, join=True)
+    o = Oracle()
+    d = 7
+    full = (np.arange(n, dtype=np.uint32) * 5) % d + 1
+    off, _ = o.rebuild(full, d)
+    c, s = o.aggregate_count_sum(full, np.ones(n, np.uint64), d)
+    r = [np.load(tmp_path / f"s{k}.npz") for k in range(world)]
+    spans = o.chunk_spans(n, world)
+    bad_rows = [spans[k][0] for k in (1, world - 1) if spans[k][1] > spans[k][0]]
+    for k in range(world):
+        assert np.array_equal(r[k]["off"], off)
+        assert int(r[k]["raised"][0]) == (min(bad_rows) if bad_rows else -1)
+    assert np.array_equal(r[0]["c"], c) and np.array_equal(r[0]["s"], s)
+    assert sum(int(x["rows"][0]) for x in r) == n
