@@ -89,13 +89,13 @@ int grouped(skx_comm* c, const char* where, F fn) {
 int make_locals(skx_comm* c, int n, const int* devices) {
   for (int i = 0; i < n; ++i) {
     c->device[i] = devices[i];
+    c->nlocal = i + 1;  // what skx_comm_destroy releases if a later step fails
     int rc = skx_ctx_create(devices[i], &c->ctx[i]);
     if (rc != SKX_OK) return comm_fail(c, rc, "comm_init", "skx_ctx_create failed");
     cudaSetDevice(devices[i]);
     if (cudaStreamCreateWithFlags(&c->stream[i], cudaStreamNonBlocking) != cudaSuccess)
       return comm_fail(c, SKX_CUDA_ERROR, "comm_init", "cudaStreamCreate failed");
   }
-  c->nlocal = n;
   return SKX_OK;
 }
 
