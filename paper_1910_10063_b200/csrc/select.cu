@@ -791,6 +791,7 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
   cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
   k1<<<grid1, kThreads1, smem1, s>>>(fact, n, w32, bits, entries, counts, sw, ctx->err);
   ctx->launches++;
+  SKX_CHECK_LAUNCH(ctx, "select pass 1");
   int rc = launch_exclusive_scan_u32(ctx, counts, offs, nslices, total, 3, s);
   if (rc) return rc;
   const size_t smem = sums_on && cols.n_categories <= kFixedCategories
@@ -804,6 +805,7 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
   k2<<<grid2, kThreads, smem, s>>>(fact, n, w32, bits, entries, counts, offs, base, total, out,
                                    cols, reinterpret_cast<unsigned long long*>(count_dev));
   ctx->launches++;
+  SKX_CHECK_LAUNCH(ctx, "select pass 2");
   if (sums_on) {
     k_sum_finalize<<<(cols.n_categories + 255) / 256, 256, 0, s>>>(cols.acc96, cols.ctl,
                                                                    cols.n_categories, cols.sums);

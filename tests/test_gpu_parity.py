@@ -284,6 +284,46 @@ def test_select_gather_sum_paths(sx, oracle, case):
         assert np.isnan(s).sum() == 1
 
 
+@pytest.mark.parametrize("thr", [100, 1000, 3])
+def test_select_many_tiles(sx, oracle, thr):
+    """2^25 + 12345 rows (thousands of slice groups per CTA, a ragged last
+    slice), sparse / all-selected / nearly empty selections, and a capacity
+    below the selected count (rows past it are counted, not written; the
+    category sums still cover every selected row)."""
+    d, n = 1 << 20, (1 << 25) + 12345
+    rng = np.random.default_rng(thr)
+    cat = rng.integers(0, 1000, size=d, dtype=np.int32)
+    price = np.exp(3 + rng.standard_normal(d)).astype(np.float32)
+    supp = rng.integers(0, 2**63, size=d, dtype=np.uint64)
+    flag = rng.integers(0, 2**16, size=d, dtype=np.uint16)
+    fact = sx.generate_zipf(cu(sx.zipf_cdf(d, 1.0)), n, 17)
+    bm = sx.build_bitmap_lt(cu(cat), thr)
+    f_np = np_(fact)
+    exp_off = oracle.select_offsets(f_np, np_(bm.words), d, base=9)
+    assert np.array_equal(np_(sx.select(fact, bm, base=9)), exp_off)
+    got = sx.select_gather_sum(fact, bm, cu(cat), cu(price), cu(supp), cu(flag), 1000, base=9)
+    exp = oracle.select_gather_sum(f_np, np_(bm.words), cat, price, supp, flag, 1000, base=9)
+    for g, e in zip(got[:5], exp[:5]):
+        assert np.array_equal(np_(g), e)
+    assert np.allclose(np_(got[5]), exp[5], rtol=1e-6, atol=0)
+    if thr == 100:  # truncated output: the first `cap` rows written, the count exact
+        cap = len(exp_off) // 3
+        out = (torch.empty(cap, dtype=torch.uint32, device="cuda"),
+               torch.empty(cap, dtype=torch.int32, device="cuda"),
+               torch.empty(cap, dtype=torch.float32, device="cuda"),
+               torch.empty(cap, dtype=torch.uint64, device="cuda"),
+               torch.empty(cap, dtype=torch.uint16, device="cuda"),
+               torch.empty(1000, dtype=torch.float64, device="cuda"),
+               torch.zeros(1, dtype=torch.uint64, device="cuda"))
+        sx.select_gather_sum(fact, bm, cu(cat), cu(price), cu(supp), cu(flag), 1000, base=9,
+                             out=out, sync=False)
+        sx.context(0).sync()
+        assert int(out[6].item()) == len(exp_off)
+        for g, e in zip(out[:5], exp[:5]):
+            assert np.array_equal(np_(g), e[:cap])
+        assert np.allclose(np_(out[5]), exp[5], rtol=1e-6, atol=0)  # sums cover every row
+
+
 def test_reorder_invariants_at_scale(sx):
     """Size-independent properties at 2^26 rows: gather equality across
     layouts, rank-space counts map back through offsets, multiset of counts
@@ -514,7 +554,7 @@ def test_aggregate_tier_edges(sx, oracle, d, n, hot):
     assert np.array_equal(np_(c), oracle.aggregate_count_sum(np_(fact), None, d)[0])
 
 
-@pytest.mark.parametrize("n", [1, 255, 256, 257, 4097])
+@pytest.mark.parametrize("n", [1, 255, 256, 257, 4097, 8191, 8192, 8193, 3 * 8192 + 5])
 def test_select_tiny_and_slice_edges(sx, oracle, n):
     """Row counts around the 256-row slice and 4-row vector boundaries."""
     d = 1000

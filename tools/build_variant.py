@@ -18,7 +18,7 @@ B._run([B._nvcc(), *B.NVCC_FLAGS, *defs, "-c", os.path.join(B.CSRC, src), "-o", 
 objs = [o for o in sorted(glob.glob(os.path.join(B.OBJ, "*.o")))
         if os.path.basename(o) != os.path.basename(src)[:-3] + ".o"] + [obj]
 so = os.path.join(out_dir, f"libskx_{name}.so")
-B._run([B._nvcc(), *B.ARCH, "-shared", "-o", so, *objs, "-lcudart_static", "-lrt", "-lpthread",
-        "-ldl"])
+B._run([B._nvcc(), *B.ARCH, "-shared", "-o", so, *objs, "-lcudart_static", "-lnccl", "-lrt",
+        "-lpthread", "-ldl"])
 os.remove(obj)
 print(so)
