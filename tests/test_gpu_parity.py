@@ -415,11 +415,14 @@ def test_aggregate_large_domain_modes(sx, oracle, mode, z):
 
 
 @pytest.mark.parametrize("case", ["big_measure", "count_wrap", "sum_carry", "mixed",
-                                  "far_count_wrap", "far_sum_carry", "far_ok"])
+                                  "far_count_wrap", "far_sum_carry", "far_ok", "hot_lo_wrap",
+                                  "hot_wide"])
 def test_aggregate_packed_tail_fallback(sx, oracle, case):
-    """The packed tail (count << 40 | sum) must detect every overflow on the
-    device and redo the call exactly: measures >= 2^16, a cold key with
-    >= 2^24 rows (count field wraps), a cold key whose sum reaches 2^40."""
+    """The packed mode must detect every overflow on the device and redo the
+    call exactly: measures >= 2^16, a cold key with >= 2^24 rows (count field
+    wraps), a cold key whose sum reaches 2^40 -- and hot keys whose 32-bit
+    sum-lo bins wrap within a CTA or take measures >= 2^32 (carried to the
+    global sums)."""
     d, hot = 1000, 16
     rng = np.random.default_rng(5)
     if case.startswith("far"):
@@ -447,6 +450,15 @@ def test_aggregate_packed_tail_fallback(sx, oracle, case):
         n = (1 << 25) + 2
         fact = np.full(n, 700, np.uint32)
         meas = np.full(n, 65535, np.int64)
+    elif case == "hot_lo_wrap":  # ~28 K rows per CTA of ~2^31 each on hot keys: bins wrap
+        n = (1 << 22) + 9
+        fact = rng.integers(1, 4, size=n, dtype=np.uint32)
+        meas = rng.integers(2**30, 2**31, size=n, dtype=np.int64)
+    elif case == "hot_wide":
+        n = 300_007
+        fact = rng.integers(1, d + 1, size=n, dtype=np.uint32)
+        meas = rng.integers(1, 101, size=n, dtype=np.int64)
+        meas[fact <= hot] = rng.integers(2**32, 2**40, size=int((fact <= hot).sum()))
     else:
         n = 1 << 20
         fact = rng.integers(1, d + 1, size=n, dtype=np.uint32)
