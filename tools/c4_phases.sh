@@ -1,0 +1,4 @@
+# C4 index build: per-phase times of bench.py (for tools/ab.sh A/B runs of library variants)
+python bench.py --steps 10 --warmup 3 --configs c4 --no-cpu --no-e2e 2>/dev/null | python -c "
+import sys,json
+d=json.loads(sys.stdin.read().strip().splitlines()[-1]); g=d.get('index_build_c4',{}); print(g.get('ms_per_build'), g.get('phases_ms'))"
