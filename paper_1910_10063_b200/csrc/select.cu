@@ -10,17 +10,19 @@
 // B200 design: two passes with a device scan
 // between them, no inter-CTA ordering inside a kernel.  Pass 1 streams the
 // FK column once (one 256-bit load of 8 consecutive rows per lane; the bitmap
-// prefix that holds the hot ids of a reordered column sits in shared memory),
-// and every warp places the selected rows of its 256-row slice in row order
-// (one warp scan of the lanes' popcounts) into a private slot of up to 64
-// (dimension index, row) entries plus a count.  The scan turns the slice
-// counts into output offsets.  Pass 2 walks groups of 4 slices: each warp
-// copies their entries (flattened over the lanes) to offset + rank --
+// prefix that holds the hot ids of a reordered column sits in shared memory);
+// each warp owns a contiguous run of 256-row slices and appends their
+// selected rows -- (dimension index, row), in row order (one warp scan of the
+// lanes' popcounts per slice) -- densely to its own region, then writes the
+// region's count.  The scan turns the region counts into output offsets.
+// Pass 2 streams the regions: entry e of a region goes to its offset + e --
 // ascending row order, exactly the reference's chunk-ordered concatenation --
-// so the FK column is read once.  A slice with more than 64 selected rows
-// (dense selections) is re-derived in pass 2 from the FK column and bitmap.
-// (A single-pass decoupled look-back version was measured ~2x slower on
-// B200, profiles/r1_experiments.md.)
+// with 4 entries per lane loaded before their records and stores, so the FK
+// column is read once.  A region whose selected rows overflow its capacity
+// (a quarter of its rows: dense selections) is re-derived in pass 2 from the
+// FK column and the bitmap.  (Single-pass decoupled look-back forms were
+// measured slower on B200: profiles/r1_experiments.md,
+// profiles/r2_experiments.md §11.)
 //
 // The C5 variant first interleaves the four dimension columns into 32-byte
 // records (one 256-bit load and one sector per selected row instead of four
@@ -42,9 +44,6 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kWarpRows = 256;                 // rows per warp slice
 constexpr int kItems = kWarpRows / 128;        // 4 items of 128 rows (4 per lane)
 constexpr uint32_t kCap = 64;                  // compacted entries kept per slice
-#ifndef SKX_SEL_GROUP
-#define SKX_SEL_GROUP 4
-#endif
 #ifndef SKX_SEL_P2_MINB
 #define SKX_SEL_P2_MINB 3   // pass 2 CTAs per SM the registers must allow (80 regs)
 #endif
@@ -54,7 +53,7 @@ constexpr uint32_t kCap = 64;                  // compacted entries kept per sli
 #ifndef SKX_SEL_PER
 #define SKX_SEL_PER 4
 #endif
-constexpr int kGroup = SKX_SEL_GROUP;          // pass 2: slices per warp iteration
+constexpr int kParts = 8;                      // pass 2: work items per pass-1 region
 constexpr int kPer = SKX_SEL_PER;              // pass 2: entries per lane in flight
 constexpr int kThreads1 = 1024;                // pass 1 CTA (shares one bitmap prefix)
 constexpr uint32_t kSmemCategories = 2048;     // fp64 fallback: 8 warps x 2048 x 8 B
@@ -248,12 +247,15 @@ __device__ __forceinline__ void load_rows8(const uint32_t* p, bool v8, uint32_t 
 }
 
 // Pass 1, any slice (unaligned column, empty domain): per-item ballots.
+// Appends the slice's selected rows at region[wpos..] (while they fit the
+// region's capacity) and returns the slice's count (warp-uniform).
 template <bool VEC>
-__device__ __forceinline__ void count_slice_generic(const uint32_t* __restrict__ fact, uint64_t n,
-                                                 uint64_t sl, const uint32_t* __restrict__ words32,
-                                                 uint32_t bits32, uint32_t sw, uint32_t s_base,
-                                                 uint2* __restrict__ entries,
-                                                 uint32_t* __restrict__ slice_counts, DevErr* err) {
+__device__ __forceinline__ uint32_t count_slice_generic(const uint32_t* __restrict__ fact,
+                                                        uint64_t n, uint64_t sl,
+                                                        const uint32_t* __restrict__ words32,
+                                                        uint32_t bits32, uint32_t sw,
+                                                        uint32_t s_base, uint2* __restrict__ region,
+                                                        uint64_t wpos, uint64_t capw, DevErr* err) {
   const int lane = threadIdx.x & 31;
   const uint32_t lt = lanemask_lt();
   const uint64_t row0 = sl * kWarpRows;
@@ -265,7 +267,6 @@ __device__ __forceinline__ void count_slice_generic(const uint32_t* __restrict__
     probe_slice<true>(fk, row0, n, bits32, sw, s_base, words32, lane, err, sel);
   else
     probe_slice<false>(fk, row0, n, bits32, sw, s_base, words32, lane, err, sel);
-  uint2* out = entries + sl * kCap;
   const uint32_t row_l = (uint32_t)row0 + 4u * lane;  // n < 2^32
   uint32_t run = 0;
 #pragma unroll
@@ -274,29 +275,32 @@ __device__ __forceinline__ void count_slice_generic(const uint32_t* __restrict__
 #pragma unroll
     for (int j = 0; j < 4; ++j) b[j] = __ballot_sync(0xffffffffu, (sel[i] >> j) & 1u);
     if (sel[i]) {
-      uint32_t pos = run + item_base(b, lt);
+      uint64_t pos = wpos + run + item_base(b, lt);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         if ((sel[i] >> j) & 1u) {
-          if (pos < kCap) out[pos] = make_uint2(fk[i][j] - 1u, row_l + i * 128 + j);
+          if (pos < capw) region[pos] = make_uint2(fk[i][j] - 1u, row_l + i * 128 + j);
           ++pos;
         }
       }
     }
     run += item_count(b);
   }
-  if (lane == 0) slice_counts[sl] = run;
+  return run;
 }
 
-// Pass 1: probe every row once; each warp compacts its slice's selected rows
-// (dimension index, row) in row order into entries[slice][kCap] and writes
-// the slice count.
+// Pass 1: probe every row once.  Global warp g owns the contiguous slices
+// [g * spw, (g + 1) * spw) and appends their selected rows -- (dimension
+// index, row), in row order -- densely to its region entries[g * spw * kCap ..]
+// (capacity spw * kCap, a quarter of its rows), then writes its count.  Row
+// order across regions is warp order, so an exclusive scan of the counts
+// gives every region's output offset, and pass 2 streams each region.
 template <bool VEC, bool FAST>
 __global__ void __launch_bounds__(kThreads1, 1)
     k_select_count(const uint32_t* __restrict__ fact, uint64_t n,
                    const uint32_t* __restrict__ words32, uint64_t bits,
-                   uint2* __restrict__ entries, uint32_t* __restrict__ slice_counts, uint32_t sw,
-                   DevErr* err) {
+                   uint2* __restrict__ entries, uint32_t* __restrict__ warp_counts, uint64_t spw,
+                   uint32_t sw, DevErr* err) {
   extern __shared__ __align__(16) uint32_t s_words[];  // bitmap prefix [sw]
   const int lane = threadIdx.x & 31;
   const uint64_t nslices = (n + kWarpRows - 1) / kWarpRows;
@@ -306,12 +310,17 @@ __global__ void __launch_bounds__(kThreads1, 1)
   __syncthreads();
   const uint32_t maxw = bits32 ? (bits32 - 1u) >> 5 : 0u;
   const bool v8 = (reinterpret_cast<uintptr_t>(fact) & 31u) == 0;
-  const uint64_t warps = (uint64_t)gridDim.x * (kThreads1 / 32);
-  const uint64_t first = (uint64_t)blockIdx.x * (kThreads1 / 32) + (threadIdx.x >> 5);
+  const uint64_t gw = (uint64_t)blockIdx.x * (kThreads1 / 32) + (threadIdx.x >> 5);
+  const uint64_t s_begin = gw * spw < nslices ? gw * spw : nslices;
+  const uint64_t s_end = s_begin + spw < nslices ? s_begin + spw : nslices;
+  uint2* region = entries + gw * spw * kCap;
+  const uint64_t capw = spw * kCap;
+  uint64_t wpos = 0;  // warp-uniform: selected rows of the slices done so far
   if constexpr (!FAST) {
-    for (uint64_t sl = first; sl < nslices; sl += warps)
-      count_slice_generic<VEC>(fact, n, sl, words32, bits32, sw, s_base, entries, slice_counts,
-                               err);
+    for (uint64_t sl = s_begin; sl < s_end; ++sl)
+      wpos += count_slice_generic<VEC>(fact, n, sl, words32, bits32, sw, s_base, region, wpos,
+                                       capw, err);
+    if (lane == 0) warp_counts[gw] = (uint32_t)wpos;  // < 2^32: n < 2^32
     return;
   }
   // Fast path: lane l owns the 8 consecutive rows row0 + 8l + j, so the
@@ -342,12 +351,12 @@ __global__ void __launch_bounds__(kThreads1, 1)
     return live;
   };
   uint32_t fk[8];
-  uint32_t live = load8(first, fk);
-  for (uint64_t sl = first; sl < nslices; sl += warps) {
+  uint32_t live = s_begin < s_end ? load8(s_begin, fk) : 0u;
+  for (uint64_t sl = s_begin; sl < s_end; ++sl) {
     const uint64_t row0 = sl * kWarpRows;
 #if SKX_SEL_P1_PREF
     uint32_t fkn[8];
-    const uint32_t liven = load8(sl + warps, fkn);
+    const uint32_t liven = load8(sl + 1 < s_end ? sl + 1 : nslices, fkn);
 #endif
     uint32_t sel = 0;
     bool bad = false;
@@ -374,9 +383,9 @@ __global__ void __launch_bounds__(kThreads1, 1)
     }
     const uint32_t row_l = (uint32_t)row0 + 8u * lane;  // n < 2^32
     if (sel) {
-      uint32_t pos = incl - c;
-      uint2* o = entries + sl * kCap + pos;
-      if (incl <= kCap) {  // all of this lane's rows fit: predicated stores only
+      uint64_t pos = wpos + incl - c;
+      uint2* o = region + pos;
+      if (wpos + incl <= capw) {  // all of this lane's rows fit: predicated stores only
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           if ((sel >> j) & 1u) *o++ = make_uint2(fk[j] - 1u, row_l + j);
@@ -384,20 +393,21 @@ __global__ void __launch_bounds__(kThreads1, 1)
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           if ((sel >> j) & 1u) {
-            if (pos < kCap) *o = make_uint2(fk[j] - 1u, row_l + j);
+            if (pos < capw) *o = make_uint2(fk[j] - 1u, row_l + j);
             ++o, ++pos;
           }
       }
     }
-    if (lane == 31) slice_counts[sl] = incl;
+    wpos += __shfl_sync(0xffffffffu, incl, 31);
 #if SKX_SEL_P1_PREF
 #pragma unroll
     for (int j = 0; j < 8; ++j) fk[j] = fkn[j];
     live = liven;
 #else
-    live = load8(sl + warps, fk);
+    live = load8(sl + 1 < s_end ? sl + 1 : nslices, fk);
 #endif
   }
+  if (lane == 0) warp_counts[gw] = (uint32_t)wpos;  // < 2^32: n < 2^32
 }
 
 struct Rec8 {
@@ -440,19 +450,22 @@ __device__ __forceinline__ void emit_row(uint64_t p, uint32_t row, const Rec8& r
   }
 }
 
-// Pass 2: every warp takes groups of slices; a slice's selected rows go to
-// slice_off[slice] + rank.  Slices with <= kCap rows copy pass 1's entries
-// (a group's entries flattened over the lanes, kPer rows per lane in flight);
-// denser slices are re-derived from the FK column and the bitmap (global
-// probes).
+// Pass 2: streams the regions of pass 1 (each split into kParts work items for
+// balance): a region's entries are the selected rows of a contiguous run of
+// slices, already dense and in row order, so entry e goes to region_off + e.  kPer entries per lane are loaded
+// (coalesced) before their records (C5) and before any store, so each warp
+// keeps 32 x kPer independent record loads in flight.  A region whose rows
+// overflowed its capacity (dense selections) is re-derived from the FK column
+// and the bitmap, slice by slice.
 template <bool FUSED, bool VEC>
 __global__ void __launch_bounds__(kThreads, SKX_SEL_P2_MINB)
-    k_select_write(const uint32_t* __restrict__ fact, uint64_t n,
-                   const uint32_t* __restrict__ words32, uint64_t bits,
-                   const uint2* __restrict__ entries, const uint32_t* __restrict__ slice_counts,
-                   const uint32_t* __restrict__ slice_off, uint32_t base_off,
-                   const uint32_t* __restrict__ total, uint32_t* __restrict__ out_off, Cols cols,
-                   unsigned long long* __restrict__ count_dev) {
+    k_select_emit(const uint32_t* __restrict__ fact, uint64_t n,
+                  const uint32_t* __restrict__ words32, uint64_t bits,
+                  const uint2* __restrict__ entries, const uint32_t* __restrict__ warp_counts,
+                  const uint32_t* __restrict__ warp_off, uint64_t nregions, uint64_t spw,
+                  uint32_t base_off, const uint32_t* __restrict__ total,
+                  uint32_t* __restrict__ out_off, Cols cols,
+                  unsigned long long* __restrict__ count_dev) {
   extern __shared__ __align__(16) unsigned int s_acc[];  // [3][ncat] (fixed-point sums)
   const int lane = threadIdx.x & 31;
   if (blockIdx.x == 0 && threadIdx.x == 0) *count_dev = *total;
@@ -470,103 +483,73 @@ __global__ void __launch_bounds__(kThreads, SKX_SEL_P2_MINB)
   const uint64_t nslices = (n + kWarpRows - 1) / kWarpRows;
   const uint32_t bits32 = bits < 0xFFFFFFFFull ? (uint32_t)bits : 0xFFFFFFFFu;
   const uint32_t lt = lanemask_lt();
+  const uint64_t capw = spw * kCap;
   const uint64_t warps = (uint64_t)gridDim.x * kWarps;
-  // One slice at a time: its entries, or (dense) a re-derivation from the FK
-  // column and the bitmap.
-  auto write_slice = [&](uint64_t sl, uint32_t cnt, uint64_t ob) {
-    if (cnt <= kCap) {
-      const uint2* src = entries + sl * kCap;
-      for (uint32_t j0 = 0; j0 < cnt; j0 += 32) {
-        const uint32_t ja = j0 + lane;
-        const uint2 ea = ja < cnt ? __ldcs(src + ja) : make_uint2(0u, 0u);
-        Rec8 ra{};
-        if (FUSED && ja < cnt) ra = load_rec(cols.rec, ea.x);
-        if (ja < cnt) emit_row<FUSED>(ob + ja, ea.y, ra, base_off, out_off, cols, fixed, S, s_acc);
-      }
-      return;
-    }
-    const uint64_t row0 = sl * kWarpRows;
-    const bool full = row0 + kWarpRows <= n;
-    uint32_t fk[kItems][4];
-    load_slice<VEC>(fact, n, row0, full, lane, fk);
-    uint32_t sel[kItems];
-    // domain already checked in pass 1 (err = nullptr)
-    if (full)
-      probe_slice<true>(fk, row0, n, bits32, 0u, 0u, words32, lane, nullptr, sel);
-    else
-      probe_slice<false>(fk, row0, n, bits32, 0u, 0u, words32, lane, nullptr, sel);
-    const uint32_t row_l = (uint32_t)row0 + 4u * lane;
-    uint32_t run = 0;
+  // work item = (region, part): a region's entries split into kParts even runs
+  const uint64_t items = nregions * kParts;
+  for (uint64_t it = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); it < items; it += warps) {
+    const uint64_t r = it / kParts;
+    const uint32_t part = (uint32_t)(it % kParts);
+    const uint32_t cnt = __ldg(warp_counts + r);
+    const uint64_t ob = __ldg(warp_off + r);
+    if (cnt <= capw) {
+      const uint2* src = entries + r * capw;
+      const uint32_t e_end = (uint32_t)((uint64_t)cnt * (part + 1) / kParts);
+      for (uint32_t j0 = (uint32_t)((uint64_t)cnt * part / kParts); j0 < e_end; j0 += 32 * kPer) {
+        uint2 e[kPer];
+        Rec8 rc[kPer];
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-      uint32_t b[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = __ballot_sync(0xffffffffu, (sel[i] >> j) & 1u);
-      uint32_t pos = run + item_base(b, lt);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if ((sel[i] >> j) & 1u) {
-          Rec8 r{};
-          if (FUSED) r = load_rec(cols.rec, fk[i][j] - 1u);
-          emit_row<FUSED>(ob + pos, row_l + i * 128 + j, r, base_off, out_off, cols, fixed, S,
-                          s_acc);
-          ++pos;
+        for (int u = 0; u < kPer; ++u) {
+          const uint32_t f = j0 + u * 32 + lane;
+          e[u] = f < e_end ? __ldcs(src + f) : make_uint2(0u, 0u);
         }
-      }
-      run += item_count(b);
-    }
-  };
-  // Warps take groups of kGroup consecutive slices.  Their outputs are one
-  // contiguous run (slice offsets are the exclusive scan of the counts), so
-  // the group's entries are flattened over the lanes: up to kPer entries per
-  // lane with all entry and record loads in flight before any store -- a
-  // slice alone holds ~20 selected rows at C5's selectivity, too few to hide
-  // the count -> entries -> record latency chain.
-  const uint64_t ngroups = (nslices + kGroup - 1) / kGroup;
-  for (uint64_t g = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); g < ngroups; g += warps) {
-    const uint64_t sl0 = g * kGroup;
-    const uint32_t ns = (uint32_t)(nslices - sl0 < (uint64_t)kGroup ? nslices - sl0 : kGroup);
-    const uint32_t c_l = (uint32_t)lane < ns ? __ldg(slice_counts + sl0 + lane) : 0u;
-    const uint64_t ob0 = __ldg(slice_off + sl0);
-    if (__any_sync(0xffffffffu, c_l > kCap)) {  // a dense slice: one slice at a time
-      for (uint32_t s2 = 0; s2 < ns; ++s2) {
-        const uint32_t c = __shfl_sync(0xffffffffu, c_l, (int)s2);
-        write_slice(sl0 + s2, c, s2 ? (uint64_t)__ldg(slice_off + sl0 + s2) : ob0);
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          rc[u] = Rec8{};
+          if (FUSED && j0 + u * 32 + lane < e_end) rc[u] = load_rec(cols.rec, e[u].x);
+        }
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          const uint32_t f = j0 + u * 32 + lane;
+          if (f < e_end)
+            emit_row<FUSED>(ob + f, e[u].y, rc[u], base_off, out_off, cols, fixed, S, s_acc);
+        }
       }
       continue;
     }
-    uint32_t pre[kGroup];  // warp-uniform inclusive prefix of the counts
-    uint32_t acc = 0;
+    if (part != 0) continue;  // an overflowed region is re-derived by its first item
+    // overflowed region: every slice re-derived (domain already checked in pass 1)
+    const uint64_t s_begin = r * spw < nslices ? r * spw : nslices;
+    const uint64_t s_end = s_begin + spw < nslices ? s_begin + spw : nslices;
+    uint64_t run = 0;
+    for (uint64_t sl = s_begin; sl < s_end; ++sl) {
+      const uint64_t row0 = sl * kWarpRows;
+      const bool full = row0 + kWarpRows <= n;
+      uint32_t fk[kItems][4];
+      load_slice<VEC>(fact, n, row0, full, lane, fk);
+      uint32_t sel[kItems];
+      if (full)
+        probe_slice<true>(fk, row0, n, bits32, 0u, 0u, words32, lane, nullptr, sel);
+      else
+        probe_slice<false>(fk, row0, n, bits32, 0u, 0u, words32, lane, nullptr, sel);
+      const uint32_t row_l = (uint32_t)row0 + 4u * lane;
 #pragma unroll
-    for (int s2 = 0; s2 < kGroup; ++s2) {
-      acc += __shfl_sync(0xffffffffu, c_l, s2);
-      pre[s2] = acc;
-    }
-    const uint32_t T = pre[kGroup - 1];
-    for (uint32_t j0 = 0; j0 < T; j0 += 32 * kPer) {
-      uint2 e[kPer];
-      Rec8 r[kPer];
+      for (int i = 0; i < kItems; ++i) {
+        uint32_t b[4];
 #pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const uint32_t f = j0 + u * 32 + lane;
-        e[u] = make_uint2(0u, 0u);
-        if (f < T) {
-          uint32_t s2 = 0, pb = 0;
+        for (int j = 0; j < 4; ++j) b[j] = __ballot_sync(0xffffffffu, (sel[i] >> j) & 1u);
+        uint64_t pos = run + item_base(b, lt);
 #pragma unroll
-          for (int q = 0; q < kGroup - 1; ++q)
-            if (f >= pre[q]) s2 = q + 1, pb = pre[q];
-          e[u] = __ldcs(entries + (sl0 + s2) * kCap + (f - pb));
+        for (int j = 0; j < 4; ++j) {
+          if ((sel[i] >> j) & 1u) {
+            Rec8 rr{};
+            if (FUSED) rr = load_rec(cols.rec, fk[i][j] - 1u);
+            emit_row<FUSED>(ob + pos, row_l + i * 128 + j, rr, base_off, out_off, cols, fixed, S,
+                            s_acc);
+            ++pos;
+          }
         }
-      }
-#pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        r[u] = Rec8{};
-        if (FUSED && j0 + u * 32 + lane < T) r[u] = load_rec(cols.rec, e[u].x);
-      }
-#pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const uint32_t f = j0 + u * 32 + lane;
-        if (f < T) emit_row<FUSED>(ob0 + f, e[u].y, r[u], base_off, out_off, cols, fixed, S, s_acc);
+        run += item_count(b);
       }
     }
   }
@@ -742,18 +725,24 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
     return e == cudaSuccess ? SKX_OK : cuda_fail(ctx, e, "select memset");
   }
   const uint64_t nslices = (n + kWarpRows - 1) / kWarpRows;
-  // scratch: entries [nslices][kCap] | slice counts | slice offsets | total |
+  // pass 1 grid: one CTA per SM (they share nothing but the bitmap prefix);
+  // global warp g owns the slices [g * spw, (g + 1) * spw)
+  const uint64_t cta1 = (nslices + kThreads1 / 32 - 1) / (kThreads1 / 32);
+  const unsigned grid1 = (unsigned)(cta1 < (uint64_t)ctx->num_sms ? cta1 : ctx->num_sms);
+  const uint64_t nregions = (uint64_t)grid1 * (kThreads1 / 32);
+  const uint64_t spw = (nslices + nregions - 1) / nregions;
+  // scratch: entries [nregions][spw * kCap] | region counts | region offsets | total |
   //          (fused) SumCtl 256 B | acc96 [ncat][4] | records [d][32 B]
-  const uint64_t ent_b = nslices * kCap * 8;
-  const uint64_t base_b = (ent_b + nslices * 8 + 256 + 255) & ~uint64_t(255);
+  const uint64_t ent_b = nregions * spw * kCap * 8;
+  const uint64_t base_b = (ent_b + nregions * 8 + 256 + 255) & ~uint64_t(255);
   const uint64_t acc_b = fused ? (((uint64_t)cols.n_categories * 16 + 255) & ~uint64_t(255)) : 0;
   const uint64_t rec_b = fused ? bits * 32 : 0;
   char* raw = static_cast<char*>(scratch(ctx, 2, base_b + (fused ? 256 : 0) + acc_b + rec_b, s));
   if (!raw) return set_error(ctx, SKX_CUDA_ERROR, "select: out of device memory");
   uint2* entries = reinterpret_cast<uint2*>(raw);
   uint32_t* counts = reinterpret_cast<uint32_t*>(raw + ent_b);
-  uint32_t* offs = counts + nslices;
-  uint32_t* total = offs + nslices;
+  uint32_t* offs = counts + nregions;
+  uint32_t* total = offs + nregions;
   if (fused) {
     cols.ctl = reinterpret_cast<SumCtl*>(raw + base_b);
     cols.acc96 = reinterpret_cast<unsigned int*>(raw + base_b + 256);
@@ -784,26 +773,25 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
   if (sbytes > ctx->smem_optin - 1024) sbytes = ctx->smem_optin - 1024;
   const uint32_t sw = (uint32_t)(nw32 < sbytes / 4 ? nw32 : sbytes / 4);
   const size_t smem1 = (size_t)sw * 4;
-  const uint64_t cta1 = (nslices + kThreads1 / 32 - 1) / (kThreads1 / 32);
-  const unsigned grid1 = (unsigned)(cta1 < (uint64_t)ctx->num_sms ? cta1 : ctx->num_sms);
   auto k1 = vec ? (bits ? k_select_count<true, true> : k_select_count<true, false>)
                 : k_select_count<false, false>;
   cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
-  k1<<<grid1, kThreads1, smem1, s>>>(fact, n, w32, bits, entries, counts, sw, ctx->err);
+  k1<<<grid1, kThreads1, smem1, s>>>(fact, n, w32, bits, entries, counts, spw, sw, ctx->err);
   ctx->launches++;
   SKX_CHECK_LAUNCH(ctx, "select pass 1");
-  int rc = launch_exclusive_scan_u32(ctx, counts, offs, nslices, total, 3, s);
+  int rc = launch_exclusive_scan_u32(ctx, counts, offs, nregions, total, 3, s);
   if (rc) return rc;
   const size_t smem = sums_on && cols.n_categories <= kFixedCategories
                           ? (size_t)cols.n_categories * 12 : 0;
-  auto k2 = fused ? (vec ? k_select_write<true, true> : k_select_write<true, false>)
-                  : (vec ? k_select_write<false, true> : k_select_write<false, false>);
+  auto k2 = fused ? (vec ? k_select_emit<true, true> : k_select_emit<true, false>)
+                  : (vec ? k_select_emit<false, true> : k_select_emit<false, false>);
   cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2, kThreads, smem);
-  const unsigned grid2 = grid_for(ctx, (nslices + kWarps - 1) / kWarps, 1, per_sm < 1 ? 1 : per_sm);
-  k2<<<grid2, kThreads, smem, s>>>(fact, n, w32, bits, entries, counts, offs, base, total, out,
-                                   cols, reinterpret_cast<unsigned long long*>(count_dev));
+  const unsigned grid2 = grid_for(ctx, (nregions + kWarps - 1) / kWarps, 1, per_sm < 1 ? 1 : per_sm);
+  k2<<<grid2, kThreads, smem, s>>>(fact, n, w32, bits, entries, counts, offs, nregions, spw, base,
+                                   total, out, cols,
+                                   reinterpret_cast<unsigned long long*>(count_dev));
   ctx->launches++;
   SKX_CHECK_LAUNCH(ctx, "select pass 2");
   if (sums_on) {
