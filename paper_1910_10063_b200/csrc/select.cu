@@ -45,13 +45,13 @@ constexpr int kWarpRows = 256;                 // rows per warp slice
 constexpr int kItems = kWarpRows / 128;        // 4 items of 128 rows (4 per lane)
 constexpr uint32_t kCap = 64;                  // compacted entries kept per slice
 #ifndef SKX_SEL_P2_MINB
-#define SKX_SEL_P2_MINB 3   // pass 2 CTAs per SM the registers must allow (80 regs)
+#define SKX_SEL_P2_MINB 2   // pass 2 CTAs per SM the registers must allow
 #endif
 #ifndef SKX_SEL_P1_PREF
 #define SKX_SEL_P1_PREF 0   // pass 1: next slice's FKs in flight while probing
 #endif
 #ifndef SKX_SEL_PER
-#define SKX_SEL_PER 4
+#define SKX_SEL_PER 8
 #endif
 constexpr int kParts = 8;                      // pass 2: work items per pass-1 region
 constexpr int kPer = SKX_SEL_PER;              // pass 2: entries per lane in flight
@@ -74,7 +74,8 @@ struct Cols {
   uint16_t* out_flag;
   double* sums;
   uint32_t n_categories;
-  const uint4* rec;          // [d][2]: {cat, price, supp lo, supp hi}, {flag, 0, 0, 0}
+  const uint4* rec;          // [selected keys][2]: {cat, price, supp lo, supp hi}, {flag, 0, 0, 0}
+  const uint2* dir;          // rank directory of the bitmap: key -> dense record index
   struct SumCtl* ctl;
   unsigned int* acc96;       // [n_categories][4]: lo, mid, hi, pad
   unsigned long long cap;    // output rows the caller's buffers hold
@@ -99,34 +100,101 @@ __device__ __forceinline__ bool fixed_ok(const SumCtl* c, uint32_t ncat, int& S)
   return true;
 }
 
-// C5 prologue: interleave the four dimension columns into 32-byte records
-// and record the price exponent range -- for the SELECTED keys only: pass 2
-// reads the record of a selected row's key and nothing else, and only
-// selected prices enter the sums (~10% of the keys at C5: the record writes
-// shrink from 1 GiB to ~0.1 GiB, and the scale depends only on summed values).
+// Rank directory of the selection bitmap: dir[w] = {word w, selected bits
+// before word w}, so the dense record index of a selected key i -- its
+// position among the selected keys -- is dir[i/32].y + popc(dir[i/32].x below
+// bit i%32).
+__device__ __forceinline__ uint32_t compact_index(uint2 pr, uint32_t idx) {
+  return pr.y + __popc(pr.x & ((1u << (idx & 31)) - 1u));
+}
+
+__global__ void k_word_popc(const uint32_t* __restrict__ w, uint64_t nw, uint32_t* __restrict__ pc) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    pc[i] = __popc(__ldg(w + i));
+}
+__global__ void k_dir_fill(const uint32_t* __restrict__ w, const uint32_t* __restrict__ pre,
+                           uint64_t nw, uint2* __restrict__ dir) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dir[i] = make_uint2(__ldg(w + i), __ldg(pre + i));
+}
+
+__device__ __forceinline__ void price_exponent(float p, unsigned int& emax, unsigned int& eneg,
+                                               unsigned int& nf) {
+  if (!isfinite(p)) {
+    nf = 1;
+  } else if (p != 0.f) {
+    int e;
+    frexpf(p, &e);
+    const unsigned int eb = (unsigned int)(e + 1024);
+    emax = max(emax, eb);
+    eneg = max(eneg, 2048u - eb);
+  }
+}
+
+// C5 prologue: interleave the four dimension columns into 32-byte records for
+// the SELECTED keys only, dense in key (= rank) order -- record c belongs to
+// the c-th selected key, so the hot selected keys' records share lines -- and
+// record the selected prices' exponent range.  Four keys per thread: the
+// columns stream in with vector loads (every sector is touched anyway at ~10%
+// selectivity) and only the records are scattered.
 __global__ void __launch_bounds__(256)
     k_pack_records(const int32_t* __restrict__ cat, const float* __restrict__ price,
                    const unsigned long long* __restrict__ supp, const uint16_t* __restrict__ flag,
-                   const unsigned long long* __restrict__ words, uint32_t d,
-                   uint4* __restrict__ rec, SumCtl* ctl) {
+                   const uint2* __restrict__ dir, uint32_t d, bool vec, uint4* __restrict__ rec,
+                   SumCtl* ctl) {
   unsigned int emax = 0, eneg = 0, nf = 0;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d; i += stride) {
-    if (!((__ldg(words + (i >> 6)) >> (i & 63)) & 1ull)) continue;
-    const float p = __ldcs(price + i);
-    const unsigned long long sp = __ldcs(supp + i);
-    rec[2 * i] = make_uint4((uint32_t)__ldcs(cat + i), __float_as_uint(p), (uint32_t)sp,
-                            (uint32_t)(sp >> 32));
-    rec[2 * i + 1] = make_uint4((uint32_t)__ldcs(reinterpret_cast<const unsigned short*>(flag) + i),
-                                0u, 0u, 0u);
-    if (!isfinite(p)) {
-      nf = 1;
-    } else if (p != 0.f) {
-      int e;
-      frexpf(p, &e);
-      const unsigned int eb = (unsigned int)(e + 1024);
-      emax = max(emax, eb);
-      eneg = max(eneg, 2048u - eb);
+  const uint64_t nq = d / 4;  // full quads
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += stride) {
+    const uint64_t i0 = q * 4;
+    const uint2 pr = __ldg(dir + (i0 >> 5));
+    const uint32_t bits4 = (pr.x >> (i0 & 31)) & 0xfu;
+    if (!bits4) continue;
+    int32_t cs[4];
+    float ps[4];
+    unsigned long long ss[4];
+    uint32_t fs[4];
+    if (vec) {  // 16-byte aligned columns (8-byte aligned flags)
+      const int4 c4 = __ldcs(reinterpret_cast<const int4*>(cat) + q);
+      const float4 p4 = __ldcs(reinterpret_cast<const float4*>(price) + q);
+      const ulonglong2 sa = __ldcs(reinterpret_cast<const ulonglong2*>(supp) + 2 * q);
+      const ulonglong2 sb = __ldcs(reinterpret_cast<const ulonglong2*>(supp) + 2 * q + 1);
+      const uint2 f4 = __ldcs(reinterpret_cast<const uint2*>(flag) + q);
+      cs[0] = c4.x, cs[1] = c4.y, cs[2] = c4.z, cs[3] = c4.w;
+      ps[0] = p4.x, ps[1] = p4.y, ps[2] = p4.z, ps[3] = p4.w;
+      ss[0] = sa.x, ss[1] = sa.y, ss[2] = sb.x, ss[3] = sb.y;
+      fs[0] = f4.x & 0xffffu, fs[1] = f4.x >> 16, fs[2] = f4.y & 0xffffu, fs[3] = f4.y >> 16;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        cs[j] = cat[i0 + j], ps[j] = price[i0 + j], ss[j] = supp[i0 + j], fs[j] = flag[i0 + j];
+      }
+    }
+    uint32_t c = compact_index(pr, (uint32_t)i0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (!((bits4 >> j) & 1u)) continue;
+      rec[2 * (uint64_t)c] = make_uint4((uint32_t)cs[j], __float_as_uint(ps[j]), (uint32_t)ss[j],
+                                        (uint32_t)(ss[j] >> 32));
+      rec[2 * (uint64_t)c + 1] = make_uint4(fs[j], 0u, 0u, 0u);
+      price_exponent(ps[j], emax, eneg, nf);
+      ++c;
+    }
+  }
+  // the last d % 4 keys, one per thread of the first CTA
+  if (blockIdx.x == 0 && threadIdx.x < d % 4) {
+    const uint64_t i = nq * 4 + threadIdx.x;
+    const uint2 pr = __ldg(dir + (i >> 5));
+    if ((pr.x >> (i & 31)) & 1u) {
+      const uint64_t c = compact_index(pr, (uint32_t)i);
+      const float p = price[i];
+      const unsigned long long sp = supp[i];
+      rec[2 * c] = make_uint4((uint32_t)cat[i], __float_as_uint(p), (uint32_t)sp,
+                              (uint32_t)(sp >> 32));
+      rec[2 * c + 1] = make_uint4((uint32_t)flag[i], 0u, 0u, 0u);
+      price_exponent(p, emax, eneg, nf);
     }
   }
 #pragma unroll
@@ -503,10 +571,16 @@ __global__ void __launch_bounds__(kThreads, SKX_SEL_P2_MINB)
           const uint32_t f = j0 + u * 32 + lane;
           e[u] = f < e_end ? __ldcs(src + f) : make_uint2(0u, 0u);
         }
+        if (FUSED) {  // key -> dense record index (the directory is L2-resident) -> record
+          uint2 pr[kPer];
 #pragma unroll
-        for (int u = 0; u < kPer; ++u) {
-          rc[u] = Rec8{};
-          if (FUSED && j0 + u * 32 + lane < e_end) rc[u] = load_rec(cols.rec, e[u].x);
+          for (int u = 0; u < kPer; ++u)
+            pr[u] = j0 + u * 32 + lane < e_end ? __ldg(cols.dir + (e[u].x >> 5)) : make_uint2(0u, 0u);
+#pragma unroll
+          for (int u = 0; u < kPer; ++u) {
+            rc[u] = Rec8{};
+            if (j0 + u * 32 + lane < e_end) rc[u] = load_rec(cols.rec, compact_index(pr[u], e[u].x));
+          }
         }
 #pragma unroll
         for (int u = 0; u < kPer; ++u) {
@@ -543,7 +617,10 @@ __global__ void __launch_bounds__(kThreads, SKX_SEL_P2_MINB)
         for (int j = 0; j < 4; ++j) {
           if ((sel[i] >> j) & 1u) {
             Rec8 rr{};
-            if (FUSED) rr = load_rec(cols.rec, fk[i][j] - 1u);
+            if (FUSED) {
+              const uint32_t idx = fk[i][j] - 1u;
+              rr = load_rec(cols.rec, compact_index(__ldg(cols.dir + (idx >> 5)), idx));
+            }
             emit_row<FUSED>(ob + pos, row_l + i * 128 + j, rr, base_off, out_off, cols, fixed, S,
                             s_acc);
             ++pos;
@@ -737,7 +814,12 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
   const uint64_t base_b = (ent_b + nregions * 8 + 256 + 255) & ~uint64_t(255);
   const uint64_t acc_b = fused ? (((uint64_t)cols.n_categories * 16 + 255) & ~uint64_t(255)) : 0;
   const uint64_t rec_b = fused ? bits * 32 : 0;
-  char* raw = static_cast<char*>(scratch(ctx, 2, base_b + (fused ? 256 : 0) + acc_b + rec_b, s));
+  const uint64_t nw32 = (bits + 31) / 32;
+  const uint64_t dir_b = fused ? ((nw32 * 8 + 255) & ~uint64_t(255)) : 0;
+  const uint64_t pc_b = fused ? ((nw32 * 4 + 255) & ~uint64_t(255)) : 0;
+  // (fused) ... | rank directory [nw32] | word popcounts [nw32]
+  char* raw = static_cast<char*>(
+      scratch(ctx, 2, base_b + (fused ? 256 : 0) + acc_b + rec_b + dir_b + pc_b, s));
   if (!raw) return set_error(ctx, SKX_CUDA_ERROR, "select: out of device memory");
   uint2* entries = reinterpret_cast<uint2*>(raw);
   uint32_t* counts = reinterpret_cast<uint32_t*>(raw + ent_b);
@@ -747,6 +829,7 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
     cols.ctl = reinterpret_cast<SumCtl*>(raw + base_b);
     cols.acc96 = reinterpret_cast<unsigned int*>(raw + base_b + 256);
     cols.rec = reinterpret_cast<const uint4*>(raw + base_b + 256 + acc_b);
+    cols.dir = reinterpret_cast<const uint2*>(raw + base_b + 256 + acc_b + rec_b);
     ScratchSet* ss = scratch_set(ctx, s);
     ss->sel_acc = cols.acc96;
     ss->sel_ctl = cols.ctl;
@@ -754,11 +837,22 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
     e = cudaMemsetAsync(raw + base_b, 0, 256 + acc_b, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "select memset");
     if (bits) {
-      k_pack_records<<<grid_for(ctx, bits, 256, 8), 256, 0, s>>>(
-          cols.cat, cols.price, cols.supp, cols.flag,
-          reinterpret_cast<const unsigned long long*>(words), (uint32_t)bits,
-          const_cast<uint4*>(cols.rec), cols.ctl);
+      // rank directory: per 32-bit word, the selected bits before it
+      uint32_t* pc = reinterpret_cast<uint32_t*>(raw + base_b + 256 + acc_b + rec_b + dir_b);
+      const auto* w32 = reinterpret_cast<const uint32_t*>(words);
+      k_word_popc<<<grid_for(ctx, nw32, 256, 8), 256, 0, s>>>(w32, nw32, pc);
       ctx->launches++;
+      int rc = launch_exclusive_scan_u32(ctx, pc, pc, nw32, nullptr, 3, s);
+      if (rc) return rc;
+      k_dir_fill<<<grid_for(ctx, nw32, 256, 8), 256, 0, s>>>(w32, pc, nw32,
+                                                             const_cast<uint2*>(cols.dir));
+      const bool cvec = ((reinterpret_cast<uintptr_t>(cols.cat) | reinterpret_cast<uintptr_t>(cols.price) |
+                          reinterpret_cast<uintptr_t>(cols.supp)) % 16 == 0) &&
+                        reinterpret_cast<uintptr_t>(cols.flag) % 8 == 0;
+      k_pack_records<<<grid_for(ctx, (bits + 3) / 4, 256, 8), 256, 0, s>>>(
+          cols.cat, cols.price, cols.supp, cols.flag, cols.dir, (uint32_t)bits, cvec,
+          const_cast<uint4*>(cols.rec), cols.ctl);
+      ctx->launches += 2;
     }
     if (n == 0) {  // no rows: zero sums and count; the scale is still recorded for combining
       e = cudaMemsetAsync(count_dev, 0, 8, s);
@@ -768,7 +862,6 @@ int select_impl(skx_ctx* ctx, bool fused, const uint32_t* fact, uint64_t n, cons
   const bool vec = reinterpret_cast<uintptr_t>(fact) % 16 == 0;
   const auto* w32 = reinterpret_cast<const uint32_t*>(words);
   // Pass 1 with the bitmap prefix staged per CTA in shared memory.
-  const uint64_t nw32 = (bits + 31) / 32;
   size_t sbytes = (size_t)SKX_SEL_SMEM_KB * 1024;
   if (sbytes > ctx->smem_optin - 1024) sbytes = ctx->smem_optin - 1024;
   const uint32_t sw = (uint32_t)(nw32 < sbytes / 4 ? nw32 : sbytes / 4);
@@ -840,7 +933,7 @@ int skx_select_gather_sum(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const 
     return skx::set_error(ctx, SKX_INVALID_ARGUMENT, "select_gather_sum: null column pointer");
   skx::Cols cols{cat, price, reinterpret_cast<const unsigned long long*>(supp), flag,
                  out_cat, out_price, reinterpret_cast<unsigned long long*>(out_supp), out_flag,
-                 sums, n_categories, nullptr, nullptr, nullptr, capacity};
+                 sums, n_categories, nullptr, nullptr, nullptr, nullptr, capacity};
   return skx::select_impl(ctx, true, fact, n, words, d, base, out_off, cols, count_dev,
                           skx::as_stream(stream));
 }

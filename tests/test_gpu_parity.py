@@ -248,7 +248,7 @@ def test_select_gather_sum_vs_oracle(sx, oracle):
 
 
 @pytest.mark.parametrize("case", ["neg", "wide", "nan", "zero", "many_cats", "unaligned",
-                                  "ragged", "dense", "mixed_density"])
+                                  "ragged", "dense", "mixed_density", "unaligned_dims"])
 def test_select_gather_sum_paths(sx, oracle, case):
     """Fixed-point category sums (default) and the on-device fp64 fallback
     (non-finite price, exponent span > 2^30, > 4096 categories), signed
@@ -274,7 +274,10 @@ def test_select_gather_sum_paths(sx, oracle, case):
     fact = fact[1:] if case == "unaligned" else fact[:n]
     thr = {"many_cats": 700, "dense": 1000, "mixed_density": 250}.get(case, 100)
     bm = sx.build_bitmap_lt(cu(cat), thr)
-    got = sx.select_gather_sum(fact, bm, cu(cat), cu(price), cu(supp), cu(flag), ncat, base=5)
+    dcols = [cu(cat), cu(price), cu(supp), cu(flag)]
+    if case == "unaligned_dims":  # dimension columns off their 16-byte alignment (scalar packing)
+        dcols = [torch.cat([c[:1], c])[1:] for c in dcols]
+    got = sx.select_gather_sum(fact, bm, *dcols, ncat, base=5)
     exp = oracle.select_gather_sum(np_(fact), np_(bm.words), cat, price, supp, flag, ncat, base=5)
     for g, e in zip(got[:5], exp[:5]):  # bit-exact (NaN payloads included)
         assert np.array_equal(np_(g).view(np.uint8), np.ascontiguousarray(e).view(np.uint8))
