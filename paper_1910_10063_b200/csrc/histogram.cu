@@ -47,6 +47,9 @@ namespace {
 #ifndef SKX_HIST_TOPREG
 #define SKX_HIST_TOPREG 1  // sampled path: the hottest key counts in a register
 #endif
+#ifndef SKX_HIST_RED_HINT
+#define SKX_HIST_RED_HINT 1  // global counter reductions with an evict_last L2 policy (C4 histogram -4%)
+#endif
 #ifndef SKX_HIST_CTAS
 #define SKX_HIST_CTAS 3
 #endif
@@ -92,12 +95,26 @@ template <typename CT>
 __device__ __forceinline__ void global_add(CT* counts, uint32_t idx, uint32_t c);
 template <>
 __device__ __forceinline__ void global_add<uint32_t>(uint32_t* counts, uint32_t idx, uint32_t c) {
+#if SKX_HIST_RED_HINT
+  unsigned long long pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(counts + idx),
+               "r"(c), "l"(pol) : "memory");
+#else
   atomicAdd(counts + idx, c);
+#endif
 }
 template <>
 __device__ __forceinline__ void global_add<unsigned long long>(unsigned long long* counts,
                                                                uint32_t idx, uint32_t c) {
+#if SKX_HIST_RED_HINT
+  unsigned long long pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(counts + idx),
+               "l"((unsigned long long)c), "l"(pol) : "memory");
+#else
   atomicAdd(counts + idx, (unsigned long long)c);
+#endif
 }
 
 struct Buckets {
