@@ -50,6 +50,9 @@ constexpr uint32_t kCap = 64;                  // compacted entries kept per sli
 #ifndef SKX_SEL_P1_PREF
 #define SKX_SEL_P1_PREF 0   // pass 1: next slice's FKs in flight while probing
 #endif
+#ifndef SKX_SEL_OUT_CS
+#define SKX_SEL_OUT_CS 1    // pass 2 output columns as streaming stores
+#endif
 #ifndef SKX_SEL_PER
 #define SKX_SEL_PER 8
 #endif
@@ -500,15 +503,27 @@ __device__ __forceinline__ void emit_row(uint64_t p, uint32_t row, const Rec8& r
                                          uint32_t base_off, uint32_t* __restrict__ out_off,
                                          const Cols& cols, bool fixed, int S, unsigned int* s_acc) {
   const bool fits = p < cols.cap;  // rows past the caller's capacity are counted, not written
+#if SKX_SEL_OUT_CS
+  // output columns: streaming (.cs) stores, so they do not displace the records in L2
+  if (fits) __stcs(out_off + p, base_off + row);
+#else
   if (fits) out_off[p] = base_off + row;
+#endif
   if (FUSED) {
     const int32_t ct = (int32_t)r.a0;
     const float pr = __uint_as_float(r.a1);
     if (fits) {
+#if SKX_SEL_OUT_CS
+      __stcs(cols.out_cat + p, ct);
+      __stcs(cols.out_price + p, pr);
+      __stcs(cols.out_supp + p, (unsigned long long)r.a2 | ((unsigned long long)r.a3 << 32));
+      __stcs(reinterpret_cast<unsigned short*>(cols.out_flag) + p, (unsigned short)r.b0);
+#else
       cols.out_cat[p] = ct;
       cols.out_price[p] = pr;
       cols.out_supp[p] = (unsigned long long)r.a2 | ((unsigned long long)r.a3 << 32);
       cols.out_flag[p] = (uint16_t)r.b0;
+#endif
     }
     const uint32_t ncat = cols.n_categories;
     if (fixed && (uint32_t)ct < ncat) {
