@@ -96,7 +96,41 @@ struct HotBins {
   uint32_t* cnt;
   uint32_t* lo;
   uint32_t* hi;
+  uint32_t* warm;  // packed mode: 4-byte warm bins for ids [hot8, hot)
+  uint32_t hot8;   // packed mode: ids below get the 8-byte {count, sum lo} bins
 };
+
+// Packed mode: past the hottest kHot8 keys, a shared bin is ONE 32-bit word
+// (count << 22 | sum), twice the keys per byte of shared memory, so fewer rows
+// reach the global tail.  The add returns the old word: a sum field that
+// carried into the count field, or a count field that wrapped out of the
+// word, is corrected in the key's global pair right away -- exact for any
+// input; at C3 a warm key sees a few hundred rows per CTA, so corrections
+// are rare.
+#ifndef SKX_AGG_WARM
+#define SKX_AGG_WARM 1
+#endif
+constexpr uint32_t kHot8 = 1024;
+constexpr int kWarmSumBits = 22;
+constexpr uint32_t kWarmMask = (1u << kWarmSumBits) - 1u;
+
+__device__ __forceinline__ void warm_add(const HotBins& b, uint32_t idx, unsigned long long m,
+                                         unsigned long long* gpairs) {
+  if (m > kWarmMask) {  // wide measure: straight to the exact global pair
+    atomicAdd(&gpairs[2 * (uint64_t)idx], 1ull);
+    atomicAdd(&gpairs[2 * (uint64_t)idx + 1], m);
+    return;
+  }
+  const uint32_t inc = (1u << kWarmSumBits) | (uint32_t)m;
+  const uint32_t old = atomicAdd(&b.warm[idx - b.hot8], inc);
+  const uint32_t carry = ((old & kWarmMask) + (uint32_t)m) >> kWarmSumBits;  // sum -> count field
+  const bool wrap = (uint32_t)(old + inc) < old;                               // count field -> out
+  if (carry | (uint32_t)wrap) {
+    const long long dc = (wrap ? (1ll << (32 - kWarmSumBits)) : 0ll) - (long long)carry;
+    if (dc) atomicAdd(&gpairs[2 * (uint64_t)idx], (unsigned long long)dc);
+    if (carry) atomicAdd(&gpairs[2 * (uint64_t)idx + 1], 1ull << kWarmSumBits);
+  }
+}
 
 // Device-side exactness check of the packed tail (see the header).
 struct AggCheck {
@@ -191,7 +225,10 @@ __device__ __forceinline__ void agg_row(uint32_t idx, unsigned long long m, uint
                                         uint32_t limit, const HotBins& b, const Tail& t,
                                         PackTally& pt) {
   if (idx < hot) {
-    hot_add(b, idx, m, MW != 0, t.pairs);
+    if (PACK && MW && SKX_AGG_WARM && idx >= b.hot8)
+      warm_add(b, idx, m, t.pairs);
+    else
+      hot_add(b, idx, m, MW != 0, t.pairs);
   } else if (idx < limit) {
     if (!MW) {
       if (t.cnt32)
@@ -238,14 +275,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
   extern __shared__ uint32_t smem_agg[];
   PackTally pt;
-  HotBins b{smem_agg, smem_agg + hot, smem_agg + 2 * (size_t)hot};  // lo (hi) only if MW
-  for (uint32_t i = threadIdx.x; i < hot; i += kThreads) {
+  // bins: cnt [hot8] | lo [hot8] (| hi [hot8]) | warm [hot - hot8] (packed mode)
+  const uint32_t hot8 = PACK && MW && SKX_AGG_WARM && kBinBytes == 8 ? min(hot, kHot8) : hot;
+  HotBins b{smem_agg, smem_agg + hot8, smem_agg + 2 * (size_t)hot8,
+            smem_agg + (MW ? 2 * (size_t)hot8 : (size_t)hot8), hot8};
+  for (uint32_t i = threadIdx.x; i < hot8; i += kThreads) {
     b.cnt[i] = 0u;
     if (MW) {
       b.lo[i] = 0u;
       if (kBinBytes == 12) b.hi[i] = 0u;
     }
   }
+  for (uint32_t i = hot8 + threadIdx.x; i < hot; i += kThreads) b.warm[i - hot8] = 0u;
   __syncthreads();
   const uint64_t pol = policy_evict_first();
   const uint4* fv = reinterpret_cast<const uint4*>(fact + head);
@@ -339,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   // Fold the CTA's private bins into the result (the reference's serial fold
   // of parallel.cpp:199-204, here one 64-bit atomic per live bin).
-  for (uint32_t i = threadIdx.x; i < hot; i += kThreads) {
+  for (uint32_t i = threadIdx.x; i < hot8; i += kThreads) {
     const unsigned long long c = b.cnt[i];
     if (c) {
       if (MW) {
@@ -352,6 +393,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         else
           atomicAdd(&t.pairs[i], c);
       }
+    }
+  }
+  for (uint32_t i = hot8 + threadIdx.x; i < hot; i += kThreads) {  // packed warm bins
+    const uint32_t w = b.warm[i - hot8];
+    if (w) {
+      atomicAdd(&t.pairs[2 * (uint64_t)i], (unsigned long long)(w >> kWarmSumBits));
+      atomicAdd(&t.pairs[2 * (uint64_t)i + 1], (unsigned long long)(w & kWarmMask));
     }
   }
 }
@@ -367,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                        uint64_t head, uint64_t nvec, uint64_t n, uint32_t d, uint32_t hot, bool mvec,
                        Tail t, DevErr* err) {
   extern __shared__ uint32_t smem_agg[];
-  HotBins b{smem_agg, smem_agg + hot, smem_agg + 2 * (size_t)hot};
+  HotBins b{smem_agg, smem_agg + hot, smem_agg + 2 * (size_t)hot, nullptr, hot};
   __shared__ unsigned int s_cnt[kMaxBuckets];
   __shared__ unsigned long long s_base[kMaxBuckets];
   for (uint32_t i = threadIdx.x; i < hot; i += kThreads) {
@@ -548,13 +596,26 @@ __global__ void __launch_bounds__(256)
     __stcs(counts + i, (unsigned long long)__ldcs(c32 + i));
 }
 
-uint32_t hot_keys(const skx_ctx* ctx, int mw, uint32_t hot_req, uint32_t limit) {
-  const size_t per_key = mw ? kBinBytes : 4;
+// Keys with private shared-memory bins.  Packed mode (pack, MW != 0): kHot8
+// 8-byte bins, then 4-byte warm bins for the rest of the budget.
+uint32_t hot_keys(const skx_ctx* ctx, int mw, uint32_t hot_req, uint32_t limit, bool pack = false) {
   const size_t budget = ctx->smem_optin > 2048 ? ctx->smem_optin - 2048 : 0;
-  uint32_t hot = (uint32_t)(budget / per_key);
+  uint32_t hot;
+  if (pack && mw && SKX_AGG_WARM && kBinBytes == 8 && budget >= (size_t)kHot8 * 8)
+    hot = kHot8 + (uint32_t)((budget - (size_t)kHot8 * 8) / 4);
+  else
+    hot = (uint32_t)(budget / (mw ? kBinBytes : 4));
   if (hot_req && hot_req < hot) hot = hot_req;
   if (hot > limit) hot = limit;
   return hot;
+}
+
+size_t hot_smem(int mw, bool pack, uint32_t hot) {
+  if (pack && mw && SKX_AGG_WARM && kBinBytes == 8) {
+    const uint32_t h8 = hot < kHot8 ? hot : kHot8;
+    return (size_t)h8 * 8 + (size_t)(hot - h8) * 4;
+  }
+  return (size_t)hot * (mw ? kBinBytes : 4);
 }
 
 template <int MW, bool PACK>
@@ -572,8 +633,8 @@ int aggregate_impl(skx_ctx* ctx, const uint32_t* fact, const void* measure, uint
   // Per-CTA counts must fit the u32 bins.
   if (n / grid + 4 * (uint64_t)kThreads >= (uint64_t(1) << 32))
     return set_error(ctx, SKX_INVALID_ARGUMENT, "aggregate: too many rows per call");
-  const uint32_t hot = hot_keys(ctx, MW, hot_req, limit);
-  const size_t smem = (size_t)hot * (MW ? kBinBytes : 4);
+  const uint32_t hot = hot_keys(ctx, MW, hot_req, limit, PACK);
+  const size_t smem = hot_smem(MW, PACK, hot);
   // Stage the cold tail when its pairs overflow half of L2 (MW != 0 only).
   const uint64_t tail_keys = limit > hot ? limit - hot : 0;
   if (MW && !PACK && !gate && limit == d && ctx->agg_mode == 1 &&
@@ -645,7 +706,7 @@ int launch_aggregate(skx_ctx* ctx, const uint32_t* fact, const void* measure, in
     return aggregate_impl<0, false>(ctx, fact, nullptr, n, d, d, hot_req, t, s);
   }
   const bool pack = ctx->agg_mode == 0 && n > 0;
-  const uint32_t hot = hot_keys(ctx, mw, hot_req, d);
+  const uint32_t hot = hot_keys(ctx, mw, hot_req, d, pack);
   // Far tail for domains whose 8-byte accumulators would not fit half of L2.
   uint32_t far = d;
 #ifndef SKX_AGG_FAR_BITS

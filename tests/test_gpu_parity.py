@@ -478,6 +478,31 @@ def test_aggregate_packed_tail_fallback(sx, oracle, case):
         assert np.array_equal(np_(c), ce) and np.array_equal(np_(s), se)
 
 
+@pytest.mark.parametrize("case", ["wrap_and_carry", "wide", "threshold"])
+def test_aggregate_warm_bins_exact(sx, oracle, case):
+    """Packed mode's 4-byte warm bins (ids past the 1024 hottest, count << 22 |
+    sum in one shared word): a warm key with tens of thousands of rows per CTA
+    (the count field wraps, the sum field carries) and measures >= 2^22 (sent
+    to the exact global pair) stay exact; a caller's hot threshold bounds the
+    warm range."""
+    d = 70000
+    rng = np.random.default_rng(31)
+    n = (1 << 22) + 13
+    fact = rng.integers(1, d + 1, size=n, dtype=np.uint32)
+    fact[: n // 2] = 2000  # a warm key: ~14 K rows per CTA
+    meas = rng.integers(150, 250, size=n, dtype=np.int64)
+    hot = 0
+    if case == "wide":
+        meas[::7] = rng.integers(1 << 22, 1 << 40, size=len(meas[::7]))
+        meas[::7] = np.where(fact[::7] < 50000, meas[::7], 5)  # wide only on hot / warm keys
+    elif case == "threshold":
+        hot = 1500
+        fact[n // 2: n // 2 + 100000] = 1400
+    c, s = sx.aggregate_count_sum(cu(fact), cu(meas), d, hot_threshold=hot)
+    ce, se = oracle.aggregate_count_sum(fact, meas.view(np.uint64), d)
+    assert np.array_equal(np_(c), ce) and np.array_equal(np_(s), se)
+
+
 def test_cache_model_vs_reference_fixtures(sx):
     """Cache model on the device (csrc/cachemodel.cu) against the reference's
     outputs: line_frequencies and trace_from_column bit-exact,
