@@ -63,7 +63,7 @@ constexpr uint32_t kSmemCategories = 2048;     // fp64 fallback: 8 warps x 2048 
 constexpr uint32_t kFixedCategories = 4096;    // fixed point: 3 x 4096 x 4 B per CTA
 constexpr int kRangeLimit = 30;                // max exponent span for fixed point
 #ifndef SKX_SEL_SMEM_KB
-#define SKX_SEL_SMEM_KB 128
+#define SKX_SEL_SMEM_KB 160
 #endif
 
 struct Cols {
