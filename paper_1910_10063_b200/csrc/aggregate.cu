@@ -14,7 +14,10 @@
 // native 64-bit shared add (it compiles to a compare-and-swap spin loop that
 // serialises on the hottest keys), while 32-bit adds are native and merge
 // same-address lanes.  A bin is {u32 count, u32 sum lo}; the rare bits above
-// 32 go straight to the key's global sum.
+// 32 go straight to the key's global sum.  In the packed mode only the 1024
+// hottest keys get such bins; the rest of the shared memory holds 4-byte warm
+// bins (count << 22 | sum, carries and wraps corrected from the returned word),
+// twice the keys per byte.
 //
 // Tail keys (id > H), default "packed" mode: ONE fire-and-forget 64-bit
 // reduction of (1 << 40 | m) per cold row into an 8 B/key accumulator, so a
