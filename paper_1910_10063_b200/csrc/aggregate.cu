@@ -113,7 +113,10 @@ struct HotBins {
 #ifndef SKX_AGG_WARM
 #define SKX_AGG_WARM 1
 #endif
-constexpr uint32_t kHot8 = 1024;
+#ifndef SKX_AGG_HOT8
+#define SKX_AGG_HOT8 1024
+#endif
+constexpr uint32_t kHot8 = SKX_AGG_HOT8;
 constexpr int kWarmSumBits = 22;
 constexpr uint32_t kWarmMask = (1u << kWarmSumBits) - 1u;
 
@@ -604,7 +607,7 @@ __global__ void __launch_bounds__(256)
 uint32_t hot_keys(const skx_ctx* ctx, int mw, uint32_t hot_req, uint32_t limit, bool pack = false) {
   const size_t budget = ctx->smem_optin > 2048 ? ctx->smem_optin - 2048 : 0;
   uint32_t hot;
-  if (pack && mw && SKX_AGG_WARM && kBinBytes == 8 && budget >= (size_t)kHot8 * 8)
+  if (pack && mw && SKX_AGG_WARM && kBinBytes == 8 && budget >= (size_t)kHot8 * 8 + 4)
     hot = kHot8 + (uint32_t)((budget - (size_t)kHot8 * 8) / 4);
   else
     hot = (uint32_t)(budget / (mw ? kBinBytes : 4));
