@@ -327,6 +327,30 @@ def test_select_many_tiles(sx, oracle, thr):
         assert np.allclose(np_(out[5]), exp[5], rtol=1e-6, atol=0)  # sums cover every row
 
 
+@pytest.mark.parametrize("z", [1.0, 0.0])
+def test_recode_large_rank_table(sx, z):
+    """recode_fact for a rank table beyond half of L2 (D = 2^24 + 3, >= 4 rows
+    per id): the hottest ids' ranks come from each CTA's shared-memory table,
+    the rest from the rank table -- against numpy on an unaligned FK column
+    (scalar head and tail rows), then the first out-of-domain row."""
+    from paper_1910_10063_b200 import DomainViolation
+    d = (1 << 24) + 3
+    n = 4 * d + 1001
+    fact = sx.generate_zipf(cu(sx.zipf_cdf(d, z)), n + 1, 29,
+                            rank_to_id=cu(sx.random_bijection(d, 29)))[1:]
+    idx = sx.rebuild(fact, d)
+    out = torch.empty(n + 1, dtype=torch.uint32, device="cuda")[1:]  # same 16-byte phase
+    got = np_(sx.recode_fact(fact, idx, out=out))
+    exp = np_(idx.ranks)[np_(fact).astype(np.int64) - 1]
+    assert np.array_equal(got, exp)
+    bad = fact.clone()
+    bad[n - 2] = d + 7
+    bad[12345] = 0
+    with pytest.raises(DomainViolation) as e:
+        sx.recode_fact(bad, idx, out=out)
+    assert e.value.row() == 12345 and e.value.value() == 0
+
+
 def test_reorder_invariants_at_scale(sx):
     """Size-independent properties at 2^26 rows: gather equality across
     layouts, rank-space counts map back through offsets, multiset of counts
