@@ -61,8 +61,8 @@ def parse():
     p.add_argument("--no-extras", action="store_true", help="headline C2 gather only")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--policy", type=int, default=129,
-                   help="skx_set_gather_policy bits (include/skx.h); 129 = library default")
+    p.add_argument("--policy", type=int, default=129 | 8192,
+                   help="skx_set_gather_policy bits (include/skx.h); 8321 = library default")
     return p.parse_args()
 
 

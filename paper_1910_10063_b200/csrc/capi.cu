@@ -200,7 +200,7 @@ int skx_scratch_bytes(const skx_ctx* ctx, void* stream, uint64_t* bytes) {
 }
 
 int skx_set_gather_policy(skx_ctx* ctx, int policy) {
-  if (!ctx || policy < 0 || policy > 8191) return SKX_INVALID_ARGUMENT;
+  if (!ctx || policy < 0 || policy > 16383) return SKX_INVALID_ARGUMENT;
   cudaSetDevice(ctx->device);
   const bool want = (policy & 4) != 0 && ctx->persist_max > 0;
   if (want != ctx->setaside_on) {

@@ -64,6 +64,13 @@ struct GatherTiers {
   uint64_t t2;
 };
 
+// Control word of the partitioned gather (below); the one-pass kernel runs
+// only when its plan leaves the path off.
+struct PgCtrl {
+  uint32_t mode;   // 1: partitioned
+  uint32_t items;  // fill work-item counter
+};
+
 template <typename V>
 struct Pack4;  // 4 values of width V as 16B/8B stores
 
@@ -146,7 +153,8 @@ template <typename V, bool OUT_VEC, int F>
 __global__ void __launch_bounds__((F & kPolHot) ? kThreadsHot : kThreads, (F & kPolHot) ? 1 : SKX_GATHER_MINB)
     k_gather_vec(const uint32_t* __restrict__ fact, uint64_t head, uint64_t nvec,
                  const V* __restrict__ dim, uint64_t dim_len, V* __restrict__ out, DevErr* err,
-                 GatherTiers tiers) {
+                 GatherTiers tiers, const PgCtrl* gate) {
+  if (gate && gate->mode != 0) return;  // the partitioned path does this launch's work
   constexpr bool HOT = (F & kPolHot) != 0;
   constexpr bool HINTS = (F & kPolHints) != 0;
   constexpr bool NOL1 = (F & kPolNoL1) != 0;
@@ -328,7 +336,8 @@ __global__ void k_gather_scalar(const uint32_t* __restrict__ fact, uint64_t b, u
 
 template <typename V, bool OUT_VEC, int F>
 cudaError_t launch_vec(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64_t nvec,
-                       const V* dim, uint64_t dim_len, V* out, GatherTiers tiers, cudaStream_t s) {
+                       const V* dim, uint64_t dim_len, V* out, GatherTiers tiers, cudaStream_t s,
+                       const PgCtrl* gate) {
   const uint32_t hot = tiers.hot;
   constexpr bool HOT = (F & kPolHot) != 0;
   cudaLaunchConfig_t cfg = {};
@@ -367,24 +376,449 @@ cudaError_t launch_vec(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64
     cudaFuncSetAttribute(k_gather_vec<V, OUT_VEC, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)cfg.dynamicSmemBytes);
   return cudaLaunchKernelEx(&cfg, k_gather_vec<V, OUT_VEC, F>, fact, head, nvec, dim, dim_len, out,
-                            ctx->err, tiers);
+                            ctx->err, tiers, gate);
 }
 
 template <typename V, bool OUT_VEC>
 cudaError_t dispatch_vec(skx_ctx* ctx, int F, const uint32_t* fact, uint64_t head, uint64_t nvec,
-                         const V* dim, uint64_t dim_len, V* out, GatherTiers t, cudaStream_t s) {
+                         const V* dim, uint64_t dim_len, V* out, GatherTiers t, cudaStream_t s,
+                         const PgCtrl* gate) {
   // Bit 4 (window) is a launch attribute; instantiate the useful variants only.
   const bool win = (F & kPolWindow) != 0;
 #define SKX_F(x)                                                                            \
   if ((F & ~kPolWindow) == (x))                                                             \
     return win ? launch_vec<V, OUT_VEC, (x) | kPolWindow>(ctx, fact, head, nvec, dim, dim_len, \
-                                                          out, t, s)                        \
-               : launch_vec<V, OUT_VEC, (x)>(ctx, fact, head, nvec, dim, dim_len, out, t, s);
+                                                          out, t, s, gate)                  \
+               : launch_vec<V, OUT_VEC, (x)>(ctx, fact, head, nvec, dim, dim_len, out, t, s, gate);
   SKX_F(0) SKX_F(1) SKX_F(3) SKX_F(9) SKX_F(17) SKX_F(19)
   SKX_F(33) SKX_F(35) SKX_F(49) SKX_F(51) SKX_F(65) SKX_F(97) SKX_F(69) SKX_F(129) SKX_F(128)
   SKX_F(131) SKX_F(385) SKX_F(641) SKX_F(1153) SKX_F(2177) SKX_F(4225)
 #undef SKX_F
   return cudaErrorInvalidValue;
+}
+
+// ---- partitioned gather (policy bit kPolPart) --------------------------------
+// Same result as the one-pass gather; what changes is how the cold rows meet
+// the dimension.  A row whose id lies past the L2-resident prefix (idx >= t)
+// costs the one-pass kernel a random HBM access, and random accesses complete
+// at ~43 G/s whatever their size: at C2 s=1.0 the ~200 M cold
+// rows are two thirds of the launch.  Here they are radix-partitioned by key
+// range instead, so each partition's dimension slice is read while it sits in
+// L2 -- the GPU form of a partitioned hash join.  Over 8192-row chunks:
+//   plan : one CTA samples 16 K rows and turns the path on only when the cold
+//          share pays for the extra passes (>= SKX_PG_MIN_COLD_PERMILLE); when
+//          it is off only the one-pass kernel (gated on the same flag) works;
+//   part : FK through a double-buffered 1-D TMA ring in shared memory; the
+//          chunk's cold keys go to its record segment grouped by partition
+//          (keys[]), and every row gets a translated word tr[] = its id - 1
+//          (hot), 2^31 | its record slot (cold) or ~0 (out of domain);
+//   fill : partition by partition (work items handed out in order by one
+//          counter, so all CTAs share one slice), vals[i] = dim[keys[i]];
+//   emit : the one-pass gather's streaming loop over tr: hot rows read the
+//          dimension, cold rows their chunk's vals.
+// Slots inside a chunk: each thread owns fixed rows and ranks its cold rows
+// per partition with shared atomics on a private column (one thread per
+// address, so program order, and pipelined -- a read-modify-write would chain
+// every row behind the previous one); an exclusive scan over (partition,
+// thread) turns the counts into slots.
+constexpr int kPolPart = 8192;
+constexpr int kPgT = 256;                         // threads per CTA (part)
+constexpr int kPgU = 8;                           // FK vectors per thread per chunk
+constexpr uint32_t kPgChunkVec = kPgT * kPgU;     // 2048 vectors = 8192 rows
+constexpr uint32_t kPgChunkRows = kPgChunkVec * 4;
+constexpr int kPgChunkShift = 13;
+constexpr int kPgRows = 32;                       // count rows: partitions + 1 dummy
+constexpr uint32_t kPgMaxParts = kPgRows - 1;
+constexpr int kPgFillChunks = 64;                 // chunks per fill work item
+constexpr uint32_t kPgCold = 0x80000000u;         // tr: cold row, low bits = record slot
+#ifndef SKX_PG_HOT_MB
+#define SKX_PG_HOT_MB 32                          // direct (L2-resident) dimension prefix
+#endif
+#ifndef SKX_PG_SLICE_MB
+#define SKX_PG_SLICE_MB 32                        // dimension bytes per partition
+#endif
+#ifndef SKX_PG_MIN_COLD_PERMILLE
+#define SKX_PG_MIN_COLD_PERMILLE 40
+#endif
+// part: ring[2][2048] uint4 | cnt[32][256] | base[64] | bar[2]
+constexpr int kPgRing = 2 * kPgChunkVec * 16;
+constexpr int kPgCnt = kPgRows * kPgT * 4;
+constexpr int kPgPartSmem = kPgRing + kPgCnt + 64 * 4 + 16;
+
+struct PgPlan {
+  uint32_t t;        // idx < t: direct gather
+  uint32_t dl;       // dimension length (<= 2^32 - 1)
+  uint32_t shift;    // partition of a cold idx: (idx - t) >> shift
+  uint32_t nparts;   // <= kPgMaxParts
+  uint32_t nchunks;
+  uint32_t* keys;    // [nchunks * kPgChunkRows]: chunk c's records start at c * kPgChunkRows
+  void* vals;        // same layout, of V
+  uint32_t* tr;      // [nvec * 4] translated FK words
+  uint16_t* ends;    // [nchunks][32] end of partition p's records within the chunk
+  PgCtrl* ctrl;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ bool pg_cold(const PgPlan& pl, uint32_t idx) {
+  return idx - pl.t < pl.dl - pl.t;  // t <= idx < dl
+}
+
+__global__ void __launch_bounds__(256) k_pg_plan(const uint4* __restrict__ fv, uint64_t nvec,
+                                                 PgPlan pl) {
+  __shared__ uint32_t wsum[8];
+  constexpr uint32_t kS = 4096;  // sampled vectors, evenly spread over the column
+  uint32_t cold = 0;
+  for (uint32_t i = threadIdx.x; i < kS; i += 256) {
+    const uint4 q = fv[(uint64_t)i * nvec / kS];
+    cold += pg_cold(pl, q.x - 1u) + pg_cold(pl, q.y - 1u) + pg_cold(pl, q.z - 1u) +
+            pg_cold(pl, q.w - 1u);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cold += __shfl_down_sync(0xffffffffu, cold, o);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = cold;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t c = 0;
+    for (int w = 0; w < 8; ++w) c += wsum[w];
+    pl.ctrl->mode = (uint64_t)c * 1000u >= (uint64_t)kS * 4u * SKX_PG_MIN_COLD_PERMILLE ? 1u : 0u;
+    pl.ctrl->items = 0;
+  }
+}
+
+__device__ __forceinline__ uint32_t pg_chunk_vecs(uint64_t nvec, uint32_t c) {
+  const uint64_t left = nvec - (uint64_t)c * kPgChunkVec;
+  return left < kPgChunkVec ? (uint32_t)left : kPgChunkVec;
+}
+
+// One 1-D TMA copy of chunk c's FK vectors into ring buffer b.
+__device__ __forceinline__ void pg_issue(uint4* ring, uint64_t* bar, int b, const uint4* fv,
+                                         uint64_t nvec, uint32_t c, uint64_t pol) {
+  const uint32_t bytes = pg_chunk_vecs(nvec, c) * 16;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar + b)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
+      "%2, [%3], %4;" ::"r"(smem_u32(ring + (size_t)b * kPgChunkVec)),
+      "l"(fv + (uint64_t)c * kPgChunkVec), "r"(bytes), "r"(smem_u32(bar + b)), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ void pg_wait(uint64_t* bar, int b, uint32_t parity) {
+  asm volatile(
+      "{ .reg .pred p;\n\t"
+      "PG_WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra PG_WAIT_%=; }" ::"r"(smem_u32(bar + b)),
+      "r"(parity)
+      : "memory");
+}
+
+// part: per chunk, the cold keys grouped by partition and the translated FK.
+__global__ void __launch_bounds__(kPgT, 2)
+    k_pg_part(const uint4* __restrict__ fv, uint64_t head, uint64_t nvec, PgPlan pl, DevErr* err) {
+  if (pl.ctrl->mode == 0) return;
+  extern __shared__ __align__(128) unsigned char pg_raw[];
+  uint4* ring = reinterpret_cast<uint4*>(pg_raw);  // [2][kPgChunkVec]
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(pg_raw + kPgRing);
+  uint32_t* base = cnt + kPgRows * kPgT;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + 64);
+  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  uint32_t* dummy = cnt + kPgMaxParts * kPgT + tid;  // sink of the other rows' updates
+  const uint64_t pol = policy_evict_first();
+  uint4* trv = reinterpret_cast<uint4*>(pl.tr);
+  for (uint32_t i = tid; i < kPgRows * kPgT; i += kPgT) cnt[i] = 0;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar + 1)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t c = blockIdx.x;
+  if (tid == 0 && c < pl.nchunks) pg_issue(ring, bar, 0, fv, nvec, c, pol);
+  for (uint32_t k = 0; c < pl.nchunks; ++k, c += gridDim.x) {
+    const int cur = k & 1;
+    if (tid == 0 && c + gridDim.x < pl.nchunks) pg_issue(ring, bar, cur ^ 1, fv, nvec, c + gridDim.x, pol);
+    pg_wait(bar, cur, (k >> 1) & 1);
+    const uint32_t nv = pg_chunk_vecs(nvec, c);
+    const uint64_t v0 = (uint64_t)c * kPgChunkVec;
+    const uint4* fk = ring + (size_t)cur * kPgChunkVec;
+    uint4 q[kPgU];
+    uint32_t rk[kPgU];  // four 8-bit ranks per vector
+#pragma unroll
+    for (int u = 0; u < kPgU; ++u) {
+      const uint32_t vi = tid + u * kPgT;
+      q[u] = vi < nv ? fk[vi] : make_uint4(0, 0, 0, 0);
+      const uint32_t ids[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+      rk[u] = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t idx = ids[j] - 1u;
+        uint32_t* a = pg_cold(pl, idx) ? cnt + ((idx - pl.t) >> pl.shift) * kPgT + tid : dummy;
+        rk[u] |= (atomicAdd(a, 1u) & 0xffu) << (8 * j);  // the dummy's count is garbage
+      }
+      const uint32_t mx = max(max(ids[0] - 1u, ids[1] - 1u), max(ids[2] - 1u, ids[3] - 1u));
+      if (vi < nv && mx >= pl.dl) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (ids[j] - 1u >= pl.dl) record_violation(err, head + (v0 + vi) * 4 + j, ids[j]);
+      }
+    }
+    // counts -> slots: warp w scans rows w, w+8, ... over the 256 thread
+    // columns; row bases are added once the row totals are known.
+    __syncthreads();
+    uint4 ex[4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t r = w + 8 * i;
+      uint32_t tot = 0;
+      ex[i][0] = ex[i][1] = make_uint4(0, 0, 0, 0);
+      if (r < pl.nparts) {
+        const uint4* row = reinterpret_cast<const uint4*>(cnt + r * kPgT) + 2 * lane;
+        const uint4 x0 = row[0], x1 = row[1];
+        const uint32_t ls = x0.x + x0.y + x0.z + x0.w + x1.x + x1.y + x1.z + x1.w;
+        uint32_t inc = ls;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += y;
+        }
+        uint32_t x = inc - ls;
+        ex[i][0].x = x; x += x0.x; ex[i][0].y = x; x += x0.y; ex[i][0].z = x; x += x0.z;
+        ex[i][0].w = x; x += x0.w; ex[i][1].x = x; x += x1.x; ex[i][1].y = x; x += x1.y;
+        ex[i][1].z = x; x += x1.z; ex[i][1].w = x;
+        tot = __shfl_sync(0xffffffffu, inc, 31);
+      }
+      if (lane == 0) base[r] = tot;
+    }
+    __syncthreads();
+    if (w == 0) {
+      const uint32_t v = base[lane];
+      uint32_t inc = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      base[32 + lane] = inc - v;
+      if (lane == 31) base[32] = inc;  // base[32] = total, base[33 + r] = start of row r + 1
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t r = w + 8 * i;
+      if (r < pl.nparts) {
+        const uint32_t b = r ? base[32 + r] : 0u;
+        uint4* row = reinterpret_cast<uint4*>(cnt + r * kPgT) + 2 * lane;
+        row[0] = make_uint4(ex[i][0].x + b, ex[i][0].y + b, ex[i][0].z + b, ex[i][0].w + b);
+        row[1] = make_uint4(ex[i][1].x + b, ex[i][1].y + b, ex[i][1].z + b, ex[i][1].w + b);
+      }
+    }
+    const uint32_t total = base[32];
+    if (tid < 32) pl.ends[(size_t)c * 32 + tid] = (uint16_t)(tid + 1 < pl.nparts ? base[33 + tid] : total);
+    __syncthreads();
+    // keys in slot order over this chunk's ring buffer; tr in row order
+    uint32_t* stage = reinterpret_cast<uint32_t*>(ring + (size_t)cur * kPgChunkVec);
+#pragma unroll
+    for (int u = 0; u < kPgU; ++u) {
+      const uint32_t vi = tid + u * kPgT;
+      const uint32_t ids[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+      uint32_t o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t idx = ids[j] - 1u;
+        const bool cold = pg_cold(pl, idx);
+        const uint32_t p = cold ? (idx - pl.t) >> pl.shift : kPgMaxParts;
+        const uint32_t slot = cnt[p * kPgT + tid] + ((rk[u] >> (8 * j)) & 0xffu);
+        *(cold ? stage + slot : dummy) = idx;
+        o[j] = cold ? kPgCold | slot : (idx < pl.t ? idx : 0xffffffffu);
+      }
+      if (vi < nv) st_stream_v4(trv + v0 + vi, make_uint4(o[0], o[1], o[2], o[3]), pol);
+    }
+    __syncthreads();
+    const uint64_t r0 = (uint64_t)c * kPgChunkRows;
+    for (uint32_t i = tid; i < total; i += kPgT) pl.keys[r0 + i] = stage[i];
+    for (uint32_t i = tid; i < pl.nparts * kPgT; i += kPgT) cnt[i] = 0;
+    __syncthreads();  // ring buffer cur is refilled next iteration
+  }
+}
+
+// fill: vals[i] = dim[keys[i]], partition-major: the work items (partition,
+// 64 chunks) are handed out in order by one counter, so the CTAs stay within
+// one or two partitions and each dimension slice is read while L2-resident.
+template <typename V>
+__global__ void __launch_bounds__(256)
+    k_pg_fill(const V* __restrict__ dim, PgPlan pl) {
+  if (pl.ctrl->mode == 0) return;
+  __shared__ uint32_t sb[kPgFillChunks];
+  __shared__ uint32_t soff[kPgFillChunks + 1];
+  __shared__ uint32_t s_item;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t nblk = (pl.nchunks + kPgFillChunks - 1) / kPgFillChunks;
+  const uint32_t items = nblk * pl.nparts;
+  V* vals = static_cast<V*>(pl.vals);
+  const uint64_t pol_s = policy_evict_first();
+  for (;;) {
+    if (tid == 0) s_item = atomicAdd(&pl.ctrl->items, 1u);
+    __syncthreads();
+    const uint32_t it = s_item;
+    if (it >= items) break;
+    const uint32_t p = it / nblk, blk = it % nblk;
+    if (tid < kPgFillChunks) {
+      const uint32_t c = blk * kPgFillChunks + tid;
+      uint32_t n = 0, b = 0;
+      if (c < pl.nchunks) {
+        const uint32_t st = p ? pl.ends[(size_t)c * 32 + p - 1] : 0u;
+        n = pl.ends[(size_t)c * 32 + p] - st;
+        b = c * kPgChunkRows + st;
+      }
+      sb[tid] = b;
+      const int lane = tid & 31;
+      uint32_t inc = n;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      soff[tid + 1] = inc;  // warp-local inclusive; the second warp is offset below
+    }
+    __syncthreads();
+    if (tid >= 32 && tid < kPgFillChunks) soff[tid + 1] += soff[32];
+    if (tid == 0) soff[0] = 0;
+    __syncthreads();
+    const uint32_t total = soff[kPgFillChunks];
+    for (uint32_t i0 = 0; i0 < total; i0 += 4 * 256) {
+      uint32_t pos[4], key[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint32_t i = i0 + r * 256 + tid;
+        pos[r] = 0xffffffffu;
+        if (i < total) {
+          uint32_t lo = 0, hi = kPgFillChunks;  // soff[lo] <= i < soff[hi]
+#pragma unroll
+          for (int st = 0; st < 6; ++st) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (soff[mid] <= i) lo = mid; else hi = mid;
+          }
+          pos[r] = sb[lo] + (i - soff[lo]);
+          key[r] = ld_stream_u32(pl.keys + pos[r], pol_s);
+        }
+      }
+      V v[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (pos[r] != 0xffffffffu) v[r] = __ldg(dim + key[r]);
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (pos[r] != 0xffffffffu) vals[pos[r]] = v[r];
+    }
+    __syncthreads();  // sb / soff / s_item are rewritten for the next item
+  }
+}
+
+// emit: the one-pass gather's loop over the translated column.
+template <typename V>
+__global__ void __launch_bounds__(kThreads, SKX_GATHER_MINB)
+    k_pg_emit(uint64_t nvec, const V* __restrict__ dim, V* __restrict__ o, PgPlan pl) {
+  if (pl.ctrl->mode == 0) return;
+  const uint64_t pol_s = policy_evict_first();
+  const uint64_t pol_d = policy_evict_last();
+  const uint4* trv = reinterpret_cast<const uint4*>(pl.tr);
+  const V* vals = static_cast<const V*>(pl.vals);
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads * kUnroll;
+  for (uint64_t base = (uint64_t)blockIdx.x * kThreads * kUnroll + threadIdx.x; base < nvec;
+       base += stride) {
+    uint4 f[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint64_t vi = base + (uint64_t)u * kThreads;
+      f[u] = vi < nvec ? __ldcs(trv + vi) : make_uint4(~0u, ~0u, ~0u, ~0u);
+    }
+    V v[kUnroll][4];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint64_t vi = base + (uint64_t)u * kThreads;
+      const V* cv = vals + ((vi * 4) >> kPgChunkShift << kPgChunkShift);  // the chunk's records
+      const uint32_t w[4] = {f[u].x, f[u].y, f[u].z, f[u].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t x = w[j];
+        if (x < kPgCold)
+          v[u][j] = ld_dim<V>(dim + x, pol_d, true);
+        else if (x != 0xffffffffu)
+          v[u][j] = ld_dim<V>(cv + (x & ~kPgCold), pol_s, true);
+        else
+          v[u][j] = 0;  // out of domain (recorded by part)
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint64_t vi = base + (uint64_t)u * kThreads;
+      if (vi < nvec) {
+        if constexpr (sizeof(V) == 8) {
+          __stcs(reinterpret_cast<ulonglong2*>(o + vi * 4), make_ulonglong2(v[u][0], v[u][1]));
+          __stcs(reinterpret_cast<ulonglong2*>(o + vi * 4) + 1, make_ulonglong2(v[u][2], v[u][3]));
+        } else {
+          Pack4<V>::store(o + vi * 4, v[u], pol_s);
+        }
+      }
+    }
+  }
+}
+
+// Returns 1 when the partitioned path does not apply (the caller runs the
+// one-pass kernel alone), else a status; on SKX_OK *gate is the flag the
+// one-pass kernel must be gated on (it runs when the plan turns the path off).
+template <typename V>
+int pgather_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64_t nvec, const V* dim,
+                 uint64_t dim_len, V* out, cudaStream_t s, const PgCtrl** gate) {
+  if constexpr (sizeof(V) < 4) {
+    return 1;
+  } else {
+    const uint64_t t = ((uint64_t)SKX_PG_HOT_MB << 20) / sizeof(V);
+    if (dim_len <= 2 * t || dim_len > 0xFFFFFFFFull || nvec < (1u << 20)) return 1;
+    const uint64_t nchunks = (nvec + kPgChunkVec - 1) / kPgChunkVec;
+    if (nchunks * kPgChunkRows > 0xFFFFFFFFull) return 1;  // 32-bit record positions
+    if (reinterpret_cast<uintptr_t>(out + head) % 16 != 0) return 1;
+    uint32_t shift = 0;
+    while (((uint64_t)1 << shift) < ((uint64_t)SKX_PG_SLICE_MB << 20) / sizeof(V)) ++shift;
+    while (((dim_len - t + ((uint64_t)1 << shift) - 1) >> shift) > kPgMaxParts) ++shift;
+    PgPlan pl{};
+    pl.t = (uint32_t)t;
+    pl.dl = (uint32_t)dim_len;
+    pl.shift = shift;
+    pl.nparts = (uint32_t)((dim_len - t + ((uint64_t)1 << shift) - 1) >> shift);
+    pl.nchunks = (uint32_t)nchunks;
+    const uint64_t recs = nchunks * kPgChunkRows;
+    auto up = [](uint64_t b) { return (size_t)((b + 255) & ~uint64_t(255)); };
+    const size_t ends_b = up(nchunks * 32 * 2), keys_b = up(recs * 4), tr_b = up(nvec * 16);
+    char* sp = static_cast<char*>(
+        scratch(ctx, 1, 256 + ends_b + keys_b + tr_b + recs * sizeof(V), s));
+    if (!sp) return set_error(ctx, SKX_CUDA_ERROR, "gather: out of device memory (partitioned path)");
+    pl.ctrl = reinterpret_cast<PgCtrl*>(sp);
+    pl.ends = reinterpret_cast<uint16_t*>(sp + 256);
+    pl.keys = reinterpret_cast<uint32_t*>(sp + 256 + ends_b);
+    pl.tr = reinterpret_cast<uint32_t*>(sp + 256 + ends_b + keys_b);
+    pl.vals = sp + 256 + ends_b + keys_b + tr_b;
+    const uint4* fv = reinterpret_cast<const uint4*>(fact + head);
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(k_pg_part, cudaFuncAttributeMaxDynamicSharedMemorySize, kPgPartSmem);
+      attr_set = true;
+    }
+    k_pg_plan<<<1, 256, 0, s>>>(fv, nvec, pl);
+    k_pg_part<<<grid_for(ctx, nchunks, 1, 2), kPgT, kPgPartSmem, s>>>(fv, head, nvec, pl, ctx->err);
+    k_pg_fill<V><<<grid_for(ctx, (uint64_t)pl.nparts * nchunks, kPgFillChunks, 8), 256, 0, s>>>(
+        dim, pl);
+    k_pg_emit<V><<<grid_for(ctx, nvec, kThreads * kUnroll, 8), kThreads, 0, s>>>(nvec, dim,
+                                                                                out + head, pl);
+    ctx->launches += 4;
+    *gate = pl.ctrl;
+    return SKX_OK;
+  }
 }
 
 template <typename V>
@@ -406,6 +840,12 @@ int gather_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const V* dim, ui
     const uintptr_t oa = reinterpret_cast<uintptr_t>(out + head);
     const bool out_vec = (sizeof(V) == 2) ? (oa % 8 == 0) : (oa % 16 == 0);
     int F = ctx->gather_policy;
+    const PgCtrl* gate = nullptr;
+    if (F & kPolPart) {
+      const int rc = pgather_impl<V>(ctx, fact, head, nvec, dim, dim_len, out, s, &gate);
+      if (rc != 1 && rc != SKX_OK) return rc;
+    }
+    F &= ~kPolPart;
     // Shared-memory tier: as many leading dimension values as fit.
     uint32_t hot = 0;
     if ((F & kPolHot) && (reinterpret_cast<uintptr_t>(dim) % 16) == 0) {
@@ -425,8 +865,8 @@ int gather_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const V* dim, ui
       t.t2 = (uint64_t)((double)ctx->l2_bytes * ctx->tier_l2_frac) / sizeof(V);
     }
     const cudaError_t e =
-        out_vec ? dispatch_vec<V, true>(ctx, F, fact, head, nvec, dim, dim_len, out, t, s)
-                : dispatch_vec<V, false>(ctx, F, fact, head, nvec, dim, dim_len, out, t, s);
+        out_vec ? dispatch_vec<V, true>(ctx, F, fact, head, nvec, dim, dim_len, out, t, s, gate)
+                : dispatch_vec<V, false>(ctx, F, fact, head, nvec, dim, dim_len, out, t, s, gate);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "gather launch");
     ctx->launches++;
   }

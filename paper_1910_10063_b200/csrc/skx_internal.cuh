@@ -161,7 +161,7 @@ struct skx_ctx {
   skx::DevErr* err = nullptr;       // device
   skx::DevErr* err_host = nullptr;  // pinned mirror
   uint64_t last_domain = 0;
-  int gather_policy = 129;  // L2 hints + .cs streams (profiles/r1_experiments.md)
+  int gather_policy = 129 | 8192;  // L2 hints + .cs streams + partitioned cold rows
   size_t persist_max = 0;  // cudaDevAttrMaxPersistingL2CacheSize (0: no windows)
   size_t window_max = 0;   // cudaDevAttrMaxAccessPolicyWindowSize
   bool setaside_on = false;  // cudaLimitPersistingL2CacheSize currently reserved

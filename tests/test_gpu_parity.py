@@ -680,7 +680,7 @@ def test_build_index_small_count_pass(sx, oracle, case):
     assert np.array_equal(np_(idx32.offsets), off)
 
 
-@pytest.mark.parametrize("policy", [129, 2177, 4225, 1, 0])
+@pytest.mark.parametrize("policy", [129, 2177, 4225, 1, 0, 129 | 8192])
 def test_gather_output_store_policies(sx, policy):
     """Every output-store variant of the gather (128-bit .cs stores, 8 KB
     shared-memory-staged cp.async.bulk stores, 256-bit stores, plain) writes
@@ -700,7 +700,53 @@ def test_gather_output_store_policies(sx, policy):
                 exp = dim_np[fact_np[off: off + n].astype(np.int64) - 1]
                 assert np.array_equal(np_(out).view(np.uint64), exp), (policy, n, off)
     finally:
-        ctx.set_gather_policy(129)
+        ctx.set_gather_policy(129 | 8192)
+
+
+@pytest.mark.parametrize("npdt", [np.uint32, np.uint64])
+def test_gather_partitioned(sx, oracle, npdt):
+    """The partitioned gather (policy bit 8192, the default): cold rows
+    radix-partitioned by key range, their values fetched slice by slice and
+    merged back at the slots each chunk recomputes.  Same bytes as the one-pass
+    kernel (policy 129) and numpy, for Zipf and uniform ids (path on) and
+    hot-only ids (the plan turns it off), ragged sizes with partial last
+    chunks, misaligned heads, many partitions, and the first bad row."""
+    from paper_1910_10063_b200 import DomainViolation
+    ctx = sx.context(0)
+    rng = np.random.default_rng(11)
+    w = np.dtype(npdt).itemsize
+    hot = (32 << 20) // w                      # the direct prefix (SKX_PG_HOT_MB)
+    for d in [2 * hot + 1, (1 << 30) // w + 12345]:   # 1 and ~30 partitions
+        dim_np = rng.integers(0, np.iinfo(npdt).max, size=d, dtype=npdt)
+        dim = cu(dim_np)
+        cdf = oracle.zipf_cdf(d, 0.9)
+        cases = [("zipf", oracle.generate_zipf_counter(cdf, None, 7, 0, (1 << 22) + 8192 * 3 + 5)),
+                 ("uniform", rng.integers(1, d + 1, size=(1 << 23) + 3, dtype=np.uint32)),
+                 ("hot_only", rng.integers(1, hot // 2, size=(1 << 22) + 1, dtype=np.uint32))]
+        del cdf
+        for name, fact_np in cases:
+            n = fact_np.size - 1
+            full = cu(fact_np)
+            for off in (0, 1, 3):
+                exp = dim_np[fact_np[off: off + n].astype(np.int64) - 1]
+                out = sx.materialize(full[off: off + n], dim)
+                assert np.array_equal(np_(out).view(npdt), exp), (d, name, off)
+            ctx.set_gather_policy(129)
+            try:
+                one = sx.materialize(full[1: 1 + n], dim)
+            finally:
+                ctx.set_gather_policy(129 | 8192)
+            assert np.array_equal(np_(one).view(npdt), dim_np[fact_np[1: 1 + n].astype(np.int64) - 1])
+        # first bad row, path on (uniform ids) and off (hot ids)
+        for name, hi in (("on", d), ("off", hot // 2)):
+            fact_np = rng.integers(1, hi + 1, size=(1 << 22) + 7, dtype=np.uint32)
+            fact_np[3_000_001] = d + 9
+            fact_np[3_500_000] = 0
+            with pytest.raises(DomainViolation) as e:
+                sx.materialize(cu(fact_np), dim)
+            assert e.value.row() == 3_000_001 and e.value.value() == d + 9, name
+        del dim, dim_np
+        torch.cuda.empty_cache()
 
 
 @pytest.mark.parametrize("dtype,npdt", [(torch.uint32, np.uint32), (torch.int64, np.int64)])
