@@ -407,8 +407,13 @@ def timed(fn, steps, warmup, coll, ctx=None, phases=False):
     import torch
 
     from paper_1910_10063_b200 import dist as sdist
-    for _ in range(warmup):
+    for i in range(warmup):
         fn(None)
+        if i == 0:
+            # gather plans land on the host asynchronously (include/skx.h, policy bit 8192):
+            # drain once so the remaining warm-ups already follow them and any scratch the
+            # planned path needs is allocated before the timed region
+            torch.cuda.synchronize()
     torch.cuda.synchronize()
     coll.barrier()
     torch.cuda.synchronize()
@@ -469,6 +474,10 @@ class Env:
         self.coll = sdist.default_collectives(local)
         self.ctx = sx.context(local)
         self.ctx.set_gather_policy(args.policy)
+        if os.environ.get("SKX_BENCH_RESERVE_GB") and not os.environ.get("SKX_BENCH_RESERVE_LATE"):  # experiment knob (profiles/r2_experiments.md §27)
+            self.ctx.check(self.ctx.lib.skx_reserve(
+                self.ctx.handle, 1, int(float(os.environ["SKX_BENCH_RESERVE_GB"]) * 2**30),
+                self.ctx.stream()))
         self.ex = sdist.GpuExecutor(self.ctx)
         self.strong = args.scaling == "strong"
         self.peak, self.peak_kind = load_peaks()
@@ -511,6 +520,10 @@ def run_ours(args):
     data = ds.make_gather_dataset(d, n_total, args.z, ds.SEED, torch.int64, shard)
     setup_s = time.perf_counter() - t0
     out = torch.empty(rows_local, dtype=torch.int64, device="cuda")
+    if os.environ.get("SKX_BENCH_RESERVE_GB") and os.environ.get("SKX_BENCH_RESERVE_LATE"):
+        ctx.check(ctx.lib.skx_reserve(ctx.handle, 1,
+                                      int(float(os.environ["SKX_BENCH_RESERVE_GB"]) * 2**30),
+                                      ctx.stream()))
 
     def step_freq(_t):
         sdist.gather(data.fact_freq, data.dim_freq, ex, out)
@@ -519,7 +532,11 @@ def run_ours(args):
     sampler.start()
     total_ms, per, launches, _ = timed(step_freq, args.steps, args.warmup, coll, ctx)
     clocks = sampler.stop()
+    if os.environ.get("SKX_BENCH_DUMP_PER"):
+        print("per-step ms:", " ".join(f"{x:.3f}" for x in per), file=sys.stderr)
     ctx.sync()  # raises on a deferred domain violation
+    path_of = lambda: "partitioned" if ctx.gather_last_plan()["partitioned"] else "one-pass"
+    headline_path = path_of()
     total_ms = max_over_ranks(total_ms, coll)
     value = n_total * args.steps / (total_ms * 1e-3)
     alg_bytes = rows_local * (4 + 8)  # FK read + int64 output write per row
@@ -537,7 +554,7 @@ def run_ours(args):
         extras["rand_layout"] = {
             "value": n_total * args.steps / (tr * 1e-3), "unit": "rows/s",
             "roofline_frac": roofline(alg_bytes, statistics.mean(per_r), peak)["frac"],
-            "freq_over_rand": tr / total_ms, "outputs_equal": same}
+            "freq_over_rand": tr / total_ms, "outputs_equal": same, "gather_path": path_of()}
         if not same:
             raise SystemExit("CorrectnessError: rand and freq layouts disagree")
         del outr
@@ -558,7 +575,7 @@ def run_ours(args):
             if t is not None:
                 t.mark("permute")
             box["idx"] = idx
-        tib, _, _, ph = timed(ib_step, 3, 1, coll, phases=True)
+        tib, _, _, ph = timed(ib_step, 3, 3, coll, phases=True)
         ctx.sync()
         same_idx = bool(torch.equal(box["idx"].offsets, data.index.offsets)) and bool(
             torch.equal(fact_tmp, data.fact_freq))
@@ -653,7 +670,8 @@ def run_ours(args):
                 sweep[f"s{zz}_{lay}"] = {"ms_per_step": ms, "value": n_total / (ms * 1e-3),
                                          "unit": "rows/s",
                                          "roofline_frac": roofline(alg_bytes, statistics.mean(per_s),
-                                                                   peak)["frac"]}
+                                                                   peak)["frac"],
+                                         "gather_path": path_of()}
             if shard.rows < (1 << 32):
                 split_cells(zz, g.fact_freq, g.dim_freq)
             del g
@@ -690,7 +708,9 @@ def run_ours(args):
                                       "dimension replicated)",
                        "l2": "inputs larger than L2 (4 GiB FK + 8 GiB output + 1 GiB dim per step "
                              "at N=1)",
-                       "gather_policy": args.policy},
+                       "gather_policy": args.policy,
+                       # the device-side plan's choice for this column (include/skx.h, bit 8192)
+                       "gather_path": headline_path},
             "roofline": rf,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -865,7 +885,7 @@ def bench_c4(args, E):
         if t is not None:
             t.mark("permute")
     k = 3
-    t4, per4, launches, ph = timed(step, k, 1, coll, ctx, phases=True)
+    t4, per4, launches, ph = timed(step, k, 3, coll, ctx, phases=True)
     ctx.sync()
     t4 = max_over_ranks(t4, coll) / k
     alg4 = shard.rows * 12 + w.d * 28

@@ -372,9 +372,40 @@ int skx_groupby_packed_ok(const uint64_t* guard_sum);
  *       colder ids are L2 evict_first and skip L1 (skx_set_gather_tiers);
  *  64 = diagnostic: loads only, output stores dropped (NOT a valid gather);
  * 128 = FK stream / output use the .cs (streaming) cache operator;
- * 256, 512 = int64 dimension loads via the coherent / .cg (L2-only) path.
- * Default 129 (= 1 | 128); measurements in profiles/r1_experiments.md. */
+ * 256, 512 = int64 dimension loads via the coherent / .cg (L2-only) path;
+ * 2048 = output staged per CTA and written with 8 KB bulk stores;
+ * 4096 = int64 output as 256-bit stores;
+ * 8192 = partitioned gather for columns whose rows mostly miss L2: the cold
+ *       rows are radix-partitioned by key range and their values fetched
+ *       slice by slice while each dimension slice is L2-resident (the GPU form
+ *       of a partitioned join; needs ~4 + 4 + 2 x width bytes of scratch per
+ *       row, and falls back to the one-pass kernel without it).  Whether a
+ *       column takes it is planned on the device: the first launch over a
+ *       (fact pointer, rows, dimension pointer, length) pair runs the one-pass
+ *       kernel and a plan kernel that samples 64 K rows; the plan is copied
+ *       back asynchronously, and once it has landed later launches over the
+ *       same pair follow it -- partitioned when >= 30% of the sample are first
+ *       touches of dimension lines past the L2-resident prefix, the launch
+ *       touches each such line >= 4 times and the ids do not walk the
+ *       dimension in order; one pass otherwise (skew-reordered columns at
+ *       s >= ~1, in-order permutes, heavy-hitter recodes).  Plans are
+ *       refreshed in the background every 16 launches and dropped by
+ *       skx_set_gather_policy; a stale plan (the buffer now holds another
+ *       column) can cost time but never changes a result.  Inside a CUDA
+ *       Graph capture the one-pass kernel runs;
+ * 16384 = with 8192: take the partitioned path at once, whatever a plan says.
+ * Default 8321 (= 1 | 128 | 8192); measurements in profiles/r1_experiments.md
+ * and profiles/r2_experiments.md. */
 int skx_set_gather_policy(skx_ctx* ctx, int policy);
+/* Evidence: the last gather launched on this context, after draining `stream`
+ * (which must be the stream it ran on): info[0] = 1 when it ran the
+ * partitioned kernels; info[3] = its column's plan (1 = partitioned: what the
+ * next launches over the same column take); info[1] = sampled rows (of 65536)
+ * the plan counted as miss candidates, info[2] = ascending adjacent id pairs
+ * inside the sampled 4-row vectors (of 49152; >= 80% marks an in-order walk).
+ * info must hold 4 words; info[1..3] are 0 for launches that were not planned
+ * (policy bit off, small or narrow columns, forced path: info[3] = info[0]). */
+int skx_gather_last_plan(skx_ctx* ctx, uint32_t* info, void* stream);
 /* cudaLimitMaxL2FetchGranularity (32, 64 or 128 bytes): device-wide. */
 int skx_set_l2_fetch_granularity(skx_ctx* ctx, int bytes);
 /* Tier sizes: shared-memory tier (policy bit 2) capped at smem_bytes (0 = all

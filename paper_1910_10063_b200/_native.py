@@ -72,6 +72,7 @@ SIGNATURES = {
     "skx_materialize_host": (_int, [_vp, _int, _vp, _u64, _vp, _u64, _vp]),
     "skx_aggregate_host": (_int, [_vp, _vp, _vp, _int, _u64, _u32, _u32, _vp, _vp]),
     "skx_set_gather_policy": (_int, [_vp, _int]),
+    "skx_gather_last_plan": (_int, [_vp, _vp, _vp]),
     "skx_set_l2_fetch_granularity": (_int, [_vp, _int]),
     "skx_device_info": (_int, [_vp, _vp, _int]),
     "skx_reset_persisting_l2": (_int, [_vp]),

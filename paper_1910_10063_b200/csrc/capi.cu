@@ -170,6 +170,10 @@ int skx_ctx_destroy(skx_ctx* ctx) {
     if (s) cudaStreamDestroy(s);
   for (auto& ev : ctx->hevent)
     if (ev) cudaEventDestroy(ev);
+  for (auto& pe : ctx->pg_cache)
+    if (pe.ev) cudaEventDestroy(pe.ev);
+  if (ctx->pg_host) cudaFreeHost(ctx->pg_host);
+  if (ctx->pg_dev) cudaFree(ctx->pg_dev);
   cudaFree(ctx->err);
   cudaFreeHost(ctx->err_host);
   delete ctx;
@@ -200,7 +204,7 @@ int skx_scratch_bytes(const skx_ctx* ctx, void* stream, uint64_t* bytes) {
 }
 
 int skx_set_gather_policy(skx_ctx* ctx, int policy) {
-  if (!ctx || policy < 0 || policy > 16383) return SKX_INVALID_ARGUMENT;
+  if (!ctx || policy < 0 || policy > 32767) return SKX_INVALID_ARGUMENT;
   cudaSetDevice(ctx->device);
   const bool want = (policy & 4) != 0 && ctx->persist_max > 0;
   if (want != ctx->setaside_on) {
@@ -210,6 +214,9 @@ int skx_set_gather_policy(skx_ctx* ctx, int policy) {
     ctx->setaside_on = want;
   }
   ctx->gather_policy = policy;
+  for (auto& pe : ctx->pg_cache)  // plans were made under the old policy; copies in flight finish
+    if (!pe.pending) pe.state = 0;
+    else pe.fact = nullptr;  // matches no launch; the slot is reused once its copy has landed
   return SKX_OK;
 }
 

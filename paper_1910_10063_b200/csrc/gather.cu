@@ -67,8 +67,10 @@ struct GatherTiers {
 // Control word of the partitioned gather (below); the one-pass kernel runs
 // only when its plan leaves the path off.
 struct PgCtrl {
-  uint32_t mode;   // 1: partitioned
-  uint32_t items;  // fill work-item counter
+  uint32_t mode;          // 1: partitioned
+  uint32_t items;         // fill work-item counter
+  uint32_t sample_first;  // plan: sampled rows that were miss candidates (of 65536)
+  uint32_t sample_asc;    // plan: ascending adjacent id pairs within the sampled vectors (of 49152)
 };
 
 template <typename V>
@@ -375,6 +377,9 @@ cudaError_t launch_vec(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64
   if (HOT || (F & kPolBulkOut))
     cudaFuncSetAttribute(k_gather_vec<V, OUT_VEC, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)cfg.dynamicSmemBytes);
+  else  // no shared memory: ask for the whole unified array as L1 whatever ran before
+    cudaFuncSetAttribute(k_gather_vec<V, OUT_VEC, F>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxL1);
   return cudaLaunchKernelEx(&cfg, k_gather_vec<V, OUT_VEC, F>, fact, head, nvec, dim, dim_len, out,
                             ctx->err, tiers, gate);
 }
@@ -405,9 +410,10 @@ cudaError_t dispatch_vec(skx_ctx* ctx, int F, const uint32_t* fact, uint64_t hea
 // rows are two thirds of the launch.  Here they are radix-partitioned by key
 // range instead, so each partition's dimension slice is read while it sits in
 // L2 -- the GPU form of a partitioned hash join.  Over 8192-row chunks:
-//   plan : one CTA samples 16 K rows and turns the path on only when the cold
-//          share pays for the extra passes (>= SKX_PG_MIN_COLD_PERMILLE); when
-//          it is off only the one-pass kernel (gated on the same flag) works;
+//   plan : one CTA samples 64 K rows and turns the path on only when enough of
+//          them would miss L2 in the one-pass kernel to pay for the extra
+//          passes (k_pg_plan below); when it is off only the one-pass kernel
+//          (gated on the same flag) works;
 //   part : FK through a double-buffered 1-D TMA ring in shared memory; the
 //          chunk's cold keys go to its record segment grouped by partition
 //          (keys[]), and every row gets a translated word tr[] = its id - 1
@@ -422,6 +428,7 @@ cudaError_t dispatch_vec(skx_ctx* ctx, int F, const uint32_t* fact, uint64_t hea
 // every row behind the previous one); an exclusive scan over (partition,
 // thread) turns the counts into slots.
 constexpr int kPolPart = 8192;
+constexpr int kPolPartForce = 16384;  // with kPolPart: skip the plan's gate (tests, measurements)
 constexpr int kPgT = 256;                         // threads per CTA (part)
 constexpr int kPgU = 8;                           // FK vectors per thread per chunk
 constexpr uint32_t kPgChunkVec = kPgT * kPgU;     // 2048 vectors = 8192 rows
@@ -438,7 +445,7 @@ constexpr uint32_t kPgCold = 0x80000000u;         // tr: cold row, low bits = re
 #define SKX_PG_SLICE_MB 32                        // dimension bytes per partition
 #endif
 #ifndef SKX_PG_MIN_COLD_PERMILLE
-#define SKX_PG_MIN_COLD_PERMILLE 40
+#define SKX_PG_MIN_COLD_PERMILLE 300
 #endif
 // part: ring[2][2048] uint4 | cnt[32][256] | base[64] | bar[2]
 constexpr int kPgRing = 2 * kPgChunkVec * 16;
@@ -466,26 +473,97 @@ __device__ __forceinline__ bool pg_cold(const PgPlan& pl, uint32_t idx) {
   return idx - pl.t < pl.dl - pl.t;  // t <= idx < dl
 }
 
-__global__ void __launch_bounds__(256) k_pg_plan(const uint4* __restrict__ fv, uint64_t nvec,
-                                                 PgPlan pl) {
-  __shared__ uint32_t wsum[8];
-  constexpr uint32_t kS = 4096;  // sampled vectors, evenly spread over the column
-  uint32_t cold = 0;
-  for (uint32_t i = threadIdx.x; i < kS; i += 256) {
-    const uint4 q = fv[(uint64_t)i * nvec / kS];
-    cold += pg_cold(pl, q.x - 1u) + pg_cold(pl, q.y - 1u) + pg_cold(pl, q.z - 1u) +
-            pg_cold(pl, q.w - 1u);
+// plan: should this launch take the partitioned path?  It pays when many rows
+// would miss L2 in the one-pass kernel AND the partitions see each dimension
+// line several times.  A sample of kPlanRuns runs of 64 consecutive rows,
+// spread evenly over the column, is hashed by 128-byte dimension line into a
+// 2^20-bit shared-memory set: a sampled row counts as a miss candidate when
+// its id lies past the L2-resident prefix (idx >= t) and it is the first of
+// the sample on its line.  Hot ids of a skewed column repeat within the
+// sample and rows that walk the dimension in order (permute_dimension over
+// count ties) share lines within their run, so neither counts; uniform or
+// weakly skewed ids do.  The path turns on when the candidates are at least
+// SKX_PG_MIN_COLD_PERMILLE of the sample and the launch's estimated cold rows
+// touch each cold dimension line >= kPlanMinTouch times (fewer: the fill pass
+// would fetch as many HBM lines as the one-pass kernel misses), unless >= 80% of
+// the adjacent id pairs inside the sampled vectors ascend (an in-order walk).
+constexpr uint32_t kPlanRuns = 1024, kPlanRunVec = 16;
+constexpr uint32_t kPlanRows = kPlanRuns * kPlanRunVec * 4;  // 65536 sampled rows
+constexpr uint32_t kPlanBitsLog2 = 20;
+constexpr int kPlanSmem = (1 << kPlanBitsLog2) / 8;          // 128 KB
+constexpr uint32_t kPlanMinTouch = 4;
+
+__global__ void __launch_bounds__(1024) k_pg_plan(const uint4* __restrict__ fv, uint64_t nvec,
+                                                  PgPlan pl, uint32_t line_shift, uint32_t force) {
+  extern __shared__ __align__(16) uint32_t plan_bits[];
+  __shared__ uint32_t wsum[32], wasc[32];
+  const uint32_t tid = threadIdx.x;
+  constexpr int kB = 8;  // sampled vectors in flight per thread
+  const uint64_t span = nvec - kPlanRunVec;  // nvec >= 2^20 (pgather_impl)
+  uint4 q[kB];
+#pragma unroll
+  for (int k = 0; k < kB; ++k)
+    q[k] = fv[(uint64_t)((tid >> 4) + 64 * k) * span / (kPlanRuns - 1) + (tid & 15)];
+  for (uint32_t i = tid; i < (1u << kPlanBitsLog2) / 128; i += 1024)
+    reinterpret_cast<uint4*>(plan_bits)[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  uint32_t first = 0, asc = 0;
+  for (int half = 0; half < 2; ++half) {
+#pragma unroll
+    for (int k = 0; k < kB; ++k) {
+      const uint32_t ids[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+      asc += (ids[1] > ids[0]) + (ids[2] > ids[1]) + (ids[3] > ids[2]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t idx = ids[j] - 1u;
+        if (pg_cold(pl, idx)) {
+          const uint32_t h = ((idx >> line_shift) * 0x9E3779B1u) >> (32 - kPlanBitsLog2);
+          const uint32_t bit = 1u << (h & 31);
+          first += (atomicOr(plan_bits + (h >> 5), bit) & bit) == 0;
+        }
+      }
+    }
+    if (half == 0) {
+#pragma unroll
+      for (int k = 0; k < kB; ++k)
+        q[k] = fv[(uint64_t)((tid >> 4) + 64 * (k + kB)) * span / (kPlanRuns - 1) + (tid & 15)];
+    }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) cold += __shfl_down_sync(0xffffffffu, cold, o);
-  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = cold;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t c = 0;
-    for (int w = 0; w < 8; ++w) c += wsum[w];
-    pl.ctrl->mode = (uint64_t)c * 1000u >= (uint64_t)kS * 4u * SKX_PG_MIN_COLD_PERMILLE ? 1u : 0u;
-    pl.ctrl->items = 0;
+  for (int o = 16; o > 0; o >>= 1) {
+    first += __shfl_down_sync(0xffffffffu, first, o);
+    asc += __shfl_down_sync(0xffffffffu, asc, o);
   }
+  if ((tid & 31) == 0) {
+    wsum[tid >> 5] = first;
+    wasc[tid >> 5] = asc;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t c = 0, a = 0;
+    for (int w = 0; w < 32; ++w) {
+      c += wsum[w];
+      a += wasc[w];
+    }
+    const uint64_t cold_rows = nvec * 4 / kPlanRows * c;  // estimate for the whole column
+    const uint64_t lines = ((uint64_t)(pl.dl - pl.t) >> line_shift) + 1;
+    // A column that walks the dimension upwards (permute_dimension over runs of
+    // equal counts: ids ascending within a run) fetches each line once, in
+    // address order, in the one-pass kernel: not a case for partitioning.
+    const bool in_order = (uint64_t)a * 10u >= (uint64_t)(kPlanRows / 4 * 3) * 8u;
+    const bool on = (uint64_t)c * 1000u >= (uint64_t)kPlanRows * SKX_PG_MIN_COLD_PERMILLE &&
+                    cold_rows >= lines * kPlanMinTouch && !in_order;
+    pl.ctrl->mode = (on || force) ? 1u : 0u;
+    pl.ctrl->items = 0;
+    pl.ctrl->sample_first = c;
+    pl.ctrl->sample_asc = a;
+  }
+}
+
+// Cached plan (skx_internal.cuh: PgCacheEntry) says "partitioned": arm the control word.
+__global__ void k_pg_arm(PgCtrl* ctrl) {
+  ctrl->mode = 1u;
+  ctrl->items = 0;
 }
 
 __device__ __forceinline__ uint32_t pg_chunk_vecs(uint64_t nvec, uint32_t c) {
@@ -769,12 +847,88 @@ __global__ void __launch_bounds__(kThreads, SKX_GATHER_MINB)
   }
 }
 
-// Returns 1 when the partitioned path does not apply (the caller runs the
-// one-pass kernel alone), else a status; on SKX_OK *gate is the flag the
-// one-pass kernel must be gated on (it runs when the plan turns the path off).
+// ---- plan cache (skx_internal.cuh: PgCacheEntry) ------------------------------
+// A launch never waits for its own plan: the first launch over a column runs
+// the one-pass kernel and, beside it, the plan kernel, whose control word is
+// copied back asynchronously; once the copy has landed, later launches over the
+// same (fact, rows, dimension, length) take the planned path with no plan
+// kernel and no scratch unless the plan says "partitioned".  Every
+// kPgCacheUses launches the plan is refreshed in the background (the cached
+// decision keeps serving until the new one lands).
+static bool pg_same(const PgCacheEntry& e, const void* fact, uint64_t nvec, const void* dim,
+                    uint64_t dim_len, int width) {
+  return e.state != 0 && e.fact == fact && e.dim == dim && e.nvec == nvec &&
+         e.dim_len == dim_len && e.width == width;
+}
+
+// The entry's copy has landed?  Then its decision becomes the served one.
+static void pg_settle(skx_ctx* ctx, int i) {
+  PgCacheEntry& e = ctx->pg_cache[i];
+  if (!e.pending) return;
+  const cudaError_t q = cudaEventQuery(e.ev);
+  if (q == cudaErrorNotReady) return;
+  e.pending = false;
+  if (q != cudaSuccess) {
+    cudaGetLastError();
+    if (!e.known) e.state = 0;
+    return;
+  }
+  e.known = true;
+  e.mode = ctx->pg_host[i * 4];
+  e.first = ctx->pg_host[i * 4 + 2];
+  e.asc = ctx->pg_host[i * 4 + 3];
+  e.uses = 0;
+}
+
+static bool pg_cache_init(skx_ctx* ctx) {
+  if (ctx->pg_host && ctx->pg_dev) return true;
+  if (!ctx->pg_host && cudaHostAlloc(reinterpret_cast<void**>(&ctx->pg_host), kPgCacheSlots * 16,
+                                     cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    ctx->pg_host = nullptr;
+    return false;
+  }
+  if (!ctx->pg_dev && cudaMalloc(reinterpret_cast<void**>(&ctx->pg_dev), kPgCacheSlots * 16) !=
+                          cudaSuccess) {
+    cudaGetLastError();
+    ctx->pg_dev = nullptr;
+    return false;
+  }
+  return true;
+}
+
+// Launches the plan kernel for entry i and the copy of its control word.
+template <typename V>
+static void pg_plan_launch(skx_ctx* ctx, int i, const uint4* fv, uint64_t nvec, const PgPlan& base,
+                           cudaStream_t s) {
+  PgCacheEntry& e = ctx->pg_cache[i];
+  if (!e.ev && cudaEventCreateWithFlags(&e.ev, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    e.ev = nullptr;
+    if (!e.known) e.state = 0;
+    return;
+  }
+  PgPlan pl = base;
+  pl.ctrl = reinterpret_cast<PgCtrl*>(ctx->pg_dev + i * 4);
+  uint32_t line_shift = 0;
+  while ((sizeof(V) << line_shift) < 128) ++line_shift;
+  static_assert(sizeof(PgCtrl) == 16, "PgCtrl is the 4-word record of the plan cache");
+  k_pg_plan<<<1, 1024, kPlanSmem, s>>>(fv, nvec, pl, line_shift, 0u);
+  ctx->launches++;
+  if (cudaMemcpyAsync(ctx->pg_host + i * 4, pl.ctrl, 16, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaEventRecord(e.ev, s) != cudaSuccess) {
+    cudaGetLastError();
+    if (!e.known) e.state = 0;
+    return;
+  }
+  e.pending = true;
+}
+
+// Returns 1 when the one-pass kernel must do this launch, 2 when the
+// partitioned kernels did it, else an error status.
 template <typename V>
 int pgather_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64_t nvec, const V* dim,
-                 uint64_t dim_len, V* out, cudaStream_t s, const PgCtrl** gate) {
+                 uint64_t dim_len, V* out, cudaStream_t s) {
   if constexpr (sizeof(V) < 4) {
     return 1;
   } else {
@@ -783,6 +937,7 @@ int pgather_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64_t nve
     const uint64_t nchunks = (nvec + kPgChunkVec - 1) / kPgChunkVec;
     if (nchunks * kPgChunkRows > 0xFFFFFFFFull) return 1;  // 32-bit record positions
     if (reinterpret_cast<uintptr_t>(out + head) % 16 != 0) return 1;
+    const bool force = (ctx->gather_policy & kPolPartForce) != 0;
     uint32_t shift = 0;
     while (((uint64_t)1 << shift) < ((uint64_t)SKX_PG_SLICE_MB << 20) / sizeof(V)) ++shift;
     while (((dim_len - t + ((uint64_t)1 << shift) - 1) >> shift) > kPgMaxParts) ++shift;
@@ -792,32 +947,84 @@ int pgather_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64_t nve
     pl.shift = shift;
     pl.nparts = (uint32_t)((dim_len - t + ((uint64_t)1 << shift) - 1) >> shift);
     pl.nchunks = (uint32_t)nchunks;
+    const uint4* fv = reinterpret_cast<const uint4*>(fact + head);
+    if (!ctx->pg_attr_set) {  // per device, so per context
+      cudaFuncSetAttribute(k_pg_part, cudaFuncAttributeMaxDynamicSharedMemorySize, kPgPartSmem);
+      cudaFuncSetAttribute(k_pg_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlanSmem);
+      ctx->pg_attr_set = true;
+    }
+    bool on = force;
+    if (!force) {
+      // The cache queries events and enqueues a copy: neither belongs in a captured graph.
+      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+      if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+        cudaGetLastError();
+        return 1;
+      }
+      if (!pg_cache_init(ctx)) return 1;
+      int slot = -1;
+      for (int i = 0; i < kPgCacheSlots && slot < 0; ++i)
+        if (pg_same(ctx->pg_cache[i], fv, nvec, dim, dim_len, (int)sizeof(V))) slot = i;
+      if (slot < 0) {  // a new column: take a slot whose copy is not in flight, plan, run one pass
+        for (int k = 0; k < kPgCacheSlots && slot < 0; ++k) {
+          const int i = (ctx->pg_next + k) % kPgCacheSlots;
+          pg_settle(ctx, i);
+          if (!ctx->pg_cache[i].pending) slot = i;
+        }
+        ctx->last_pg_slot = -1;
+        if (slot < 0) return 1;
+        ctx->pg_next = (slot + 1) % kPgCacheSlots;
+        PgCacheEntry& e = ctx->pg_cache[slot];
+        const cudaEvent_t ev = e.ev;
+        e = PgCacheEntry{};
+        e.ev = ev;
+        e.fact = fv;
+        e.dim = dim;
+        e.nvec = nvec;
+        e.dim_len = dim_len;
+        e.width = (int)sizeof(V);
+        e.state = 1;
+        pg_plan_launch<V>(ctx, slot, fv, nvec, pl, s);
+        ctx->last_pg_slot = slot;
+        ctx->last_pg_path = 0;
+        return 1;
+      }
+      PgCacheEntry& e = ctx->pg_cache[slot];
+      pg_settle(ctx, slot);
+      ctx->last_pg_slot = slot;
+      ctx->last_pg_path = 0;
+      if (e.state == 0 || !e.known) return 1;  // its first plan is still on its way
+      if (!e.pending && ++e.uses > kPgCacheUses) {  // the column may have been rewritten
+        e.uses = 0;
+        pg_plan_launch<V>(ctx, slot, fv, nvec, pl, s);
+      }
+      on = e.mode != 0;
+      if (!on) return 1;
+    }
     const uint64_t recs = nchunks * kPgChunkRows;
     auto up = [](uint64_t b) { return (size_t)((b + 255) & ~uint64_t(255)); };
     const size_t ends_b = up(nchunks * 32 * 2), keys_b = up(recs * 4), tr_b = up(nvec * 16);
     char* sp = static_cast<char*>(
         scratch(ctx, 1, 256 + ends_b + keys_b + tr_b + recs * sizeof(V), s));
-    if (!sp) return set_error(ctx, SKX_CUDA_ERROR, "gather: out of device memory (partitioned path)");
+    if (!sp) {  // the path is an optimisation: without room for its records the one-pass kernel runs
+      cudaGetLastError();
+      return 1;
+    }
     pl.ctrl = reinterpret_cast<PgCtrl*>(sp);
     pl.ends = reinterpret_cast<uint16_t*>(sp + 256);
     pl.keys = reinterpret_cast<uint32_t*>(sp + 256 + ends_b);
     pl.tr = reinterpret_cast<uint32_t*>(sp + 256 + ends_b + keys_b);
     pl.vals = sp + 256 + ends_b + keys_b + tr_b;
-    const uint4* fv = reinterpret_cast<const uint4*>(fact + head);
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaFuncSetAttribute(k_pg_part, cudaFuncAttributeMaxDynamicSharedMemorySize, kPgPartSmem);
-      attr_set = true;
-    }
-    k_pg_plan<<<1, 256, 0, s>>>(fv, nvec, pl);
+    k_pg_arm<<<1, 1, 0, s>>>(pl.ctrl);
     k_pg_part<<<grid_for(ctx, nchunks, 1, 2), kPgT, kPgPartSmem, s>>>(fv, head, nvec, pl, ctx->err);
     k_pg_fill<V><<<grid_for(ctx, (uint64_t)pl.nparts * nchunks, kPgFillChunks, 8), 256, 0, s>>>(
         dim, pl);
     k_pg_emit<V><<<grid_for(ctx, nvec, kThreads * kUnroll, 8), kThreads, 0, s>>>(nvec, dim,
                                                                                 out + head, pl);
     ctx->launches += 4;
-    *gate = pl.ctrl;
-    return SKX_OK;
+    ctx->last_pg_path = 1;
+    if (force) ctx->last_pg_slot = -1;
+    return 2;
   }
 }
 
@@ -840,12 +1047,15 @@ int gather_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const V* dim, ui
     const uintptr_t oa = reinterpret_cast<uintptr_t>(out + head);
     const bool out_vec = (sizeof(V) == 2) ? (oa % 8 == 0) : (oa % 16 == 0);
     int F = ctx->gather_policy;
-    const PgCtrl* gate = nullptr;
+    const PgCtrl* gate = nullptr;  // the one-pass kernel's gate word (unused: plans are cached)
+    int pg = 1;
+    ctx->last_pg_slot = -1;
+    ctx->last_pg_path = 0;
     if (F & kPolPart) {
-      const int rc = pgather_impl<V>(ctx, fact, head, nvec, dim, dim_len, out, s, &gate);
-      if (rc != 1 && rc != SKX_OK) return rc;
+      pg = pgather_impl<V>(ctx, fact, head, nvec, dim, dim_len, out, s);
+      if (pg != 1 && pg != 2) return pg;
     }
-    F &= ~kPolPart;
+    F &= ~(kPolPart | kPolPartForce);
     // Shared-memory tier: as many leading dimension values as fit.
     uint32_t hot = 0;
     if ((F & kPolHot) && (reinterpret_cast<uintptr_t>(dim) % 16) == 0) {
@@ -864,11 +1074,13 @@ int gather_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const V* dim, ui
       t.t1 = hot + (uint64_t)ctx->tier_l1_bytes / sizeof(V);
       t.t2 = (uint64_t)((double)ctx->l2_bytes * ctx->tier_l2_frac) / sizeof(V);
     }
-    const cudaError_t e =
-        out_vec ? dispatch_vec<V, true>(ctx, F, fact, head, nvec, dim, dim_len, out, t, s, gate)
-                : dispatch_vec<V, false>(ctx, F, fact, head, nvec, dim, dim_len, out, t, s, gate);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "gather launch");
-    ctx->launches++;
+    if (pg != 2) {  // 2: a cached plan sent the whole launch down the partitioned path
+      const cudaError_t e =
+          out_vec ? dispatch_vec<V, true>(ctx, F, fact, head, nvec, dim, dim_len, out, t, s, gate)
+                  : dispatch_vec<V, false>(ctx, F, fact, head, nvec, dim, dim_len, out, t, s, gate);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "gather launch");
+      ctx->launches++;
+    }
   }
   if (tail_b < n) {
     k_gather_scalar<V><<<1, 32, 0, s>>>(fact, tail_b, n, dim, dim_len, out, ctx->err);
@@ -993,6 +1205,25 @@ int skx_gather_u32(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uint32_
 int skx_gather_u64(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uint64_t* dim,
                    uint64_t dim_len, uint64_t* out, void* stream) {
   return skx::launch_gather(ctx, 8, fact, n, dim, dim_len, out, skx::as_stream(stream));
+}
+
+int skx_gather_last_plan(skx_ctx* ctx, uint32_t* info, void* stream) {
+  if (!ctx || !info) return SKX_INVALID_ARGUMENT;
+  skx::bind(ctx);
+  info[0] = ctx->last_pg_path;
+  info[1] = info[2] = 0;
+  info[3] = ctx->last_pg_path;  // a forced launch has no plan: it took the path it was told to
+  const int i = ctx->last_pg_slot;
+  if (i < 0) return SKX_OK;
+  const cudaError_t e = cudaStreamSynchronize(skx::as_stream(stream));
+  if (e != cudaSuccess) return skx::cuda_fail(ctx, e, "gather_last_plan");
+  skx::PgCacheEntry& pe = ctx->pg_cache[i];
+  if (pe.pending && pe.ev) cudaEventSynchronize(pe.ev);
+  skx::pg_settle(ctx, i);
+  info[1] = pe.first;
+  info[2] = pe.asc;
+  info[3] = pe.known ? pe.mode : 0;
+  return SKX_OK;
 }
 
 int skx_recode_fact(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const uint32_t* ranks,

@@ -151,6 +151,27 @@ struct ScratchSet {
   uint32_t sel_ncat = 0;
 };
 
+// Plan cache of the partitioned gather (gather.cu): the device-side plan of a
+// (fact column, dimension) pair is copied back asynchronously, and once it has
+// arrived launches over the same pair follow it -- a stale entry can only cost
+// time, never change a result (both paths compute the same bytes); plans are
+// refreshed every kPgCacheUses launches (a buffer reused for another column is
+// re-planned soon) and skx_set_gather_policy drops them all.
+constexpr int kPgCacheSlots = 8;
+constexpr uint32_t kPgCacheUses = 16;
+struct PgCacheEntry {
+  const void* fact = nullptr;
+  const void* dim = nullptr;
+  uint64_t nvec = 0, dim_len = 0;
+  int width = 0;
+  int state = 0;         // 0 empty, 1 in use
+  bool known = false;    // mode / first / asc hold a landed plan
+  bool pending = false;  // a plan's copy is in flight (event ev)
+  uint32_t mode = 0, first = 0, asc = 0;
+  uint32_t uses = 0;
+  cudaEvent_t ev = nullptr;
+};
+
 }  // namespace skx
 
 struct skx_ctx {
@@ -161,6 +182,13 @@ struct skx_ctx {
   skx::DevErr* err = nullptr;       // device
   skx::DevErr* err_host = nullptr;  // pinned mirror
   uint64_t last_domain = 0;
+  bool pg_attr_set = false;            // shared-memory opt-in of the k_pg_* kernels done
+  skx::PgCacheEntry pg_cache[skx::kPgCacheSlots];
+  uint32_t* pg_host = nullptr;         // pinned: 4 words (PgCtrl) per cache slot
+  uint32_t* pg_dev = nullptr;          // device: the plan kernels' control words, same layout
+  int pg_next = 0;                     // next slot to evict
+  int last_pg_slot = -1;               // cache slot of the last gather launch (-1: none)
+  uint32_t last_pg_path = 0;           // 1: the last gather launch ran the partitioned kernels
   int gather_policy = 129 | 8192;  // L2 hints + .cs streams + partitioned cold rows
   size_t persist_max = 0;  // cudaDevAttrMaxPersistingL2CacheSize (0: no windows)
   size_t window_max = 0;   // cudaDevAttrMaxAccessPolicyWindowSize

@@ -93,6 +93,16 @@ class Context:
     def set_gather_policy(self, policy: int) -> None:
         self.check(self.lib.skx_set_gather_policy(self.handle, policy))
 
+    def gather_last_plan(self, stream=None) -> dict:
+        """The last gather launch of this context (include/skx.h, policy bit
+        8192): the path it took, its column's plan and the plan's sample."""
+        info = (C.c_uint32 * 4)()
+        self.check(self.lib.skx_gather_last_plan(
+            self.handle, info, stream if stream is not None else self.stream()))
+        return {"partitioned": bool(info[0]), "plan_partitioned": bool(info[3]),
+                "sample_first_touch": int(info[1]), "sample_ascending_pairs": int(info[2]),
+                "sample_rows": 65536}
+
     def call(self, name: str, *args, sync: bool = True):
         self.check(getattr(self.lib, name)(self.handle, *args))
         if sync:

@@ -705,48 +705,116 @@ def test_gather_output_store_policies(sx, policy):
 
 @pytest.mark.parametrize("npdt", [np.uint32, np.uint64])
 def test_gather_partitioned(sx, oracle, npdt):
-    """The partitioned gather (policy bit 8192, the default): cold rows
-    radix-partitioned by key range, their values fetched slice by slice and
-    merged back at the slots each chunk recomputes.  Same bytes as the one-pass
-    kernel (policy 129) and numpy, for Zipf and uniform ids (path on) and
-    hot-only ids (the plan turns it off), ragged sizes with partial last
-    chunks, misaligned heads, many partitions, and the first bad row."""
+    """The partitioned gather (policy bit 8192): cold rows radix-partitioned by
+    key range, their values fetched slice by slice and merged back at the slots
+    each chunk recorded.  Same bytes as the one-pass kernel (policy 129) and
+    numpy with the path forced on (bit 16384) and under the plan's own gate,
+    for Zipf, uniform and hot-only ids, ragged sizes with partial last chunks,
+    misaligned heads, one and ~30 partitions, and the first bad row."""
     from paper_1910_10063_b200 import DomainViolation
     ctx = sx.context(0)
     rng = np.random.default_rng(11)
     w = np.dtype(npdt).itemsize
     hot = (32 << 20) // w                      # the direct prefix (SKX_PG_HOT_MB)
-    for d in [2 * hot + 1, (1 << 30) // w + 12345]:   # 1 and ~30 partitions
-        dim_np = rng.integers(0, np.iinfo(npdt).max, size=d, dtype=npdt)
-        dim = cu(dim_np)
-        cdf = oracle.zipf_cdf(d, 0.9)
-        cases = [("zipf", oracle.generate_zipf_counter(cdf, None, 7, 0, (1 << 22) + 8192 * 3 + 5)),
-                 ("uniform", rng.integers(1, d + 1, size=(1 << 23) + 3, dtype=np.uint32)),
-                 ("hot_only", rng.integers(1, hot // 2, size=(1 << 22) + 1, dtype=np.uint32))]
-        del cdf
-        for name, fact_np in cases:
-            n = fact_np.size - 1
-            full = cu(fact_np)
-            for off in (0, 1, 3):
-                exp = dim_np[fact_np[off: off + n].astype(np.int64) - 1]
-                out = sx.materialize(full[off: off + n], dim)
-                assert np.array_equal(np_(out).view(npdt), exp), (d, name, off)
-            ctx.set_gather_policy(129)
-            try:
+    try:
+        for d in [2 * hot + 1, (1 << 30) // w + 12345]:   # 1 and ~30 partitions
+            dim_np = rng.integers(0, np.iinfo(npdt).max, size=d, dtype=npdt)
+            dim = cu(dim_np)
+            cdf = oracle.zipf_cdf(d, 0.9)
+            cases = [("zipf", oracle.generate_zipf_counter(cdf, None, 7, 0, (1 << 22) + 8192 * 3 + 5)),
+                     ("uniform", rng.integers(1, d + 1, size=(1 << 23) + 3, dtype=np.uint32)),
+                     ("hot_only", rng.integers(1, hot // 2, size=(1 << 22) + 1, dtype=np.uint32))]
+            del cdf
+            for name, fact_np in cases:
+                n = fact_np.size - 1
+                full = cu(fact_np)
+                for pol in (129 | 8192 | 16384, 129 | 8192):
+                    ctx.set_gather_policy(pol)
+                    for off in (0, 1, 3):
+                        exp = dim_np[fact_np[off: off + n].astype(np.int64) - 1]
+                        # under the gate: the first launch plans beside the one-pass
+                        # kernel, the second follows the landed plan
+                        for rep in range(1 if pol & 16384 else 2):
+                            out = sx.materialize(full[off: off + n], dim)
+                            assert np.array_equal(np_(out).view(npdt), exp), (d, name, off, pol, rep)
+                            plan = ctx.gather_last_plan()
+                            if pol & 16384:
+                                # a fresh (aligned) output behind a misaligned FK head cannot
+                                # take 16-byte stores: those launches stay one-pass
+                                assert plan["partitioned"] == (off == 0), (d, name, off)
+                            else:
+                                assert plan["partitioned"] == (rep == 1 and plan["plan_partitioned"])
+                                if name == "hot_only":
+                                    assert not plan["plan_partitioned"]
+                                    assert plan["sample_first_touch"] == 0
+                ctx.set_gather_policy(129)
                 one = sx.materialize(full[1: 1 + n], dim)
-            finally:
-                ctx.set_gather_policy(129 | 8192)
-            assert np.array_equal(np_(one).view(npdt), dim_np[fact_np[1: 1 + n].astype(np.int64) - 1])
-        # first bad row, path on (uniform ids) and off (hot ids)
-        for name, hi in (("on", d), ("off", hot // 2)):
-            fact_np = rng.integers(1, hi + 1, size=(1 << 22) + 7, dtype=np.uint32)
-            fact_np[3_000_001] = d + 9
-            fact_np[3_500_000] = 0
-            with pytest.raises(DomainViolation) as e:
-                sx.materialize(cu(fact_np), dim)
-            assert e.value.row() == 3_000_001 and e.value.value() == d + 9, name
-        del dim, dim_np
-        torch.cuda.empty_cache()
+                assert np.array_equal(np_(one).view(npdt),
+                                      dim_np[fact_np[1: 1 + n].astype(np.int64) - 1])
+            # first bad row, path forced on and under the gate
+            for pol in (129 | 8192 | 16384, 129 | 8192):
+                ctx.set_gather_policy(pol)
+                for name, hi in (("cold", d), ("hot", hot // 2)):
+                    fact_np = rng.integers(1, hi + 1, size=(1 << 22) + 7, dtype=np.uint32)
+                    fact_np[3_000_001] = d + 9
+                    fact_np[3_500_000] = 0
+                    with pytest.raises(DomainViolation) as e:
+                        sx.materialize(cu(fact_np), dim)
+                    assert e.value.row() == 3_000_001 and e.value.value() == d + 9, (name, pol)
+            del dim, dim_np
+            torch.cuda.empty_cache()
+    finally:
+        ctx.set_gather_policy(129 | 8192)
+
+
+@pytest.mark.parametrize("npdt", [np.uint32, np.uint64])
+def test_gather_plan_gate(sx, oracle, npdt):
+    """The plan's decisions (made beside a column's first launch, followed from
+    the second) on the access patterns the index produces: uniform
+    ids over a 1 GiB dimension with enough rows per line -> partitioned; a
+    strongly skewed scattered column (recode at s=1.25), in-order walks
+    (permute over count ties: ascending ids with small random gaps) and too
+    few rows per dimension line -> one pass.
+    The result is checked against numpy either way."""
+    ctx = sx.context(0)
+    rng = np.random.default_rng(5)
+    w = np.dtype(npdt).itemsize
+    d = (256 << 20) // w
+    dim_np = rng.integers(0, np.iinfo(npdt).max, size=d, dtype=npdt)
+    dim = cu(dim_np)
+    n = 1 << 24                      # 8 rows per 128-byte line of the 256 MiB dimension
+    cdf = oracle.zipf_cdf(d, 1.25)
+    perm = oracle.random_bijection(d, 3)
+    walk = (np.arange(n, dtype=np.uint64) * 3 % d + 1).astype(np.uint32)
+    cases = [("uniform", rng.integers(1, d + 1, size=n, dtype=np.uint32), True),
+             ("zipf1.25_scattered", oracle.generate_zipf_counter(cdf, perm, 9, 0, n), False),
+             ("in_order", walk, False),
+             ("tie_runs", (np.cumsum(rng.integers(1, 10, size=n)) % d + 1).astype(np.uint32), False),
+             ("few_rows", rng.integers(1, d + 1, size=1 << 22, dtype=np.uint32), False)]
+    for name, fact_np, want in cases:
+        fact = cu(fact_np)
+        ctx.set_gather_policy(129 | 8192)   # drops cached plans (the allocator reuses addresses)
+        exp = dim_np[fact_np.astype(np.int64) - 1]
+        before = ctx.launches()
+        out = sx.materialize(fact, dim)
+        assert ctx.launches() - before == 2, name          # one-pass kernel + plan kernel
+        assert np.array_equal(np_(out).view(npdt), exp), name
+        plan = ctx.gather_last_plan()
+        assert not plan["partitioned"] and plan["plan_partitioned"] == want, (name, plan)
+        # the same column again follows the landed plan: the four partitioned
+        # kernels or the one-pass kernel alone, no plan kernel; same bytes
+        before = ctx.launches()
+        out2 = sx.materialize(fact, dim)
+        assert ctx.launches() - before == (4 if want else 1), (name, ctx.launches() - before)
+        assert np.array_equal(np_(out2).view(npdt), exp), name
+        plan2 = ctx.gather_last_plan()
+        assert plan2["partitioned"] == want and plan2["plan_partitioned"] == want, (name, plan2)
+        assert plan2["sample_first_touch"] == plan["sample_first_touch"]
+        # a rewritten column under a stale "partitioned" plan still gathers exactly
+        if want:
+            fact.view(torch.int32).copy_(cu(np.minimum(fact_np, 1000)).view(torch.int32))
+            out3 = sx.materialize(fact, dim)
+            assert np.array_equal(np_(out3).view(npdt), dim_np[np.minimum(fact_np, 1000).astype(np.int64) - 1])
 
 
 @pytest.mark.parametrize("dtype,npdt", [(torch.uint32, np.uint32), (torch.int64, np.int64)])
