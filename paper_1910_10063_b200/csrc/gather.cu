@@ -444,6 +444,9 @@ constexpr uint32_t kPgCold = 0x80000000u;         // tr: cold row, low bits = re
 #ifndef SKX_PG_SLICE_MB
 #define SKX_PG_SLICE_MB 32                        // dimension bytes per partition
 #endif
+#ifndef SKX_PG_EMIT_STAGED
+#define SKX_PG_EMIT_STAGED 1                      // emit reads a chunk's records through shared memory
+#endif
 #ifndef SKX_PG_MIN_COLD_PERMILLE
 #define SKX_PG_MIN_COLD_PERMILLE 300
 #endif
@@ -739,6 +742,7 @@ __global__ void __launch_bounds__(256)
   const uint32_t items = nblk * pl.nparts;
   V* vals = static_cast<V*>(pl.vals);
   const uint64_t pol_s = policy_evict_first();
+  const uint64_t pol_d = policy_evict_last();
   for (;;) {
     if (tid == 0) s_item = atomicAdd(&pl.ctrl->items, 1u);
     __syncthreads();
@@ -785,13 +789,15 @@ __global__ void __launch_bounds__(256)
           key[r] = ld_stream_u32(pl.keys + pos[r], pol_s);
         }
       }
+      // the slice must outlive the record streams in L2: evict_last loads (no L1
+      // allocation: the reads are random), streaming stores
       V v[4];
 #pragma unroll
       for (int r = 0; r < 4; ++r)
-        if (pos[r] != 0xffffffffu) v[r] = __ldg(dim + key[r]);
+        if (pos[r] != 0xffffffffu) v[r] = ld_dim_nol1<V>(dim + key[r], pol_d);
 #pragma unroll
       for (int r = 0; r < 4; ++r)
-        if (pos[r] != 0xffffffffu) vals[pos[r]] = v[r];
+        if (pos[r] != 0xffffffffu) __stcs(vals + pos[r], v[r]);
     }
     __syncthreads();  // sb / soff / s_item are rewritten for the next item
   }
@@ -844,6 +850,80 @@ __global__ void __launch_bounds__(kThreads, SKX_GATHER_MINB)
         }
       }
     }
+  }
+}
+
+// emit, records staged: the chunk's records come into shared memory with one 1-D TMA copy (each
+// byte read once, however the CTA's lanes then address them), overlapped with the chunk's
+// translated-column loads and hot dimension reads.  One CTA per chunk at a time.
+template <typename V>
+__global__ void __launch_bounds__(kThreads)
+    k_pg_emit_s(uint64_t nvec, const V* __restrict__ dim, V* __restrict__ o, PgPlan pl) {
+  static_assert(kThreads * kUnroll == (int)kPgChunkVec, "one emit iteration is one chunk");
+  extern __shared__ __align__(128) unsigned char pg_raw[];
+  V* rec = reinterpret_cast<V*>(pg_raw);                                   // [kPgChunkRows]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(pg_raw + kPgChunkRows * sizeof(V));
+  const uint32_t tid = threadIdx.x;
+  const uint64_t pol_s = policy_evict_first();
+  const uint64_t pol_d = policy_evict_last();
+  const uint4* trv = reinterpret_cast<const uint4*>(pl.tr);
+  const V* vals = static_cast<const V*>(pl.vals);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t k = 0;
+  for (uint32_t c = blockIdx.x; c < pl.nchunks; c += gridDim.x, ++k) {
+    if (tid == 0) {
+      const uint32_t total = pl.ends[(size_t)c * 32 + pl.nparts - 1];
+      uint32_t bytes = (uint32_t)((total * sizeof(V) + 15) & ~size_t(15));  // inside the chunk's region
+      if (bytes == 0) bytes = 16;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                   "r"(bytes)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+          "[%1], %2, [%3], %4;" ::"r"(smem_u32(rec)),
+          "l"(vals + (uint64_t)c * kPgChunkRows), "r"(bytes), "r"(smem_u32(bar)), "l"(pol_s)
+          : "memory");
+    }
+    const uint64_t base = (uint64_t)c * kPgChunkVec + tid;
+    uint4 f[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint64_t vi = base + (uint64_t)u * kThreads;
+      f[u] = vi < nvec ? __ldcs(trv + vi) : make_uint4(~0u, ~0u, ~0u, ~0u);
+    }
+    V v[kUnroll][4];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t w[4] = {f[u].x, f[u].y, f[u].z, f[u].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[u][j] = w[j] < kPgCold ? ld_dim<V>(dim + w[j], pol_d, true) : (V)0;
+    }
+    pg_wait(bar, 0, k & 1);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t w[4] = {f[u].x, f[u].y, f[u].z, f[u].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (w[j] >= kPgCold && w[j] != 0xffffffffu) v[u][j] = rec[w[j] & ~kPgCold];
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint64_t vi = base + (uint64_t)u * kThreads;
+      if (vi < nvec) {
+        if constexpr (sizeof(V) == 8) {
+          __stcs(reinterpret_cast<ulonglong2*>(o + vi * 4), make_ulonglong2(v[u][0], v[u][1]));
+          __stcs(reinterpret_cast<ulonglong2*>(o + vi * 4) + 1, make_ulonglong2(v[u][2], v[u][3]));
+        } else {
+          Pack4<V>::store(o + vi * 4, v[u], pol_s);
+        }
+      }
+    }
+    __syncthreads();  // every lane has read its records before the next chunk's copy lands
   }
 }
 
@@ -1019,8 +1099,14 @@ int pgather_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64_t nve
     k_pg_part<<<grid_for(ctx, nchunks, 1, 2), kPgT, kPgPartSmem, s>>>(fv, head, nvec, pl, ctx->err);
     k_pg_fill<V><<<grid_for(ctx, (uint64_t)pl.nparts * nchunks, kPgFillChunks, 8), 256, 0, s>>>(
         dim, pl);
+#if SKX_PG_EMIT_STAGED
+    constexpr int kEmitSmem = (int)(kPgChunkRows * sizeof(V)) + 16;
+    cudaFuncSetAttribute(k_pg_emit_s<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmem);
+    k_pg_emit_s<V><<<grid_for(ctx, nchunks, 1, 8), kThreads, kEmitSmem, s>>>(nvec, dim, out + head, pl);
+#else
     k_pg_emit<V><<<grid_for(ctx, nvec, kThreads * kUnroll, 8), kThreads, 0, s>>>(nvec, dim,
                                                                                 out + head, pl);
+#endif
     ctx->launches += 4;
     ctx->last_pg_path = 1;
     if (force) ctx->last_pg_slot = -1;

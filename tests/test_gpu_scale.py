@@ -109,6 +109,27 @@ def test_c2_gather_at_scale(env, oracle, z):
     out.fill_(0)
     sx.materialize(g.fact_rand, g.dim_rand, out=out)  # original layout
     assert same(out, exp)
+    # The first launch over a column runs the one-pass kernel and plans beside it; from the
+    # second launch the landed plan is followed (include/skx.h, policy bit 8192).  Check the
+    # planned path's bytes at full size too, and which path each BASELINE column takes.
+    ctx = sx.context(0)
+    for lay, f, dm, want in (("freq", g.fact_freq, g.dim_freq, z < 1.0),
+                             ("rand", g.fact_rand, g.dim_rand, z <= 1.0)):
+        for rep in range(2):
+            out.fill_(0)
+            sx.materialize(f, dm, out=out)
+            plan = ctx.gather_last_plan()
+            assert same(out, exp), (lay, rep)
+        assert plan["partitioned"] == want and plan["plan_partitioned"] == want, (z, lay, plan)
+    # recode of the original-layout column over the 512 MB rank table, planned path
+    # (g.fact_freq, the first launch's result, was compared with the oracle above)
+    rec = torch.empty_like(g.fact_rand)
+    for rep in range(2):
+        rec.fill_(0)
+        sx.recode_fact(g.fact_rand, g.index, out=rec)
+        assert torch.equal(rec.view(torch.int32), g.fact_freq.view(torch.int32)), rep
+    assert ctx.gather_last_plan()["partitioned"] == (z <= 1.0)
+    del rec
     if z == 1.0:  # the threshold-split two-pass gather (materialize_split) at full size
         out.fill_(0)
         sx.materialize_split(g.fact_freq, g.dim_freq, 1 << 23, out=out)
