@@ -789,12 +789,12 @@ __global__ void __launch_bounds__(256)
           key[r] = ld_stream_u32(pl.keys + pos[r], pol_s);
         }
       }
-      // the slice must outlive the record streams in L2: evict_last loads (no L1
-      // allocation: the reads are random), streaming stores
+      // the slice must outlive the record streams in L2: evict_last loads (L1-allocating:
+      // the hot ids of a scattered skewed column repeat), streaming stores
       V v[4];
 #pragma unroll
       for (int r = 0; r < 4; ++r)
-        if (pos[r] != 0xffffffffu) v[r] = ld_dim_nol1<V>(dim + key[r], pol_d);
+        if (pos[r] != 0xffffffffu) v[r] = ld_dim<V>(dim + key[r], pol_d, true);
 #pragma unroll
       for (int r = 0; r < 4; ++r)
         if (pos[r] != 0xffffffffu) __stcs(vals + pos[r], v[r]);
