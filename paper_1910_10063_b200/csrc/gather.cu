@@ -64,10 +64,10 @@ struct GatherTiers {
   uint64_t t2;
 };
 
-// Control word of the partitioned gather (below); the one-pass kernel runs
-// only when its plan leaves the path off.
+// Control word of the partitioned gather (below): the plan kernel's verdict and
+// sample (copied to the host's plan cache), and the fill pass's work counter.
 struct PgCtrl {
-  uint32_t mode;          // 1: partitioned
+  uint32_t mode;          // plan: 1 = partition this column
   uint32_t items;         // fill work-item counter
   uint32_t sample_first;  // plan: sampled rows that were miss candidates (of 65536)
   uint32_t sample_asc;    // plan: ascending adjacent id pairs within the sampled vectors (of 49152)
@@ -155,8 +155,7 @@ template <typename V, bool OUT_VEC, int F>
 __global__ void __launch_bounds__((F & kPolHot) ? kThreadsHot : kThreads, (F & kPolHot) ? 1 : SKX_GATHER_MINB)
     k_gather_vec(const uint32_t* __restrict__ fact, uint64_t head, uint64_t nvec,
                  const V* __restrict__ dim, uint64_t dim_len, V* __restrict__ out, DevErr* err,
-                 GatherTiers tiers, const PgCtrl* gate) {
-  if (gate && gate->mode != 0) return;  // the partitioned path does this launch's work
+                 GatherTiers tiers) {
   constexpr bool HOT = (F & kPolHot) != 0;
   constexpr bool HINTS = (F & kPolHints) != 0;
   constexpr bool NOL1 = (F & kPolNoL1) != 0;
@@ -338,8 +337,7 @@ __global__ void k_gather_scalar(const uint32_t* __restrict__ fact, uint64_t b, u
 
 template <typename V, bool OUT_VEC, int F>
 cudaError_t launch_vec(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64_t nvec,
-                       const V* dim, uint64_t dim_len, V* out, GatherTiers tiers, cudaStream_t s,
-                       const PgCtrl* gate) {
+                       const V* dim, uint64_t dim_len, V* out, GatherTiers tiers, cudaStream_t s) {
   const uint32_t hot = tiers.hot;
   constexpr bool HOT = (F & kPolHot) != 0;
   cudaLaunchConfig_t cfg = {};
@@ -381,20 +379,19 @@ cudaError_t launch_vec(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64
     cudaFuncSetAttribute(k_gather_vec<V, OUT_VEC, F>,
                          cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxL1);
   return cudaLaunchKernelEx(&cfg, k_gather_vec<V, OUT_VEC, F>, fact, head, nvec, dim, dim_len, out,
-                            ctx->err, tiers, gate);
+                            ctx->err, tiers);
 }
 
 template <typename V, bool OUT_VEC>
 cudaError_t dispatch_vec(skx_ctx* ctx, int F, const uint32_t* fact, uint64_t head, uint64_t nvec,
-                         const V* dim, uint64_t dim_len, V* out, GatherTiers t, cudaStream_t s,
-                         const PgCtrl* gate) {
+                         const V* dim, uint64_t dim_len, V* out, GatherTiers t, cudaStream_t s) {
   // Bit 4 (window) is a launch attribute; instantiate the useful variants only.
   const bool win = (F & kPolWindow) != 0;
 #define SKX_F(x)                                                                            \
   if ((F & ~kPolWindow) == (x))                                                             \
     return win ? launch_vec<V, OUT_VEC, (x) | kPolWindow>(ctx, fact, head, nvec, dim, dim_len, \
-                                                          out, t, s, gate)                  \
-               : launch_vec<V, OUT_VEC, (x)>(ctx, fact, head, nvec, dim, dim_len, out, t, s, gate);
+                                                          out, t, s)                  \
+               : launch_vec<V, OUT_VEC, (x)>(ctx, fact, head, nvec, dim, dim_len, out, t, s);
   SKX_F(0) SKX_F(1) SKX_F(3) SKX_F(9) SKX_F(17) SKX_F(19)
   SKX_F(33) SKX_F(35) SKX_F(49) SKX_F(51) SKX_F(65) SKX_F(97) SKX_F(69) SKX_F(129) SKX_F(128)
   SKX_F(131) SKX_F(385) SKX_F(641) SKX_F(1153) SKX_F(2177) SKX_F(4225)
@@ -410,10 +407,10 @@ cudaError_t dispatch_vec(skx_ctx* ctx, int F, const uint32_t* fact, uint64_t hea
 // rows are two thirds of the launch.  Here they are radix-partitioned by key
 // range instead, so each partition's dimension slice is read while it sits in
 // L2 -- the GPU form of a partitioned hash join.  Over 8192-row chunks:
-//   plan : one CTA samples 64 K rows and turns the path on only when enough of
-//          them would miss L2 in the one-pass kernel to pay for the extra
-//          passes (k_pg_plan below); when it is off only the one-pass kernel
-//          (gated on the same flag) works;
+//   plan : beside a column's first (one-pass) launch one CTA samples 64 K rows and
+//          decides whether enough of them would miss L2 in the one-pass kernel
+//          to pay for the extra passes (k_pg_plan below); the decision reaches
+//          the host asynchronously and later launches over the column follow it;
 //   part : FK through a double-buffered 1-D TMA ring in shared memory; the
 //          chunk's cold keys go to its record segment grouped by partition
 //          (keys[]), and every row gets a translated word tr[] = its id - 1
@@ -428,7 +425,7 @@ cudaError_t dispatch_vec(skx_ctx* ctx, int F, const uint32_t* fact, uint64_t hea
 // every row behind the previous one); an exclusive scan over (partition,
 // thread) turns the counts into slots.
 constexpr int kPolPart = 8192;
-constexpr int kPolPartForce = 16384;  // with kPolPart: skip the plan's gate (tests, measurements)
+constexpr int kPolPartForce = 16384;  // with kPolPart: partition at once, no plan (tests, measurements)
 constexpr int kPgT = 256;                         // threads per CTA (part)
 constexpr int kPgU = 8;                           // FK vectors per thread per chunk
 constexpr uint32_t kPgChunkVec = kPgT * kPgU;     // 2048 vectors = 8192 rows
@@ -563,7 +560,7 @@ __global__ void __launch_bounds__(1024) k_pg_plan(const uint4* __restrict__ fv, 
   }
 }
 
-// Cached plan (skx_internal.cuh: PgCacheEntry) says "partitioned": arm the control word.
+// Before the three passes: reset the fill pass's work-item counter.
 __global__ void k_pg_arm(PgCtrl* ctrl) {
   ctrl->mode = 1u;
   ctrl->items = 0;
@@ -601,7 +598,6 @@ __device__ __forceinline__ void pg_wait(uint64_t* bar, int b, uint32_t parity) {
 // part: per chunk, the cold keys grouped by partition and the translated FK.
 __global__ void __launch_bounds__(kPgT, 2)
     k_pg_part(const uint4* __restrict__ fv, uint64_t head, uint64_t nvec, PgPlan pl, DevErr* err) {
-  if (pl.ctrl->mode == 0) return;
   extern __shared__ __align__(128) unsigned char pg_raw[];
   uint4* ring = reinterpret_cast<uint4*>(pg_raw);  // [2][kPgChunkVec]
   uint32_t* cnt = reinterpret_cast<uint32_t*>(pg_raw + kPgRing);
@@ -733,7 +729,6 @@ __global__ void __launch_bounds__(kPgT, 2)
 template <typename V>
 __global__ void __launch_bounds__(256)
     k_pg_fill(const V* __restrict__ dim, PgPlan pl) {
-  if (pl.ctrl->mode == 0) return;
   __shared__ uint32_t sb[kPgFillChunks];
   __shared__ uint32_t soff[kPgFillChunks + 1];
   __shared__ uint32_t s_item;
@@ -807,7 +802,6 @@ __global__ void __launch_bounds__(256)
 template <typename V>
 __global__ void __launch_bounds__(kThreads, SKX_GATHER_MINB)
     k_pg_emit(uint64_t nvec, const V* __restrict__ dim, V* __restrict__ o, PgPlan pl) {
-  if (pl.ctrl->mode == 0) return;
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_d = policy_evict_last();
   const uint4* trv = reinterpret_cast<const uint4*>(pl.tr);
@@ -1133,7 +1127,6 @@ int gather_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const V* dim, ui
     const uintptr_t oa = reinterpret_cast<uintptr_t>(out + head);
     const bool out_vec = (sizeof(V) == 2) ? (oa % 8 == 0) : (oa % 16 == 0);
     int F = ctx->gather_policy;
-    const PgCtrl* gate = nullptr;  // the one-pass kernel's gate word (unused: plans are cached)
     int pg = 1;
     ctx->last_pg_slot = -1;
     ctx->last_pg_path = 0;
@@ -1162,8 +1155,8 @@ int gather_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t n, const V* dim, ui
     }
     if (pg != 2) {  // 2: a cached plan sent the whole launch down the partitioned path
       const cudaError_t e =
-          out_vec ? dispatch_vec<V, true>(ctx, F, fact, head, nvec, dim, dim_len, out, t, s, gate)
-                  : dispatch_vec<V, false>(ctx, F, fact, head, nvec, dim, dim_len, out, t, s, gate);
+          out_vec ? dispatch_vec<V, true>(ctx, F, fact, head, nvec, dim, dim_len, out, t, s)
+                  : dispatch_vec<V, false>(ctx, F, fact, head, nvec, dim, dim_len, out, t, s);
       if (e != cudaSuccess) return cuda_fail(ctx, e, "gather launch");
       ctx->launches++;
     }
