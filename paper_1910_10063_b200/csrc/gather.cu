@@ -441,6 +441,9 @@ constexpr uint32_t kPgCold = 0x80000000u;         // tr: cold row, low bits = re
 #ifndef SKX_PG_SLICE_MB
 #define SKX_PG_SLICE_MB 32                        // dimension bytes per partition
 #endif
+#ifndef SKX_PG_FILL_CTAS
+#define SKX_PG_FILL_CTAS 6                        // fill CTAs per SM (what its 40 registers allow)
+#endif
 #ifndef SKX_PG_EMIT_STAGED
 #define SKX_PG_EMIT_STAGED 1                      // emit reads a chunk's records through shared memory
 #endif
@@ -729,15 +732,17 @@ __global__ void __launch_bounds__(kPgT, 2)
 template <typename V>
 __global__ void __launch_bounds__(256)
     k_pg_fill(const V* __restrict__ dim, PgPlan pl) {
-  __shared__ uint32_t sb[kPgFillChunks];
-  __shared__ uint32_t soff[kPgFillChunks + 1];
+  __shared__ uint32_t sb[kPgFillChunks];  // first record of the chunk's run of partition p
+  __shared__ uint32_t sn[kPgFillChunks];  // its length
   __shared__ uint32_t s_item;
-  const uint32_t tid = threadIdx.x;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t nblk = (pl.nchunks + kPgFillChunks - 1) / kPgFillChunks;
   const uint32_t items = nblk * pl.nparts;
   V* vals = static_cast<V*>(pl.vals);
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_d = policy_evict_last();
+  constexpr int kR = 4;  // runs a warp walks side by side (independent loads in flight per lane)
+  static_assert(kPgFillChunks % (8 * kR) == 0, "8 warps x kR runs per pass");
   for (;;) {
     if (tid == 0) s_item = atomicAdd(&pl.ctrl->items, 1u);
     __syncthreads();
@@ -753,48 +758,38 @@ __global__ void __launch_bounds__(256)
         b = c * kPgChunkRows + st;
       }
       sb[tid] = b;
-      const int lane = tid & 31;
-      uint32_t inc = n;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
-      }
-      soff[tid + 1] = inc;  // warp-local inclusive; the second warp is offset below
+      sn[tid] = n;
     }
     __syncthreads();
-    if (tid >= 32 && tid < kPgFillChunks) soff[tid + 1] += soff[32];
-    if (tid == 0) soff[0] = 0;
-    __syncthreads();
-    const uint32_t total = soff[kPgFillChunks];
-    for (uint32_t i0 = 0; i0 < total; i0 += 4 * 256) {
-      uint32_t pos[4], key[4];
+    // The runs of one partition in neighbouring chunks have similar lengths: a warp walks kR
+    // of them in step, 32 records of each per iteration (coalesced key loads and record
+    // stores, no search for a record's run).
+#pragma unroll 1
+    for (int j0 = w * kR; j0 < kPgFillChunks; j0 += 8 * kR) {
+      uint32_t b[kR], n[kR], nmax = 0;
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const uint32_t i = i0 + r * 256 + tid;
-        pos[r] = 0xffffffffu;
-        if (i < total) {
-          uint32_t lo = 0, hi = kPgFillChunks;  // soff[lo] <= i < soff[hi]
-#pragma unroll
-          for (int st = 0; st < 6; ++st) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (soff[mid] <= i) lo = mid; else hi = mid;
-          }
-          pos[r] = sb[lo] + (i - soff[lo]);
-          key[r] = ld_stream_u32(pl.keys + pos[r], pol_s);
-        }
+      for (int r = 0; r < kR; ++r) {
+        b[r] = sb[j0 + r];
+        n[r] = sn[j0 + r];
+        nmax = max(nmax, n[r]);
       }
-      // the slice must outlive the record streams in L2: evict_last loads (L1-allocating:
-      // the hot ids of a scattered skewed column repeat), streaming stores
-      V v[4];
+      for (uint32_t i = lane; i - lane < nmax; i += 32) {
+        uint32_t key[kR];
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
-        if (pos[r] != 0xffffffffu) v[r] = ld_dim<V>(dim + key[r], pol_d, true);
+        for (int r = 0; r < kR; ++r)
+          if (i < n[r]) key[r] = ld_stream_u32(pl.keys + b[r] + i, pol_s);
+        // the slice must outlive the record streams in L2: evict_last loads (L1-allocating:
+        // the hot ids of a scattered skewed column repeat), streaming stores
+        V v[kR];
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
-        if (pos[r] != 0xffffffffu) __stcs(vals + pos[r], v[r]);
+        for (int r = 0; r < kR; ++r)
+          if (i < n[r]) v[r] = ld_dim<V>(dim + key[r], pol_d, true);
+#pragma unroll
+        for (int r = 0; r < kR; ++r)
+          if (i < n[r]) __stcs(vals + b[r] + i, v[r]);
+      }
     }
-    __syncthreads();  // sb / soff / s_item are rewritten for the next item
+    __syncthreads();  // sb / sn / s_item are rewritten for the next item
   }
 }
 
@@ -1091,7 +1086,7 @@ int pgather_impl(skx_ctx* ctx, const uint32_t* fact, uint64_t head, uint64_t nve
     pl.vals = sp + 256 + ends_b + keys_b + tr_b;
     k_pg_arm<<<1, 1, 0, s>>>(pl.ctrl);
     k_pg_part<<<grid_for(ctx, nchunks, 1, 2), kPgT, kPgPartSmem, s>>>(fv, head, nvec, pl, ctx->err);
-    k_pg_fill<V><<<grid_for(ctx, (uint64_t)pl.nparts * nchunks, kPgFillChunks, 8), 256, 0, s>>>(
+    k_pg_fill<V><<<grid_for(ctx, (uint64_t)pl.nparts * nchunks, kPgFillChunks, SKX_PG_FILL_CTAS), 256, 0, s>>>(
         dim, pl);
 #if SKX_PG_EMIT_STAGED
     constexpr int kEmitSmem = (int)(kPgChunkRows * sizeof(V)) + 16;
