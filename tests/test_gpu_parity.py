@@ -889,3 +889,79 @@ def test_scratch_reserve_and_graph_capture(sx, oracle):
     ctx.sync(sp)
     eo, er = oracle.build_index(oracle.count_frequencies(fact_np, d), n)
     assert np.array_equal(np_(off), eo) and np.array_equal(np_(rk), er)
+
+
+def test_gather_plan_in_graph_capture_and_two_streams(sx):
+    """The gather's plan cache stays out of captured graphs (a captured launch
+    over a partition-eligible column is the one-pass kernel alone: no plan
+    kernel, no copy, no event), a forced partitioned launch captures once its
+    scratch is reserved, and two streams of one context plan and follow their
+    own columns independently."""
+    import ctypes as C
+    ctx = sx.context(0)
+    rng = np.random.default_rng(21)
+    d = (96 << 20) // 8                      # 96 MiB int64 dimension: eligible (> 2 x 32 MB)
+    n = 1 << 23
+    dim_np = rng.integers(0, 2**62, size=d, dtype=np.int64)
+    dim = cu(dim_np)
+    fact_np = rng.integers(1, d + 1, size=n, dtype=np.uint32)
+    fact = cu(fact_np)
+    exp = dim_np[fact_np.astype(np.int64) - 1]
+    out = torch.empty(n, dtype=torch.int64, device="cuda")
+    s = torch.cuda.Stream()
+    sp = C.c_void_p(s.cuda_stream)
+
+    def gather(stream_ptr, f=fact, o=out):
+        ctx.check(ctx.lib.skx_gather_u64(ctx.handle, C.c_void_p(f.data_ptr()), f.numel(),
+                                         C.c_void_p(dim.data_ptr()), d, C.c_void_p(o.data_ptr()),
+                                         stream_ptr))
+    try:
+        ctx.set_gather_policy(129 | 8192)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        before = ctx.launches()
+        with torch.cuda.graph(g, stream=s):
+            gather(sp)
+        assert ctx.launches() - before == 1              # the one-pass kernel, nothing else
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(np_(out), exp)
+        # forced path: the records' scratch must exist before the capture
+        ctx.set_gather_policy(129 | 8192 | 16384)
+        ctx.check(ctx.lib.skx_reserve(ctx.handle, 1, 256 + (n // 8192 + 1) * 64 + n * 16 + 4096, sp))
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2, stream=s):
+            gather(sp)
+        for _ in range(2):
+            out.zero_()
+            g2.replay()
+            torch.cuda.synchronize()
+            assert np.array_equal(np_(out), exp)
+        # two streams, two columns: uniform ids (partitioned from the second launch on) and
+        # hot-only ids (one pass), interleaved
+        ctx.set_gather_policy(129 | 8192)
+        s2 = torch.cuda.Stream()
+        sp2 = C.c_void_p(s2.cuda_stream)
+        hot_np = rng.integers(1, 1000, size=n, dtype=np.uint32)
+        hot = cu(hot_np)
+        out2 = torch.empty_like(out)
+        exp2 = dim_np[hot_np.astype(np.int64) - 1]
+        torch.cuda.synchronize()
+        for rep in range(3):
+            out.zero_()
+            out2.zero_()
+            torch.cuda.synchronize()
+            gather(sp)
+            gather(sp2, hot, out2)
+            p2 = ctx.gather_last_plan(sp2)
+            torch.cuda.synchronize()
+            assert np.array_equal(np_(out), exp) and np.array_equal(np_(out2), exp2), rep
+            assert not p2["partitioned"] and not p2["plan_partitioned"]
+        gather(sp)
+        p1 = ctx.gather_last_plan(sp)
+        assert p1["partitioned"] and p1["plan_partitioned"]
+        ctx.sync(sp)
+        ctx.sync(sp2)
+    finally:
+        ctx.set_gather_policy(129 | 8192)
